@@ -1,0 +1,162 @@
+/*
+ * gids.h -- C ABI of the B200 GIDS dataloader hot path (libgids.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Device pointers are raw
+ * CUDA device addresses (e.g. torch.Tensor.data_ptr() of a cuda tensor);
+ * streams are cudaStream_t passed as void* (0 = legacy default stream).
+ * Every entry point returns 0 on success and a negative GIDS_E_* code on
+ * failure; gids_last_error() then holds a message.  A handle is bound to
+ * one device and is not thread-safe (the reference is single-writer,
+ * SPEC.md:386,468).
+ *
+ * Each entry point names the reference interface it replaces, relative to
+ * /root/reference/pkg/src/tierloader/.  The Python side that calls this ABI
+ * (paper_2306_16384_b200/) keeps those interfaces' names, argument meaning
+ * and exceptions; see INTEGRATION.md for the binding.
+ */
+#ifndef GIDS_H_
+#define GIDS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GIDS_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define GIDS_API __attribute__((visibility("default")))
+#else
+#define GIDS_API
+#endif
+
+enum {
+    GIDS_OK = 0,
+    GIDS_E_INVALID = -1,   /* bad argument (maps to ValueError) */
+    GIDS_E_CUDA = -2,      /* CUDA runtime failure */
+    GIDS_E_CAPACITY = -3,  /* a workspace bound was exceeded */
+    GIDS_E_STATE = -4      /* call out of protocol order (CacheProtocolError) */
+};
+
+enum { GIDS_POLICY_EXACT = 0, GIDS_POLICY_SETASSOC = 1 };
+enum { GIDS_KIND_HIT = 0, GIDS_KIND_MISS = 1, GIDS_KIND_BYPASS = 2 };
+
+#define GIDS_MAX_LAYERS 8
+
+typedef struct gids_handle gids_handle;
+
+typedef struct {
+    int64_t num_nodes;        /* N (< 2^31) */
+    int64_t num_edges;        /* E */
+    int32_t feature_dim;      /* fp32 columns per row */
+    int32_t device;           /* CUDA ordinal */
+    int64_t cache_lines;      /* capacity in rows: PipelineConfig.resolved_cache_lines() */
+    int32_t policy;           /* GIDS_POLICY_* */
+    int32_t ways;             /* set-associative ways (32) */
+    uint64_t evict_key;       /* set-associative eviction draw key */
+    int32_t window_depth;     /* W (<= 255) */
+    int32_t n_layers;         /* len(fanouts) */
+    int32_t fanouts[GIDS_MAX_LAYERS];
+    int64_t max_seeds;        /* largest batch the workspace must hold */
+} gids_config;
+
+/* per-batch tier split, as IterationStats counts it (dataloader.py:48-63) */
+typedef struct {
+    int64_t sampled, cache_hits, cpu_buffer_hits, storage, bypasses;
+} gids_tier_counts;
+
+/* CacheState counters (cache.py:104-113,182-187) */
+typedef struct {
+    int64_t hits, misses, bypasses, evictions, total_increments, total_decrements;
+    int64_t safe_count, filled;
+} gids_cache_counters;
+
+GIDS_API int gids_abi_version(void);
+GIDS_API const char* gids_last_error(void);
+
+/* Dataloader.__init__ device-side setup (dataloader.py:98-159).
+ * Allocates the HBM cache (cache.py:94-113: CacheState + _cache_rows) and
+ * the per-node metadata.  eviction_rng: the 6-word PCG64 state of
+ * default_rng(evict_seed) (cache.py:108), word order
+ * [state_hi, state_lo, inc_hi, inc_lo, has_uint32, uinteger]. */
+GIDS_API int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_handle** out);
+GIDS_API int gids_destroy(gids_handle* h);
+
+/* GraphCsc (graph.py:46-71): host indptr u64[N+1] / indices u64[E] are
+ * copied into HBM (indices narrowed to int32; N < 2^31 is checked). */
+GIDS_API int gids_load_graph(gids_handle* h, const uint64_t* indptr, const uint64_t* indices);
+
+/* FeatureStore rows (graph.py:278-301) as the storage tier: a pinned or
+ * registrable host table of n_rows x feature_dim fp32, read zero-copy. */
+GIDS_API int gids_set_backing(gids_handle* h, const float* table_host, int64_t n_rows);
+
+/* ConstantBuffer (cpu_buffer.py:77-138): node_ids in pin order and their
+ * rows (host, pinned or registrable); rows are read zero-copy. */
+GIDS_API int gids_set_constant_buffer(gids_handle* h, const int64_t* node_ids, int64_t k,
+                             const float* rows_host);
+
+/* sample_subgraph (sampler.py:87-112) into the handle's workspace.
+ * seeds: host int64[n_seeds] (validated by the caller as sampler.py:91-96
+ * does).  rng: 6-word PCG64 state of the sampler Generator at call time;
+ * the draws are taken by per-node jump-ahead from it, so the caller
+ * advances its Generator by the `draws` gids_sample_sizes reports
+ * (rng.bit_generator.advance(draws)) to stay in step with the reference. */
+GIDS_API int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds,
+                const uint64_t rng[6], void* stream);
+
+/* Sizes of the last gids_sample (synchronises the stream):
+ * layer_len[n_layers], n_unique, draws (doubles consumed), and the run-ahead
+ * contribution of the batch against the current cache
+ * (dataloader.py:188-192). */
+GIDS_API int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique,
+                      int64_t* draws, int64_t* contribution);
+
+/* Copy the last sample out: edges as the layers' (E_l,2) int64 [src,dst]
+ * arrays back to back; unique_nodes int64[U] ascending.  Device pointers. */
+GIDS_API int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, void* stream);
+
+/* WindowBuffer.push_iteration / pop_iteration (cache.py:66-91) for an
+ * ascending unique device list. */
+GIDS_API int gids_window_push(gids_handle* h, const int64_t* nodes_dev, int64_t n, void* stream);
+GIDS_API int gids_window_pop(gids_handle* h, const int64_t* nodes_dev, int64_t n, void* stream);
+
+/* One served batch (dataloader.py:248-290): window_update (cache.py:190-218),
+ * per-node CacheState.access in ascending order (cache.py:144-180) or the
+ * set-associative policy, tier chain, gather into out_dev (U x dim fp32,
+ * ascending unique order) and cache insertion.  epoch keys the
+ * set-associative eviction draws. */
+GIDS_API int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
+               float* out_dev, void* stream);
+
+/* Tier counts of the last gids_serve (synchronises the stream). */
+GIDS_API int gids_serve_counts(gids_handle* h, gids_tier_counts* out);
+
+/* Per-node decisions of the last gids_serve: kind int8[U] (GIDS_KIND_*) and
+ * line int64[U] (-1 on bypass).  Device pointers. */
+GIDS_API int gids_serve_decisions(gids_handle* h, int8_t* kind_dev, int64_t* line_dev, void* stream);
+
+GIDS_API int gids_cache_stats(gids_handle* h, gids_cache_counters* out);       /* synchronises */
+GIDS_API int gids_cache_rng(gids_handle* h, uint64_t words_out[6]);          /* exact-policy RNG */
+/* line table snapshot: node int64[L] (-1 empty), state int8[L] (0 empty,
+ * 1 SafeToEvict, 2 InUse) -- LineState (cache.py:38-41).  Host pointers. */
+GIDS_API int gids_cache_lines(gids_handle* h, int64_t* node_host, int8_t* state_host);
+GIDS_API int64_t gids_cache_capacity(gids_handle* h);
+
+/* Synthetic feature rows (graph.py:256-275) written by the GPU straight into
+ * a host (pinned) or device table: rows [row0, row0+n) of an N x dim table. */
+GIDS_API int gids_synthesize_rows(int device, uint64_t seed, int64_t row0, int64_t n, int32_t dim,
+                         float* dst, void* stream);
+
+/* Verify gathered rows against the synthetic formula (verify_gather,
+ * dataloader.py:291-294); returns the mismatching row count in *bad. */
+GIDS_API int gids_verify_rows(int device, uint64_t seed, const int64_t* nodes_dev, int64_t n, int32_t dim,
+                     const float* rows_dev, int64_t* bad, void* stream);
+
+/* Kernel launches issued by this handle since creation (evidence counter). */
+GIDS_API int64_t gids_launch_count(gids_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIDS_H_ */

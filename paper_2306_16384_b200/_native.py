@@ -1,0 +1,258 @@
+"""ctypes binding of libgids.so (include/gids.h).
+
+The CUDA library is the only compute path: if it is missing this module
+raises ImportError with the build command instead of falling back to any
+CPU implementation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libgids.so"
+ABI_VERSION = 1
+MAX_LAYERS = 8
+
+OK, E_INVALID, E_CUDA, E_CAPACITY, E_STATE = 0, -1, -2, -3, -4
+POLICY_EXACT, POLICY_SETASSOC = 0, 1
+KIND_HIT, KIND_MISS, KIND_BYPASS = 0, 1, 2
+
+
+class GidsConfig(C.Structure):
+    _fields_ = [("num_nodes", C.c_int64), ("num_edges", C.c_int64),
+                ("feature_dim", C.c_int32), ("device", C.c_int32),
+                ("cache_lines", C.c_int64), ("policy", C.c_int32), ("ways", C.c_int32),
+                ("evict_key", C.c_uint64), ("window_depth", C.c_int32),
+                ("n_layers", C.c_int32), ("fanouts", C.c_int32 * MAX_LAYERS),
+                ("max_seeds", C.c_int64)]
+
+
+class TierCounts(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in
+                ("sampled", "cache_hits", "cpu_buffer_hits", "storage", "bypasses")]
+
+
+class CacheCounters(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in
+                ("hits", "misses", "bypasses", "evictions", "total_increments",
+                 "total_decrements", "safe_count", "filled")]
+
+
+class GidsError(RuntimeError):
+    """A CUDA-side failure of the GIDS library."""
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"GIDS CUDA library not built ({LIB_PATH}); run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` or "
+            "`make -C paper_2306_16384_b200/csrc`")
+    L = C.CDLL(str(LIB_PATH))
+    vp, i64, u64, i32 = C.c_void_p, C.c_int64, C.c_uint64, C.c_int32
+    sig = {
+        "gids_abi_version": ([], C.c_int),
+        "gids_last_error": ([], C.c_char_p),
+        "gids_create": ([C.POINTER(GidsConfig), vp, C.POINTER(vp)], C.c_int),
+        "gids_destroy": ([vp], C.c_int),
+        "gids_load_graph": ([vp, vp, vp], C.c_int),
+        "gids_set_backing": ([vp, vp, i64], C.c_int),
+        "gids_set_constant_buffer": ([vp, vp, i64, vp], C.c_int),
+        "gids_sample": ([vp, vp, i64, vp, vp], C.c_int),
+        "gids_sample_sizes": ([vp, vp, vp, vp, vp], C.c_int),
+        "gids_sample_export": ([vp, vp, vp, vp], C.c_int),
+        "gids_window_push": ([vp, vp, i64, vp], C.c_int),
+        "gids_window_pop": ([vp, vp, i64, vp], C.c_int),
+        "gids_serve": ([vp, vp, i64, u64, vp, vp], C.c_int),
+        "gids_serve_counts": ([vp, C.POINTER(TierCounts)], C.c_int),
+        "gids_serve_decisions": ([vp, vp, vp, vp], C.c_int),
+        "gids_cache_stats": ([vp, C.POINTER(CacheCounters)], C.c_int),
+        "gids_cache_rng": ([vp, vp], C.c_int),
+        "gids_cache_lines": ([vp, vp, vp], C.c_int),
+        "gids_cache_capacity": ([vp], i64),
+        "gids_synthesize_rows": ([i32, u64, i64, i64, i32, vp, vp], C.c_int),
+        "gids_verify_rows": ([i32, u64, vp, i64, i32, vp, vp, vp], C.c_int),
+        "gids_launch_count": ([vp], i64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    if L.gids_abi_version() != ABI_VERSION:
+        raise ImportError("libgids.so ABI version mismatch; rebuild it")
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    """Every entry point include/gids.h declares (checked by the CPU tests)."""
+    return ["gids_abi_version", "gids_last_error", "gids_create", "gids_destroy",
+            "gids_load_graph", "gids_set_backing", "gids_set_constant_buffer", "gids_sample",
+            "gids_sample_sizes", "gids_sample_export", "gids_window_push", "gids_window_pop",
+            "gids_serve", "gids_serve_counts", "gids_serve_decisions", "gids_cache_stats",
+            "gids_cache_rng", "gids_cache_lines", "gids_cache_capacity",
+            "gids_synthesize_rows", "gids_verify_rows", "gids_launch_count"]
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == OK:
+        return
+    msg = lib().gids_last_error().decode(errors="replace")
+    if rc == E_INVALID:
+        raise ValueError(msg)
+    if rc == E_STATE:
+        from .feature_cache import CacheProtocolError
+        raise CacheProtocolError(msg)
+    raise GidsError(f"{what}: {msg}" if what else msg)
+
+
+def _p(a) -> int:
+    """Raw address of a numpy array or a torch tensor."""
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    return a.data_ptr()
+
+
+def stream_ptr(device: int = 0) -> int:
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Handle:
+    """One gids_handle: device-resident graph, cache and workspaces."""
+
+    def __init__(self, *, num_nodes, num_edges, feature_dim, device, cache_lines, policy,
+                 ways, evict_key, window_depth, fanouts, max_seeds, eviction_words):
+        L = lib()
+        fans = [int(f) for f in fanouts]
+        if not 1 <= len(fans) <= MAX_LAYERS:
+            raise ValueError(f"the CUDA sampler supports 1..{MAX_LAYERS} layers")
+        cfg = GidsConfig()
+        cfg.num_nodes, cfg.num_edges, cfg.feature_dim = num_nodes, num_edges, feature_dim
+        cfg.device, cfg.cache_lines = device, cache_lines
+        cfg.policy = POLICY_SETASSOC if policy == "setassoc" else POLICY_EXACT
+        cfg.ways, cfg.evict_key, cfg.window_depth = ways, evict_key, window_depth
+        cfg.n_layers = len(fans)
+        for i, f in enumerate(fans):
+            cfg.fanouts[i] = f
+        cfg.max_seeds = max_seeds
+        self.cfg = cfg
+        self.device = device
+        self.n_layers = len(fans)
+        self.dim = feature_dim
+        words = np.ascontiguousarray(eviction_words, dtype=np.uint64)
+        h = C.c_void_p()
+        check(L.gids_create(C.byref(cfg), words.ctypes.data, C.byref(h)), "gids_create")
+        self.h = h
+        self._keep = []  # host arrays the library reads zero-copy
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            lib().gids_destroy(self.h)
+            self.h = None
+            self._keep = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- setup
+    def load_graph(self, indptr: np.ndarray, indices: np.ndarray) -> None:
+        ip = np.ascontiguousarray(indptr, dtype=np.uint64)
+        ix = np.ascontiguousarray(indices, dtype=np.uint64)
+        check(lib().gids_load_graph(self.h, ip.ctypes.data, ix.ctypes.data), "load_graph")
+
+    def set_backing(self, table, n_rows: int) -> None:
+        self._keep.append(table)
+        check(lib().gids_set_backing(self.h, _p(table), n_rows), "set_backing")
+
+    def set_constant_buffer(self, node_ids: np.ndarray, rows) -> None:
+        ids = np.ascontiguousarray(node_ids, dtype=np.int64)
+        if len(ids):
+            self._keep.append(rows)
+        check(lib().gids_set_constant_buffer(self.h, ids.ctypes.data, len(ids),
+                                             _p(rows) if len(ids) else None),
+              "set_constant_buffer")
+
+    # -- sampling
+    def sample(self, seeds: np.ndarray, words: np.ndarray, stream: int) -> None:
+        s = np.ascontiguousarray(seeds, dtype=np.int64)
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        check(lib().gids_sample(self.h, s.ctypes.data, len(s), w.ctypes.data, stream), "sample")
+
+    def sample_sizes(self):
+        lens = np.zeros(self.n_layers, np.int64)
+        nu, dr, co = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib().gids_sample_sizes(self.h, lens.ctypes.data, C.byref(nu), C.byref(dr),
+                                      C.byref(co)), "sample_sizes")
+        return lens, nu.value, dr.value, co.value
+
+    def sample_export(self, edges, unique, stream: int) -> None:
+        check(lib().gids_sample_export(self.h, _p(edges) if edges is not None else None,
+                                       _p(unique) if unique is not None else None, stream),
+              "sample_export")
+
+    # -- window and serving
+    def window_push(self, nodes, stream: int) -> None:
+        check(lib().gids_window_push(self.h, _p(nodes), nodes.numel(), stream), "window_push")
+
+    def window_pop(self, nodes, stream: int) -> None:
+        check(lib().gids_window_pop(self.h, _p(nodes), nodes.numel(), stream), "window_pop")
+
+    def serve(self, unique, epoch: int, out, stream: int) -> None:
+        check(lib().gids_serve(self.h, _p(unique), unique.numel(), epoch, _p(out), stream),
+              "serve")
+
+    def serve_counts(self) -> TierCounts:
+        t = TierCounts()
+        check(lib().gids_serve_counts(self.h, C.byref(t)), "serve_counts")
+        return t
+
+    def serve_decisions(self, kind, line, stream: int) -> None:
+        check(lib().gids_serve_decisions(self.h, _p(kind), _p(line), stream), "serve_decisions")
+
+    def cache_stats(self) -> CacheCounters:
+        c = CacheCounters()
+        check(lib().gids_cache_stats(self.h, C.byref(c)), "cache_stats")
+        return c
+
+    def cache_rng(self) -> np.ndarray:
+        w = np.zeros(6, np.uint64)
+        check(lib().gids_cache_rng(self.h, w.ctypes.data), "cache_rng")
+        return w
+
+    def cache_lines(self):
+        n = self.capacity()
+        node = np.zeros(max(n, 1), np.int64)
+        st = np.zeros(max(n, 1), np.int8)
+        check(lib().gids_cache_lines(self.h, node.ctypes.data, st.ctypes.data), "cache_lines")
+        return node[:n], st[:n]
+
+    def capacity(self) -> int:
+        return int(lib().gids_cache_capacity(self.h))
+
+    def launch_count(self) -> int:
+        return int(lib().gids_launch_count(self.h))
+
+
+def synthesize_rows(device: int, seed: int, row0: int, n: int, dim: int, dst, stream: int) -> None:
+    check(lib().gids_synthesize_rows(device, seed & ((1 << 64) - 1), row0, n, dim, _p(dst),
+                                     stream), "synthesize_rows")
+
+
+def verify_rows(device: int, seed: int, nodes, rows, stream: int) -> int:
+    bad = C.c_int64()
+    check(lib().gids_verify_rows(device, seed & ((1 << 64) - 1), _p(nodes), nodes.numel(),
+                                 rows.shape[1], _p(rows), C.byref(bad), stream), "verify_rows")
+    return bad.value

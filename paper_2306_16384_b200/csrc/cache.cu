@@ -1,0 +1,546 @@
+// cache.cu -- K3/K4: lookahead-window counters and the HBM software cache.
+//
+// State (all HBM):
+//   slot_of[N]   node -> line (-1)          (CacheState.resident, cache.py:106)
+//   line_node[L] line -> node (-1 empty)    (CacheState.slot_node, cache.py:107)
+//   safe_bits    SafeToEvict bitmap over lines; with 32 ways, word s IS set s
+//   blk_cnt / sup_cnt  safe lines per 1024 / 32768 lines (exact-policy select)
+//   reuse[N]     predicted-reuse counters   (CacheState.reuse_counter)
+//   future[N]    how many lookahead-window lists contain the node; replaces
+//                the sorted-concat + searchsorted of window_update
+//                (cache.py:201-206) by +-1 on push/pop (lists are unique).
+//
+// Serving a batch:
+//   k_window_consume  window_update (cache.py:190-218) fused with the
+//                     per-access reuse consumption (cache.py:121-131): both
+//                     are order-independent per node, so fully parallel.
+//   exact policy      k_exact_seq: the reference CacheState.access sequence
+//                     (cache.py:144-180) in ascending node order on ONE warp,
+//                     tables in shared memory, uniform eviction draws from the
+//                     numpy PCG64 stream; only the order-dependent decisions
+//                     are sequential, the line/node bookkeeping is done after
+//                     in parallel (k_post_*).
+//   set-associative   32-way sets, one warp per set, lanes = ways; the same
+//                     contract per set with a counter-based eviction draw.
+#include "gids_internal.cuh"
+
+namespace {
+
+constexpr int BLOCK = 256;
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// ---------------------------------------------------------------- window
+__global__ void k_window(const int64_t* __restrict__ nodes, int64_t n, uint8_t* future,
+                         int delta) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        future[nodes[i]] += (uint8_t)delta;
+}
+
+// run-ahead contribution: unpinned and not resident (dataloader.py:188-192)
+__global__ void k_contribution(const int32_t* __restrict__ uniq, SampleCounters* sc,
+                               const int32_t* __restrict__ pinned_off,
+                               const int32_t* __restrict__ slot_of) {
+    int64_t n = sc->n_unique, c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t x = uniq[i];
+        c += (pinned_off[x] < 0 && slot_of[x] < 0) ? 1 : 0;
+    }
+    c = warp_sum64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd((unsigned long long*)&sc->contribution,
+                                                (unsigned long long)c);
+}
+
+// window_update + reuse consumption; ev[p] = (line_at_start+1)<<1 | (count_after>0)
+__global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
+                                 const uint8_t* __restrict__ future, uint32_t* reuse,
+                                 const int32_t* __restrict__ slot_of, uint32_t* safe_bits,
+                                 uint32_t* blk_cnt, uint32_t* sup_cnt, int exact,
+                                 CacheMeta* meta, uint32_t* ev) {
+    int64_t inc = 0, dec = 0, unsafe = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t x = (int32_t)uniq[p];
+        uint32_t c = future[x];
+        uint32_t old = reuse[x];
+        uint32_t now = old + c;
+        int32_t s = slot_of[x];
+        if (c > 0) {
+            inc += c;
+            if (old == 0 && s >= 0) {
+                uint32_t bit = 1u << (s & 31);
+                if (safe_bits[s >> 5] & bit) {  // resident SafeToEvict -> InUse
+                    atomicAnd(&safe_bits[s >> 5], ~bit);
+                    if (exact) {
+                        atomicSub(&blk_cnt[s >> 10], 1u);
+                        atomicSub(&sup_cnt[s >> 15], 1u);
+                    }
+                    unsafe++;
+                }
+            }
+        }
+        if (now > 0) {
+            now--;
+            dec++;
+        }
+        reuse[x] = now;
+        ev[p] = ((uint32_t)(s + 1) << 1) | (now > 0 ? 1u : 0u);
+    }
+    inc = warp_sum64(inc);
+    dec = warp_sum64(dec);
+    unsafe = warp_sum64(unsafe);
+    if ((threadIdx.x & 31) == 0) {
+        if (inc) atomicAdd((unsigned long long*)&meta->inc, (unsigned long long)inc);
+        if (dec) atomicAdd((unsigned long long*)&meta->dec, (unsigned long long)dec);
+        if (unsafe) atomicAdd((unsigned long long*)&meta->safe_count, (unsigned long long)(-unsafe));
+    }
+}
+
+// ----------------------------------------------------------- exact policy
+struct ExactTables {
+    uint32_t* safe;   // [nw]
+    uint32_t* evict;  // [nw]
+    uint32_t* blk;    // [nb]
+    uint32_t* sup;    // [ns]
+};
+
+// lane-cooperative search: index of the entry holding the r-th unit among
+// cnt[0..m); r is reduced to the rank inside that entry
+__device__ __forceinline__ int64_t warp_find(const uint32_t* cnt, int64_t m, uint32_t& r) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t base = 0; base < m; base += 32) {
+        uint32_t c = base + lane < m ? cnt[base + lane] : 0u;
+        uint32_t inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
+        }
+        uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        if (r < total) {
+            unsigned m2 = __ballot_sync(0xffffffffu, inc > r);
+            int f = __ffs(m2) - 1;
+            uint32_t excl = __shfl_sync(0xffffffffu, inc - c, f);
+            r -= excl;
+            return base + f;
+        }
+        r -= total;
+    }
+    return -1;  // unreachable when r < total safe lines
+}
+
+// r-th SafeToEvict line in ascending line order (np.flatnonzero(mask)[r])
+__device__ __forceinline__ int64_t select_safe(const ExactTables& t, int64_t nw, int64_t nb,
+                                               int64_t ns, uint32_t r) {
+    int64_t sb = warp_find(t.sup, ns, r);
+    int64_t b0 = sb * 32;
+    int64_t bsel = b0 + warp_find(t.blk + b0, (nb - b0) < 32 ? (nb - b0) : 32, r);
+    int64_t w0 = bsel * 32;
+    const int lane = threadIdx.x & 31;
+    uint32_t word = w0 + lane < nw ? t.safe[w0 + lane] : 0u;
+    uint32_t c = __popc(word), inc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += u;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, inc > r);
+    int f = __ffs(m) - 1;
+    uint32_t excl = __shfl_sync(0xffffffffu, inc - c, f);
+    uint32_t wsel = __shfl_sync(0xffffffffu, word, f);
+    int bit = __fns(wsel, 0, (int)(r - excl) + 1);
+    return (w0 + f) * 32 + bit;
+}
+
+__device__ __forceinline__ void tab_set_safe(const ExactTables& t, int64_t s) {
+    t.safe[s >> 5] |= 1u << (s & 31);
+    t.blk[s >> 10]++;
+    t.sup[s >> 15]++;
+}
+__device__ __forceinline__ void tab_clear_safe(const ExactTables& t, int64_t s) {
+    t.safe[s >> 5] &= ~(1u << (s & 31));
+    t.blk[s >> 10]--;
+    t.sup[s >> 15]--;
+}
+
+__global__ void __launch_bounds__(32, 1)
+k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* meta,
+            uint32_t* g_safe, uint32_t* g_evict, uint32_t* g_blk, uint32_t* g_sup, int smem_bits,
+            int8_t* __restrict__ kind, int32_t* __restrict__ line, int32_t* __restrict__ log_line,
+            int32_t* __restrict__ log_pos, ServeCounters* svc) {
+    extern __shared__ uint32_t sm[];
+    const int lane = threadIdx.x;
+    const int64_t nw = (L + 31) / 32, nb = (L + 1023) / 1024, ns = (L + 32767) / 32768;
+    ExactTables t;
+    uint32_t* p = sm;
+    t.blk = p;
+    p += nb;
+    t.sup = p;
+    p += ns;
+    if (smem_bits) {
+        t.safe = p;
+        p += nw;
+        t.evict = p;
+    } else {
+        t.safe = g_safe;
+        t.evict = g_evict;
+    }
+    for (int64_t i = lane; i < nb; i += 32) t.blk[i] = g_blk[i];
+    for (int64_t i = lane; i < ns; i += 32) t.sup[i] = g_sup[i];
+    if (smem_bits)
+        for (int64_t i = lane; i < nw; i += 32) {
+            t.safe[i] = g_safe[i];
+            t.evict[i] = 0u;
+        }
+    __syncwarp();
+
+    Pcg64 g = {u128{meta->rng[1], meta->rng[0]}, u128{meta->rng[3], meta->rng[2]},
+               (uint32_t)meta->rng[4], (uint32_t)meta->rng[5]};
+    int64_t fill = meta->fill, safe_count = meta->safe_count;
+    int64_t hits = 0, misses = 0, byp = 0, evs = 0, nlog = 0;
+
+    for (int64_t base = 0; base < n; base += 32) {
+        uint32_t my_ev = base + lane < n ? ev[base + lane] : 0u;
+        int my_kind = GIDS_KIND_BYPASS, my_line = -1;
+        int cnt = n - base < 32 ? (int)(n - base) : 32;
+        for (int k = 0; k < cnt; k++) {
+            uint32_t e = __shfl_sync(0xffffffffu, my_ev, k);
+            int64_t s = (int64_t)(e >> 1) - 1;
+            bool inuse = e & 1u;
+            int kd, ln;
+            if (s >= 0 && !((t.evict[s >> 5] >> (s & 31)) & 1u)) {
+                kd = GIDS_KIND_HIT;
+                ln = (int)s;
+                hits++;
+                if (!inuse && !((t.safe[s >> 5] >> (s & 31)) & 1u)) {  // InUse -> Safe
+                    if (lane == 0) tab_set_safe(t, s);
+                    safe_count++;
+                }
+            } else if (fill < L) {
+                kd = GIDS_KIND_MISS;
+                ln = (int)fill++;
+                misses++;
+                if (!inuse) {
+                    if (lane == 0) tab_set_safe(t, ln);
+                    safe_count++;
+                }
+            } else if (safe_count > 0) {
+                uint32_t r = pcg_bounded32(g, (uint32_t)safe_count);
+                int64_t v = select_safe(t, nw, nb, ns, r);
+                kd = GIDS_KIND_MISS;
+                ln = (int)v;
+                misses++;
+                evs++;
+                if (lane == 0) {
+                    t.evict[v >> 5] |= 1u << (v & 31);
+                    if (inuse) tab_clear_safe(t, v);
+                }
+                if (inuse) safe_count--;
+            } else {
+                kd = GIDS_KIND_BYPASS;
+                ln = -1;
+                byp++;
+            }
+            __syncwarp();
+            if (lane == k) {
+                my_kind = kd;
+                my_line = ln;
+            }
+        }
+        if (lane < cnt) {
+            kind[base + lane] = (int8_t)my_kind;
+            line[base + lane] = my_line;
+        }
+        unsigned mm = __ballot_sync(0xffffffffu, lane < cnt && my_kind == GIDS_KIND_MISS);
+        if (lane < cnt && my_kind == GIDS_KIND_MISS) {
+            int64_t at = nlog + __popc(mm & ((1u << lane) - 1u));
+            log_line[at] = my_line;
+            log_pos[at] = (int32_t)(base + lane);
+        }
+        nlog += __popc(mm);
+    }
+    __syncwarp();
+    for (int64_t i = lane; i < nb; i += 32) g_blk[i] = t.blk[i];
+    for (int64_t i = lane; i < ns; i += 32) g_sup[i] = t.sup[i];
+    if (smem_bits)
+        for (int64_t i = lane; i < nw; i += 32) g_safe[i] = t.safe[i];
+    if (lane == 0) {
+        meta->rng[0] = g.state.hi;
+        meta->rng[1] = g.state.lo;
+        meta->rng[4] = g.has32;
+        meta->rng[5] = g.buf32;
+        meta->fill = fill;
+        meta->safe_count = safe_count;
+        meta->hits += hits;
+        meta->misses += misses;
+        meta->bypasses += byp;
+        meta->evictions += evs;
+        svc->n_log = nlog;
+    }
+}
+
+// post-pass A: drop every displaced occupant and every inserted node from
+// slot_of, and find each line's final inserter of this batch
+__global__ void k_post_a(const int64_t* __restrict__ uniq, const ServeCounters* svc,
+                         const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
+                         const int32_t* __restrict__ line_node, int32_t* slot_of, int32_t* last_ins,
+                         uint32_t* g_evict, int clear_evict) {
+    int64_t n = svc->n_log;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t t = log_line[i];
+        int32_t o = line_node[t];
+        if (o >= 0) slot_of[o] = -1;
+        slot_of[uniq[log_pos[i]]] = -1;
+        atomicMax(&last_ins[t], (int32_t)i);
+        if (clear_evict) g_evict[t >> 5] = 0u;
+    }
+}
+// post-pass B: the final inserter owns the line
+__global__ void k_post_b(const int64_t* __restrict__ uniq, const ServeCounters* svc,
+                         const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
+                         int32_t* line_node, int32_t* slot_of, const int32_t* __restrict__ last_ins) {
+    int64_t n = svc->n_log;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t t = log_line[i];
+        if (last_ins[t] == (int32_t)i) {
+            int32_t x = (int32_t)uniq[log_pos[i]];
+            slot_of[x] = t;
+            line_node[t] = x;
+        }
+    }
+}
+__global__ void k_post_c(const ServeCounters* svc, const int32_t* __restrict__ log_line,
+                         int32_t* last_ins) {
+    int64_t n = svc->n_log;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        last_ins[log_line[i]] = -1;
+}
+
+// ------------------------------------------------- set-associative policy
+__device__ __forceinline__ int64_t sa_set_of(int64_t node, int64_t sets) {
+    return (int64_t)__umul64hi(mix64((uint64_t)node), (uint64_t)sets);
+}
+__device__ __forceinline__ uint32_t sa_draw(uint64_t key, uint64_t epoch, int64_t node,
+                                            uint32_t n) {
+    uint64_t h = mix64(key ^ mix64(epoch * 0xD1B54A32D192ED03ULL + (uint64_t)node));
+    return (uint32_t)(((uint64_t)(uint32_t)(h >> 32) * n) >> 32);
+}
+
+__global__ void k_sa_hist(const int64_t* __restrict__ uniq, int64_t n, int64_t sets,
+                          int32_t* set_cnt) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&set_cnt[sa_set_of(uniq[p], sets)], 1);
+}
+__global__ void k_sa_scatter(const int64_t* __restrict__ uniq, int64_t n, int64_t sets,
+                             const int64_t* __restrict__ set_off, int32_t* set_cur,
+                             int32_t* bucket) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int64_t s = sa_set_of(uniq[p], sets);
+        bucket[set_off[s] + atomicAdd(&set_cur[s], 1)] = (int32_t)p;
+    }
+}
+
+constexpr int SA_WARPS = BLOCK / 32;
+constexpr int SA_SORT_MAX = 256;  // bucket entries sorted in registers
+
+__global__ void __launch_bounds__(BLOCK)
+k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, int64_t sets,
+             const int32_t* __restrict__ set_cnt, const int64_t* __restrict__ set_off,
+             int32_t* bucket, int32_t* line_node, int32_t* slot_of, uint32_t* safe_bits,
+             uint64_t key, uint64_t epoch, int8_t* kind, int32_t* line, CacheMeta* meta) {
+    __shared__ int32_t order[SA_WARPS][SA_SORT_MAX];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int64_t hits = 0, misses = 0, byp = 0, evs = 0;
+    for (int64_t s = (int64_t)blockIdx.x * SA_WARPS + wib; s < sets;
+         s += (int64_t)gridDim.x * SA_WARPS) {
+        const int cnt = set_cnt[s];
+        if (cnt == 0) continue;
+        int32_t* bk = bucket + set_off[s];
+        const bool small = cnt <= SA_SORT_MAX;
+        if (small) {  // rank sort of the bucket's batch positions
+            int32_t e[SA_SORT_MAX / 32];
+            int rank[SA_SORT_MAX / 32];
+#pragma unroll
+            for (int q = 0; q < SA_SORT_MAX / 32; q++) {
+                int idx = lane + 32 * q;
+                e[q] = idx < cnt ? bk[idx] : 0x7fffffff;
+                rank[q] = 0;
+            }
+#pragma unroll
+            for (int q2 = 0; q2 < SA_SORT_MAX / 32; q2++) {
+                if (q2 * 32 >= cnt) break;
+                const int lim = cnt - q2 * 32 < 32 ? cnt - q2 * 32 : 32;
+                for (int jj = 0; jj < lim; jj++) {
+                    int32_t vj = __shfl_sync(0xffffffffu, e[q2], jj);
+#pragma unroll
+                    for (int q = 0; q < SA_SORT_MAX / 32; q++) rank[q] += vj < e[q] ? 1 : 0;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < SA_SORT_MAX / 32; q++)
+                if (lane + 32 * q < cnt) order[wib][rank[q]] = e[q];
+            __syncwarp();
+        }
+        int32_t tag = line_node[s * 32 + lane];
+        uint32_t safe = safe_bits[s];
+        int32_t last = -1;
+        for (int q = 0; q < cnt; q++) {
+            int32_t p;
+            if (small) {
+                p = order[wib][q];
+            } else {  // large bucket: next-smallest position by warp reduction
+                int32_t best = 0x7fffffff;
+                for (int idx = lane; idx < cnt; idx += 32) {
+                    int32_t v = bk[idx];
+                    if (v > last && v < best) best = v;
+                }
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) {
+                    int32_t o = __shfl_xor_sync(0xffffffffu, best, d);
+                    best = o < best ? o : best;
+                }
+                p = best;
+                last = best;
+            }
+            const int32_t x = (int32_t)uniq[p];
+            const bool inuse = ev[p] & 1u;
+            unsigned hm = __ballot_sync(0xffffffffu, tag == x);
+            int kd, ln;
+            if (hm) {
+                int w = __ffs(hm) - 1;
+                kd = GIDS_KIND_HIT;
+                ln = (int)(s * 32 + w);
+                hits++;
+                if (!inuse) safe |= 1u << w;
+            } else {
+                unsigned em = __ballot_sync(0xffffffffu, tag < 0);
+                int w = -1;
+                if (em) {
+                    w = __ffs(em) - 1;
+                } else if (safe) {
+                    uint32_t k = sa_draw(key, epoch, x, (uint32_t)__popc(safe));
+                    w = __fns(safe, 0, (int)k + 1);
+                    int32_t victim = __shfl_sync(0xffffffffu, tag, w);
+                    if (lane == 0) slot_of[victim] = -1;
+                    evs++;
+                }
+                if (w >= 0) {
+                    kd = GIDS_KIND_MISS;
+                    ln = (int)(s * 32 + w);
+                    misses++;
+                    if (lane == w) tag = x;
+                    if (inuse) safe &= ~(1u << w);
+                    else safe |= 1u << w;
+                    if (lane == 0) slot_of[x] = ln;
+                } else {
+                    kd = GIDS_KIND_BYPASS;
+                    ln = -1;
+                    byp++;
+                }
+            }
+            if (lane == 0) {
+                kind[p] = (int8_t)kd;
+                line[p] = ln;
+            }
+        }
+        line_node[s * 32 + lane] = tag;
+        if (lane == 0) safe_bits[s] = safe;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (hits) atomicAdd((unsigned long long*)&meta->hits, (unsigned long long)hits);
+        if (misses) atomicAdd((unsigned long long*)&meta->misses, (unsigned long long)misses);
+        if (byp) atomicAdd((unsigned long long*)&meta->bypasses, (unsigned long long)byp);
+        if (evs) atomicAdd((unsigned long long*)&meta->evictions, (unsigned long long)evs);
+    }
+}
+
+}  // namespace
+
+int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delta,
+                       cudaStream_t st) {
+    if (n == 0) return GIDS_OK;
+    k_window<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(nodes, n, h->future, delta);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
+}
+
+int gids_launch_contribution(gids_handle* h, cudaStream_t st) {
+    k_contribution<<<gids_grid(h->unique_cap, BLOCK, 4 * GIDS_SMS), BLOCK, 0, st>>>(
+        h->unique32, h->sc, h->pinned_off, h->slot_of);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
+}
+
+size_t gids_exact_smem_bytes(int64_t L, bool with_bits) {
+    int64_t nw = (L + 31) / 32, nb = (L + 1023) / 1024, ns = (L + 32767) / 32768;
+    return sizeof(uint32_t) * (size_t)(nb + ns + (with_bits ? 2 * nw : 0));
+}
+
+int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t epoch, float* out,
+                      cudaStream_t st) {
+    const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
+    GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
+    if (n > 0) {
+        k_window_consume<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
+            uniq, n, h->future, h->reuse, h->slot_of, h->safe_bits, h->blk_cnt, h->sup_cnt,
+            exact ? 1 : 0, h->meta, h->ev);
+        GIDS_LAUNCH_CHECK(h);
+        if (exact) {
+            size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
+            if (smem > 48 * 1024)
+                GIDS_CUDA_TRY(cudaFuncSetAttribute(k_exact_seq,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem));
+            k_exact_seq<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits,
+                                             h->evict_bits, h->blk_cnt, h->sup_cnt,
+                                             h->exact_smem ? 1 : 0, h->kind, h->line,
+                                             h->log_line, h->log_pos, h->svc);
+            GIDS_LAUNCH_CHECK(h);
+            int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
+            k_post_a<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
+                                          h->slot_of, h->last_ins, h->evict_bits,
+                                          h->exact_smem ? 0 : 1);
+            GIDS_LAUNCH_CHECK(h);
+            k_post_b<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
+                                          h->slot_of, h->last_ins);
+            GIDS_LAUNCH_CHECK(h);
+            k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
+            GIDS_LAUNCH_CHECK(h);
+        } else if (h->sets > 0) {
+            GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cnt, 0, sizeof(int32_t) * h->sets, st));
+            GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cur, 0, sizeof(int32_t) * h->sets, st));
+            int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
+            k_sa_hist<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_cnt);
+            GIDS_LAUNCH_CHECK(h);
+            int rc = gids_scan_i32_to_i64(h, h->set_cnt, h->sets, h->set_off, st);
+            if (rc) return rc;
+            k_sa_scatter<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_off, h->set_cur, h->bucket);
+            GIDS_LAUNCH_CHECK(h);
+            k_sa_process<<<gids_grid(h->sets, SA_WARPS, 16 * GIDS_SMS), BLOCK, 0, st>>>(
+                uniq, h->ev, h->sets, h->set_cnt, h->set_off, h->bucket, h->line_node, h->slot_of,
+                h->safe_bits, h->cfg.evict_key, epoch, h->kind, h->line, h->meta);
+            GIDS_LAUNCH_CHECK(h);
+        } else {  // zero lines: every access bypasses
+            gids_set_error("set-associative cache without sets");
+            return GIDS_E_STATE;
+        }
+        int rc = gids_launch_gather(h, uniq, n, out, st);
+        if (rc) return rc;
+    }
+    GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
+                                  cudaMemcpyDeviceToHost, st));
+    h->last_serve_n = n;
+    return GIDS_OK;
+}

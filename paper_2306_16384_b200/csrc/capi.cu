@@ -1,0 +1,456 @@
+// capi.cu -- the extern "C" surface declared in include/gids.h.
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "gids_internal.cuh"
+
+static thread_local std::string g_err;
+void gids_set_error(const std::string& msg) { g_err = msg; }
+
+size_t gids_exact_smem_bytes(int64_t L, bool with_bits);
+
+namespace {
+
+template <typename T>
+int dalloc(T** p, int64_t count, cudaStream_t st = 0) {
+    (void)st;
+    size_t bytes = sizeof(T) * (size_t)(count > 0 ? count : 1);
+    cudaError_t e = cudaMalloc((void**)p, bytes);
+    if (e != cudaSuccess) {
+        gids_set_error(std::string("cudaMalloc(") + std::to_string(bytes) + "): " +
+                       cudaGetErrorString(e));
+        return GIDS_E_CUDA;
+    }
+    return GIDS_OK;
+}
+
+#define TRY(x)                \
+    do {                      \
+        int _rc = (x);        \
+        if (_rc) return _rc;  \
+    } while (0)
+
+#define CHECK_H(h)                                            \
+    do {                                                      \
+        if (!(h)) {                                           \
+            gids_set_error("null gids handle");               \
+            return GIDS_E_INVALID;                            \
+        }                                                     \
+        cudaError_t _e = cudaSetDevice((h)->device);          \
+        if (_e != cudaSuccess) {                              \
+            gids_set_error(cudaGetErrorString(_e));           \
+            return GIDS_E_CUDA;                               \
+        }                                                     \
+    } while (0)
+
+// host memory the kernels read zero-copy: pinned already, or register it
+int map_host(const void* p, size_t bytes, bool* registered) {
+    *registered = false;
+    if (!p || bytes == 0) return GIDS_OK;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e == cudaSuccess && (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice ||
+                             a.type == cudaMemoryTypeManaged))
+        return GIDS_OK;
+    cudaGetLastError();
+    GIDS_CUDA_TRY(cudaHostRegister(const_cast<void*>(p), bytes,
+                                   cudaHostRegisterMapped | cudaHostRegisterReadOnly));
+    *registered = true;
+    return GIDS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gids_abi_version(void) { return GIDS_ABI_VERSION; }
+const char* gids_last_error(void) { return g_err.c_str(); }
+
+int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_handle** out) {
+    if (!cfg || !out) {
+        gids_set_error("null argument");
+        return GIDS_E_INVALID;
+    }
+    if (cfg->num_nodes <= 0 || cfg->num_nodes >= (int64_t)1 << 31) {
+        gids_set_error("num_nodes must be in [1, 2^31)");
+        return GIDS_E_INVALID;
+    }
+    if (cfg->feature_dim <= 0 || cfg->n_layers < 1 || cfg->n_layers > GIDS_MAX_LAYERS ||
+        cfg->cache_lines < 0 || cfg->cache_lines >= (int64_t)1 << 30 || cfg->max_seeds < 1 ||
+        cfg->window_depth < 0 || cfg->window_depth > 255) {
+        gids_set_error("invalid gids_config (dim, layers 1..8, lines < 2^30, W <= 255)");
+        return GIDS_E_INVALID;
+    }
+    for (int l = 0; l < cfg->n_layers; l++)
+        if (cfg->fanouts[l] < 1) {
+            gids_set_error("every fanout must be >= 1");
+            return GIDS_E_INVALID;
+        }
+    if (cfg->policy == GIDS_POLICY_SETASSOC && cfg->ways != 32) {
+        gids_set_error("set-associative policy supports 32 ways");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaSetDevice(cfg->device));
+    gids_handle* h = new gids_handle();
+    memset((void*)h, 0, sizeof(gids_handle));
+    h->cfg = *cfg;
+    h->device = cfg->device;
+    h->N = cfg->num_nodes;
+    h->E = cfg->num_edges;
+    h->row_floats = cfg->feature_dim;
+    if (cfg->policy == GIDS_POLICY_SETASSOC) {
+        h->sets = cfg->cache_lines / 32;
+        h->L = h->sets * 32;
+        if (h->L == 0) h->cfg.policy = GIDS_POLICY_EXACT;  // no sets: bypass-only cache
+    } else {
+        h->L = cfg->cache_lines;
+    }
+    const int64_t N = h->N, L = h->L;
+
+    // workspace bounds (sampler.py: every layer edge <= frontier * fanout)
+    h->max_seeds = cfg->max_seeds;
+    int64_t front = cfg->max_seeds < N ? cfg->max_seeds : N, ecap = 0, fcap = front;
+    for (int l = 0; l < cfg->n_layers; l++) {
+        int64_t e = front * cfg->fanouts[l];
+        ecap += e;
+        front = e < N ? e : N;
+        fcap = front > fcap ? front : fcap;
+    }
+    h->edge_cap = ecap > 0 ? ecap : 1;
+    h->front_cap = fcap;
+    h->unique_cap = (cfg->max_seeds + ecap) < N ? (cfg->max_seeds + ecap) : N;
+    h->serve_cap = h->unique_cap;
+
+    int rc = GIDS_OK;
+#define A(ptr, cnt) \
+    if (!rc) rc = dalloc(&(ptr), (cnt))
+    A(h->indptr, N + 1);
+    A(h->indices, h->E > 0 ? h->E : 1);
+    A(h->pinned_off, N);
+    A(h->cache_rows, L * h->row_floats);
+    A(h->slot_of, N);
+    A(h->line_node, L);
+    A(h->safe_bits, ceil_div(L, 32));
+    A(h->evict_bits, ceil_div(L, 32));
+    A(h->blk_cnt, ceil_div(L, 1024));
+    A(h->sup_cnt, ceil_div(L, 32768));
+    A(h->reuse, N);
+    A(h->future, N);
+    A(h->meta, 1);
+    A(h->last_ins, L);
+    A(h->bm_front, ceil_div(N, 32));
+    A(h->bm_all, ceil_div(N, 32));
+    A(h->frontier, h->front_cap);
+    A(h->seeds_dev, h->max_seeds);
+    A(h->take_off, h->front_cap + 1);
+    A(h->draw_off, h->front_cap + 1);
+    A(h->edges, 2 * h->edge_cap);
+    A(h->unique32, h->unique_cap);
+    A(h->jump_tab, 128);
+    A(h->sc, 1);
+    h->scan_parts_cap = 1024;
+    A(h->scan_parts, 2 * h->scan_parts_cap);
+    A(h->word_parts, h->scan_parts_cap);
+    A(h->ev, h->serve_cap);
+    A(h->kind, h->serve_cap);
+    A(h->line, h->serve_cap);
+    A(h->log_line, h->serve_cap);
+    A(h->log_pos, h->serve_cap);
+    A(h->set_cnt, h->sets);
+    A(h->set_off, h->sets + 1);
+    A(h->set_cur, h->sets);
+    A(h->bucket, h->serve_cap);
+    A(h->svc, 1);
+#undef A
+    if (rc) {
+        gids_destroy(h);
+        return rc;
+    }
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->sc_host, sizeof(SampleCounters)));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->svc_host, sizeof(ServeCounters)));
+    GIDS_CUDA_TRY(cudaMemset(h->pinned_off, 0xff, sizeof(int32_t) * N));
+    GIDS_CUDA_TRY(cudaMemset(h->slot_of, 0xff, sizeof(int32_t) * N));
+    GIDS_CUDA_TRY(cudaMemset(h->line_node, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
+    GIDS_CUDA_TRY(cudaMemset(h->last_ins, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
+    GIDS_CUDA_TRY(cudaMemset(h->safe_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->evict_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->blk_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 1024)));
+    GIDS_CUDA_TRY(cudaMemset(h->sup_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32768)));
+    GIDS_CUDA_TRY(cudaMemset(h->reuse, 0, sizeof(uint32_t) * N));
+    GIDS_CUDA_TRY(cudaMemset(h->future, 0, N));
+    GIDS_CUDA_TRY(cudaMemset(h->bm_front, 0, sizeof(uint32_t) * ceil_div(N, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->bm_all, 0, sizeof(uint32_t) * ceil_div(N, 32)));
+    CacheMeta m;
+    memset(&m, 0, sizeof(m));
+    if (eviction_rng)
+        for (int i = 0; i < 6; i++) m.rng[i] = eviction_rng[i];
+    GIDS_CUDA_TRY(cudaMemcpy(h->meta, &m, sizeof(m), cudaMemcpyHostToDevice));
+
+    // exact policy: keep the safe/evicted bitmaps in shared memory when they fit
+    int dev_smem = 0;
+    GIDS_CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                         h->device));
+    size_t with_bits = gids_exact_smem_bytes(L, true), without = gids_exact_smem_bytes(L, false);
+    h->exact_smem = with_bits <= (size_t)dev_smem;
+    if (!h->exact_smem && without > (size_t)dev_smem) {
+        gids_set_error("cache_lines too large for the exact policy (use the set-associative one)");
+        gids_destroy(h);
+        return GIDS_E_INVALID;
+    }
+    *out = h;
+    return GIDS_OK;
+}
+
+int gids_destroy(gids_handle* h) {
+    if (!h) return GIDS_OK;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    void* ptrs[] = {h->indptr,    h->indices,  h->pinned_off, h->cache_rows, h->slot_of,
+                    h->line_node, h->safe_bits, h->evict_bits, h->blk_cnt,   h->sup_cnt,
+                    h->reuse,     h->future,   h->meta,       h->last_ins,   h->bm_front,
+                    h->bm_all,    h->frontier, h->seeds_dev,  h->take_off,   h->draw_off,
+                    h->edges,     h->unique32, h->jump_tab,   h->sc,         h->scan_parts,
+                    h->word_parts, h->ev,      h->kind,       h->line,       h->log_line,
+                    h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
+                    h->svc};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->sc_host) cudaFreeHost(h->sc_host);
+    if (h->svc_host) cudaFreeHost(h->svc_host);
+    if (h->backing_registered) cudaHostUnregister(const_cast<float*>(h->backing));
+    if (h->buffer_registered) cudaHostUnregister(const_cast<float*>(h->buffer_rows));
+    delete h;
+    return GIDS_OK;
+}
+
+int gids_load_graph(gids_handle* h, const uint64_t* indptr, const uint64_t* indices) {
+    CHECK_H(h);
+    const int64_t N = h->N, E = h->E;
+    if (!indptr || (E > 0 && !indices)) {
+        gids_set_error("null graph array");
+        return GIDS_E_INVALID;
+    }
+    if (indptr[0] != 0 || (int64_t)indptr[N] != E) {
+        gids_set_error("indptr must start at 0 and end at num_edges");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaMemcpy(h->indptr, indptr, sizeof(int64_t) * (N + 1), cudaMemcpyHostToDevice));
+    // narrow indices to int32 in bounded chunks through a pinned staging buffer
+    const int64_t chunk = (int64_t)1 << 24;
+    int32_t* stage = nullptr;
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&stage, sizeof(int32_t) * chunk));
+    for (int64_t b = 0; b < E; b += chunk) {
+        int64_t n = E - b < chunk ? E - b : chunk;
+        for (int64_t i = 0; i < n; i++) {
+            uint64_t v = indices[b + i];
+            if (v >= (uint64_t)N) {
+                cudaFreeHost(stage);
+                gids_set_error("node " + std::to_string(v) + " out of range (num_nodes=" +
+                               std::to_string(N) + ")");
+                return GIDS_E_INVALID;
+            }
+            stage[i] = (int32_t)v;
+        }
+        cudaError_t e = cudaMemcpy(h->indices + b, stage, sizeof(int32_t) * n,
+                                   cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFreeHost(stage);
+            gids_set_error(cudaGetErrorString(e));
+            return GIDS_E_CUDA;
+        }
+    }
+    cudaFreeHost(stage);
+    return GIDS_OK;
+}
+
+int gids_set_backing(gids_handle* h, const float* table, int64_t n_rows) {
+    CHECK_H(h);
+    if (n_rows != h->N) {
+        gids_set_error("feature table and graph disagree on node count");
+        return GIDS_E_INVALID;
+    }
+    if (h->backing_registered) cudaHostUnregister(const_cast<float*>(h->backing));
+    TRY(map_host(table, sizeof(float) * (size_t)n_rows * h->row_floats, &h->backing_registered));
+    h->backing = table;
+    return GIDS_OK;
+}
+
+int gids_set_constant_buffer(gids_handle* h, const int64_t* node_ids, int64_t k,
+                             const float* rows) {
+    CHECK_H(h);
+    if (h->buffer_registered) cudaHostUnregister(const_cast<float*>(h->buffer_rows));
+    h->buffer_registered = false;
+    std::vector<int32_t> off((size_t)h->N, -1);
+    for (int64_t i = 0; i < k; i++) {
+        int64_t x = node_ids[i];
+        if (x < 0 || x >= h->N) {
+            gids_set_error("pinned list names nodes outside the feature table");
+            return GIDS_E_INVALID;
+        }
+        off[(size_t)x] = (int32_t)i;
+    }
+    GIDS_CUDA_TRY(cudaMemcpy(h->pinned_off, off.data(), sizeof(int32_t) * h->N,
+                             cudaMemcpyHostToDevice));
+    if (k > 0) TRY(map_host(rows, sizeof(float) * (size_t)k * h->row_floats, &h->buffer_registered));
+    h->buffer_rows = k > 0 ? rows : nullptr;
+    h->buffer_k = k;
+    return GIDS_OK;
+}
+
+int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds, const uint64_t rng[6],
+                void* stream) {
+    CHECK_H(h);
+    if (n_seeds < 1 || n_seeds > h->max_seeds) {
+        gids_set_error("seed count must be in [1, max_seeds]");
+        return GIDS_E_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    GIDS_CUDA_TRY(cudaMemcpyAsync(h->seeds_dev, seeds, sizeof(int64_t) * n_seeds,
+                                  cudaMemcpyHostToDevice, st));
+    h->last_stream = st;
+    return gids_launch_sample(h, n_seeds, rng, st);
+}
+
+int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique, int64_t* draws,
+                      int64_t* contribution) {
+    CHECK_H(h);
+    GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    const SampleCounters& c = *h->sc_host;
+    if (c.overflow) {
+        gids_set_error("sampler workspace bound exceeded");
+        return GIDS_E_CAPACITY;
+    }
+    for (int l = 0; l < h->cfg.n_layers; l++) layer_len[l] = c.layer_len[l];
+    *n_unique = c.n_unique;
+    *draws = c.layer_draw_base[h->cfg.n_layers];
+    *contribution = c.contribution;
+    return GIDS_OK;
+}
+
+int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, void* stream) {
+    CHECK_H(h);
+    cudaStream_t st = (cudaStream_t)stream;
+    const SampleCounters& c = *h->sc_host;
+    int64_t e = 0;
+    for (int l = 0; l < h->cfg.n_layers; l++) e += c.layer_len[l];
+    if (e > 0 && edges_dev)
+        GIDS_CUDA_TRY(cudaMemcpyAsync(edges_dev, h->edges, sizeof(int64_t) * 2 * e,
+                                      cudaMemcpyDeviceToDevice, st));
+    if (unique_dev && c.n_unique > 0) TRY(gids_launch_export_unique(h, unique_dev, st));
+    return GIDS_OK;
+}
+
+int gids_window_push(gids_handle* h, const int64_t* nodes, int64_t n, void* stream) {
+    CHECK_H(h);
+    return gids_launch_window(h, nodes, n, +1, (cudaStream_t)stream);
+}
+int gids_window_pop(gids_handle* h, const int64_t* nodes, int64_t n, void* stream) {
+    CHECK_H(h);
+    return gids_launch_window(h, nodes, n, -1, (cudaStream_t)stream);
+}
+
+int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
+               float* out_dev, void* stream) {
+    CHECK_H(h);
+    if (n < 0 || n > h->serve_cap) {
+        gids_set_error("batch larger than the serving workspace");
+        return GIDS_E_CAPACITY;
+    }
+    if (n > 0 && (!h->backing)) {
+        gids_set_error("no backing store attached (gids_set_backing)");
+        return GIDS_E_STATE;
+    }
+    h->last_stream = (cudaStream_t)stream;
+    return gids_launch_serve(h, unique_dev, n, epoch, out_dev, (cudaStream_t)stream);
+}
+
+int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
+    CHECK_H(h);
+    GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    const ServeCounters& c = *h->svc_host;
+    out->sampled = h->last_serve_n;
+    out->cache_hits = c.tiers[0];
+    out->cpu_buffer_hits = c.tiers[1];
+    out->storage = c.tiers[2];
+    out->bypasses = c.tiers[3];
+    return GIDS_OK;
+}
+
+int gids_serve_decisions(gids_handle* h, int8_t* kind_dev, int64_t* line_dev, void* stream) {
+    CHECK_H(h);
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t n = h->last_serve_n;
+    if (n == 0) return GIDS_OK;
+    GIDS_CUDA_TRY(cudaMemcpyAsync(kind_dev, h->kind, n, cudaMemcpyDeviceToDevice, st));
+    std::vector<int32_t> l32((size_t)n);
+    GIDS_CUDA_TRY(cudaMemcpyAsync(l32.data(), h->line, sizeof(int32_t) * n,
+                                  cudaMemcpyDeviceToHost, st));
+    GIDS_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<int64_t> l64(l32.begin(), l32.end());
+    GIDS_CUDA_TRY(cudaMemcpy(line_dev, l64.data(), sizeof(int64_t) * n, cudaMemcpyHostToDevice));
+    return GIDS_OK;
+}
+
+int gids_cache_stats(gids_handle* h, gids_cache_counters* out) {
+    CHECK_H(h);
+    GIDS_CUDA_TRY(cudaDeviceSynchronize());
+    CacheMeta m;
+    GIDS_CUDA_TRY(cudaMemcpy(&m, h->meta, sizeof(m), cudaMemcpyDeviceToHost));
+    out->hits = m.hits;
+    out->misses = m.misses;
+    out->bypasses = m.bypasses;
+    out->evictions = m.evictions;
+    out->total_increments = m.inc;
+    out->total_decrements = m.dec;
+    if (h->cfg.policy == GIDS_POLICY_EXACT) {
+        out->safe_count = m.safe_count;
+        out->filled = m.fill;
+    } else {  // derived from the line table
+        std::vector<uint32_t> bits((size_t)ceil_div(h->L, 32));
+        std::vector<int32_t> nodes((size_t)h->L);
+        if (h->L > 0) {
+            GIDS_CUDA_TRY(cudaMemcpy(bits.data(), h->safe_bits, 4 * bits.size(),
+                                     cudaMemcpyDeviceToHost));
+            GIDS_CUDA_TRY(cudaMemcpy(nodes.data(), h->line_node, 4 * nodes.size(),
+                                     cudaMemcpyDeviceToHost));
+        }
+        int64_t sc = 0, fill = 0;
+        for (uint32_t b : bits) sc += __builtin_popcount(b);
+        for (int32_t x : nodes) fill += x >= 0;
+        out->safe_count = sc;
+        out->filled = fill;
+    }
+    return GIDS_OK;
+}
+
+int gids_cache_rng(gids_handle* h, uint64_t words_out[6]) {
+    CHECK_H(h);
+    GIDS_CUDA_TRY(cudaDeviceSynchronize());
+    CacheMeta m;
+    GIDS_CUDA_TRY(cudaMemcpy(&m, h->meta, sizeof(m), cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 6; i++) words_out[i] = m.rng[i];
+    return GIDS_OK;
+}
+
+int gids_cache_lines(gids_handle* h, int64_t* node_host, int8_t* state_host) {
+    CHECK_H(h);
+    GIDS_CUDA_TRY(cudaDeviceSynchronize());
+    const int64_t L = h->L;
+    if (L == 0) return GIDS_OK;
+    std::vector<int32_t> nodes((size_t)L);
+    std::vector<uint32_t> bits((size_t)ceil_div(L, 32));
+    GIDS_CUDA_TRY(cudaMemcpy(nodes.data(), h->line_node, 4 * L, cudaMemcpyDeviceToHost));
+    GIDS_CUDA_TRY(cudaMemcpy(bits.data(), h->safe_bits, 4 * bits.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < L; i++) {
+        node_host[i] = nodes[(size_t)i];
+        bool safe = (bits[(size_t)(i >> 5)] >> (i & 31)) & 1u;
+        state_host[i] = nodes[(size_t)i] < 0 ? 0 : (safe ? 1 : 2);
+    }
+    return GIDS_OK;
+}
+
+int64_t gids_cache_capacity(gids_handle* h) { return h ? h->L : -1; }
+int64_t gids_launch_count(gids_handle* h) { return h ? h->launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+// gids_internal.cuh -- shared state, device helpers and launcher prototypes
+// for libgids.so (B200 / sm_100a).  See DESIGN.md for the data layout.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/gids.h"
+
+#define GIDS_WARP 32
+
+// ---------------------------------------------------------------- errors
+void gids_set_error(const std::string& msg);
+
+#define GIDS_CUDA_TRY(expr)                                                      \
+    do {                                                                         \
+        cudaError_t _e = (expr);                                                 \
+        if (_e != cudaSuccess) {                                                 \
+            gids_set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));  \
+            return GIDS_E_CUDA;                                                  \
+        }                                                                        \
+    } while (0)
+
+#define GIDS_LAUNCH_CHECK(h)                                                      \
+    do {                                                                          \
+        cudaError_t _e = cudaGetLastError();                                      \
+        if (_e != cudaSuccess) {                                                  \
+            gids_set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            return GIDS_E_CUDA;                                                   \
+        }                                                                         \
+        (h)->launches++;                                                          \
+    } while (0)
+
+// ------------------------------------------------------------ 128-bit math
+struct u128 {
+    uint64_t lo, hi;
+};
+
+__host__ __device__ __forceinline__ u128 mul128(u128 a, u128 b) {
+    u128 r;
+#ifdef __CUDA_ARCH__
+    r.lo = a.lo * b.lo;
+    r.hi = __umul64hi(a.lo, b.lo) + a.lo * b.hi + a.hi * b.lo;
+#else
+    unsigned __int128 p = (unsigned __int128)a.lo * b.lo;
+    r.lo = (uint64_t)p;
+    r.hi = (uint64_t)(p >> 64) + a.lo * b.hi + a.hi * b.lo;
+#endif
+    return r;
+}
+__host__ __device__ __forceinline__ u128 add128(u128 a, u128 b) {
+    u128 r;
+    r.lo = a.lo + b.lo;
+    r.hi = a.hi + b.hi + (r.lo < a.lo ? 1 : 0);
+    return r;
+}
+
+// numpy PCG64 (XSL-RR 128/64): multiplier of the 128-bit LCG
+static constexpr uint64_t PCG_MULT_HI = 0x2360ED051FC65DA4ULL;
+static constexpr uint64_t PCG_MULT_LO = 0x4385DF649FCCF645ULL;
+
+struct Pcg64 {
+    u128 state, inc;
+    uint32_t has32, buf32;
+};
+
+__host__ __device__ __forceinline__ uint64_t pcg_output(u128 s) {
+    uint64_t x = s.hi ^ s.lo;
+    unsigned rot = (unsigned)(s.hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+__host__ __device__ __forceinline__ uint64_t pcg_next64(Pcg64& g) {
+    g.state = add128(mul128(g.state, u128{PCG_MULT_LO, PCG_MULT_HI}), g.inc);
+    return pcg_output(g.state);
+}
+__host__ __device__ __forceinline__ uint32_t pcg_next32(Pcg64& g) {
+    if (g.has32) {
+        g.has32 = 0;
+        return g.buf32;
+    }
+    uint64_t v = pcg_next64(g);
+    g.has32 = 1;
+    g.buf32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+// Generator.integers(n), 1 <= n < 2^32 (buffered-uint32 Lemire, numpy)
+__host__ __device__ __forceinline__ uint32_t pcg_bounded32(Pcg64& g, uint32_t n) {
+    if (n <= 1) return 0;
+    uint64_t m = (uint64_t)pcg_next32(g) * n;
+    uint32_t left = (uint32_t)m;
+    if (left < n) {
+        uint32_t thresh = (uint32_t)(0u - n) % n;
+        while (left < thresh) {
+            m = (uint64_t)pcg_next32(g) * n;
+            left = (uint32_t)m;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+
+inline Pcg64 pcg_from_words(const uint64_t* w) {
+    Pcg64 g;
+    g.state = u128{w[1], w[0]};
+    g.inc = u128{w[3], w[2]};
+    g.has32 = (uint32_t)w[4];
+    g.buf32 = (uint32_t)w[5];
+    return g;
+}
+inline void pcg_to_words(const Pcg64& g, uint64_t* w) {
+    w[0] = g.state.hi;
+    w[1] = g.state.lo;
+    w[2] = g.inc.hi;
+    w[3] = g.inc.lo;
+    w[4] = g.has32;
+    w[5] = g.buf32;
+}
+
+// splitmix64 finaliser (set hashing and set-associative eviction draws)
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------- the handle
+// Per-batch device counters (one struct, zeroed per sample / serve).
+struct SampleCounters {
+    int64_t n_front;                      // current frontier size
+    int64_t layer_len[GIDS_MAX_LAYERS];   // edges per layer
+    int64_t layer_draw_base[GIDS_MAX_LAYERS + 1];  // doubles consumed before layer l
+    int64_t n_unique;
+    int64_t contribution;
+    int64_t overflow;                     // workspace bound exceeded
+};
+
+struct ServeCounters {
+    int64_t tiers[4];      // hits, buffer, storage, bypasses (this batch)
+    int64_t n_log;         // insertions logged by the exact policy this batch
+};
+
+struct CacheMeta {  // persistent cache counters (CacheState)
+    int64_t hits, misses, bypasses, evictions, inc, dec;
+    int64_t safe_count, fill;
+    uint64_t rng[6];       // exact-policy eviction PCG64 words
+};
+
+struct gids_handle {
+    gids_config cfg;
+    int device;
+    int64_t N, E, L;       // nodes, edges, cache lines (effective)
+    int64_t sets;          // set-associative sets (L / 32)
+    int64_t row_floats;
+    int64_t launches;
+    cudaStream_t last_stream;
+
+    // graph (HBM)
+    int64_t* indptr;       // [N+1]
+    int32_t* indices;      // [E]
+
+    // tiers
+    const float* backing;  // host table (zero-copy), N x dim
+    bool backing_registered;
+    const float* buffer_rows;  // host constant buffer rows, k x dim
+    bool buffer_registered;
+    int64_t buffer_k;
+    int32_t* pinned_off;   // [N] node -> constant-buffer row, -1
+
+    // cache state (HBM)
+    float* cache_rows;     // [L x dim]
+    int32_t* slot_of;      // [N] node -> line, -1
+    int32_t* line_node;    // [L] line -> node, -1
+    uint32_t* safe_bits;   // [ceil(L/32)] SafeToEvict bitmap
+    uint32_t* blk_cnt;     // [ceil(L/1024)] safe lines per 1024-line block
+    uint32_t* sup_cnt;     // [ceil(L/32768)] safe lines per 32768-line superblock
+    uint32_t* evict_bits;  // [ceil(L/32)] lines evicted during the current batch
+    uint32_t* reuse;       // [N] predicted-reuse counters
+    uint8_t* future;       // [N] lookahead-window occurrence counts
+    CacheMeta* meta;       // device
+    int32_t* last_ins;     // [L] scratch: last log index per line (-1)
+
+    // sampler workspace (HBM)
+    int64_t max_seeds;
+    int64_t edge_cap;      // total edges over all layers
+    int64_t front_cap;     // max frontier size
+    uint32_t* bm_front;    // [ceil(N/32)]
+    uint32_t* bm_all;      // [ceil(N/32)]
+    int32_t* frontier;     // [front_cap]
+    int64_t* seeds_dev;    // [max_seeds]
+    int64_t* take_off;     // [front_cap+1] exclusive scan of min(deg, f)
+    int64_t* draw_off;     // [front_cap+1] exclusive scan of draws
+    int64_t* edges;        // [2*edge_cap]
+    int32_t* unique32;     // [front_cap_all]
+    int64_t unique_cap;
+    u128* jump_tab;        // [64][2] {A_i, H_i} for the sampler stream's inc
+    uint64_t jump_inc_hi, jump_inc_lo;
+    bool jump_valid;
+    SampleCounters* sc;    // device
+    SampleCounters* sc_host;  // pinned mirror
+    int64_t scan_parts_cap;
+    int64_t* scan_parts;   // [scan_parts_cap * 2]
+    uint32_t* word_parts;  // [scan_parts_cap]
+
+    // serve workspace
+    int64_t serve_cap;     // max unique per batch
+    uint32_t* ev;          // [serve_cap] packed (line+1)<<1 | inuse_after
+    int8_t* kind;          // [serve_cap]
+    int32_t* line;         // [serve_cap]
+    int32_t* log_line;     // [serve_cap] exact-policy insertion log
+    int32_t* log_pos;      // [serve_cap]
+    int32_t* set_cnt;      // [sets]
+    int64_t* set_off;      // [sets+1]
+    int32_t* set_cur;      // [sets]
+    int32_t* bucket;       // [serve_cap]
+    ServeCounters* svc;    // device
+    ServeCounters* svc_host;  // pinned mirror
+    int64_t last_serve_n;
+    bool exact_smem;       // exact-policy tables fit in shared memory
+};
+
+// ------------------------------------------------------------- launchers
+// scan.cu
+int gids_scan_take_draw(gids_handle* h, int fanout, int layer, cudaStream_t st);
+int gids_bitmap_compact(gids_handle* h, uint32_t* bm, int32_t* out, int64_t* count_out,
+                        int64_t cap, bool clear, cudaStream_t st);
+int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* out,
+                         cudaStream_t st);
+// sampler.cu
+int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_words,
+                       cudaStream_t st);
+int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
+// cache.cu
+int gids_launch_serve(gids_handle* h, const int64_t* unique, int64_t n, uint64_t epoch,
+                      float* out, cudaStream_t st);
+int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delta,
+                       cudaStream_t st);
+int gids_launch_contribution(gids_handle* h, cudaStream_t st);
+// gather.cu
+int gids_launch_gather(gids_handle* h, const int64_t* unique, int64_t n, float* out,
+                       cudaStream_t st);
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+static inline int gids_grid(int64_t work, int block, int max_blocks) {
+    int64_t g = ceil_div(work, block);
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (int)g;
+}
+constexpr int GIDS_SMS = 148;

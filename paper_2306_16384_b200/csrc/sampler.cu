@@ -1,0 +1,205 @@
+// sampler.cu -- K1/K2: layered uniform neighbour sampling over the HBM CSC.
+//
+// Replaces sample_layer / sample_subgraph (sampler.py:50-112) bit-exactly.
+// The reference draws `fanout` doubles per frontier node with deg > fanout
+// from ONE sequential numpy PCG64 stream, visiting the frontier ascending.
+// Here every draw is addressed by its stream offset instead:
+//   offset(node i, draw t) = draws before this layer + exclusive_scan(draws)_i + t
+// and each lane jumps the LCG straight to it (x -> A_i x + H_i per set bit,
+// tables for the stream's increment), so a layer is fully parallel and the
+// host Generator is advanced by the total afterwards (D1 in SURVEY.md).
+//
+// The partial Fisher-Yates (sampler.py:76-78) is resolved without
+// materialising the pool: with j_t = t + int(u_t * (deg - t)), the value
+// settled at position t is indices[lo + p] where p starts at j_t and walks
+// s = t-1 .. 0 taking p = s whenever j_s == p (the last earlier swap that
+// moved something into position p).  One warp handles one frontier node.
+#include "gids_internal.cuh"
+
+namespace {
+
+constexpr int SAMPLE_BLOCK = 256;
+constexpr int SAMPLE_WARPS = SAMPLE_BLOCK / 32;
+constexpr int MAX_FANOUT = 1024;
+
+__device__ __forceinline__ u128 jump(u128 s, uint64_t k, const u128* __restrict__ tab) {
+    while (k) {
+        int i = __ffsll((long long)k) - 1;
+        k &= k - 1;
+        s = add128(mul128(tab[2 * i], s), tab[2 * i + 1]);
+    }
+    return s;
+}
+
+__device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
+    atomicOr(bm + (v >> 5), 1u << (v & 31));
+}
+
+__global__ void k_seed_mark(const int64_t* __restrict__ seeds, int64_t n, uint32_t* bm_front,
+                            uint32_t* bm_all) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = (int32_t)seeds[i];
+        mark(bm_front, v);
+        mark(bm_all, v);
+    }
+}
+
+// one warp per frontier node; fanout <= 32 keeps the swap targets in registers
+__global__ void __launch_bounds__(SAMPLE_BLOCK)
+k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
+               const int32_t* __restrict__ front, const int64_t* __restrict__ take_off,
+               const int64_t* __restrict__ draw_off, const SampleCounters* __restrict__ sc,
+               int layer, int fanout, u128 s0, const u128* __restrict__ tab,
+               int64_t* __restrict__ edges, uint32_t* bm_front, uint32_t* bm_all) {
+    extern __shared__ int64_t j_smem[];  // fanout > 32: swap targets per warp
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    const int64_t nf = sc->n_front;
+    int64_t ebase = 0;
+    for (int l = 0; l < layer; l++) ebase += sc->layer_len[l];
+    const uint64_t dbase = (uint64_t)sc->layer_draw_base[layer];
+    int64_t* jw = j_smem + (int64_t)wib * fanout;
+
+    for (int64_t i = (int64_t)blockIdx.x * SAMPLE_WARPS + wib; i < nf;
+         i += (int64_t)gridDim.x * SAMPLE_WARPS) {
+        const int32_t v = front[i];
+        const int64_t lo = indptr[v];
+        const int64_t deg = indptr[v + 1] - lo;
+        if (deg == 0) continue;
+        int64_t* out = edges + 2 * (ebase + take_off[i]);
+        if (deg <= fanout) {  // whole slice in stored order (sampler.py:70-71)
+            for (int64_t t = lane; t < deg; t += 32) {
+                int32_t src = indices[lo + t];
+                out[2 * t] = src;
+                out[2 * t + 1] = v;
+                mark(bm_front, src);
+                mark(bm_all, src);
+            }
+            continue;
+        }
+        const uint64_t r0 = dbase + (uint64_t)draw_off[i];
+        if (fanout <= 32) {
+            int64_t j = 0;
+            if (lane < fanout) {
+                // draw r0+lane is the output of the state r0+lane+1 steps on
+                double u = (double)(pcg_output(jump(s0, r0 + lane + 1, tab)) >> 11) *
+                           (1.0 / 9007199254740992.0);
+                j = lane + (int64_t)__dmul_rn(u, (double)(deg - lane));
+            }
+            int64_t p = j;
+            for (int s = 30; s >= 0; s--) {
+                int64_t js = __shfl_sync(0xffffffffu, j, s);
+                if (s < lane && js == p) p = s;
+            }
+            if (lane < fanout) {
+                int32_t src = indices[lo + p];
+                out[2 * lane] = src;
+                out[2 * lane + 1] = v;
+                mark(bm_front, src);
+                mark(bm_all, src);
+            }
+        } else {
+            for (int t = lane; t < fanout; t += 32) {
+                double u = (double)(pcg_output(jump(s0, r0 + t + 1, tab)) >> 11) *
+                           (1.0 / 9007199254740992.0);
+                jw[t] = t + (int64_t)__dmul_rn(u, (double)(deg - t));
+            }
+            __syncwarp();
+            for (int t = lane; t < fanout; t += 32) {
+                int64_t p = jw[t];
+                for (int s = t - 1; s >= 0; s--)
+                    if (jw[s] == p) p = s;
+                int32_t src = indices[lo + p];
+                out[2 * t] = src;
+                out[2 * t + 1] = v;
+                mark(bm_front, src);
+                mark(bm_all, src);
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// int32 ids -> int64 (export of unique_nodes)
+__global__ void k_widen(const int32_t* __restrict__ in, const SampleCounters* sc,
+                        int64_t* __restrict__ out) {
+    int64_t n = sc->n_unique;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
+}  // namespace
+
+// LCG jump tables for one increment: A_i = M^(2^i), H_i = inc * sum_{k<2^i} M^k
+static void build_jump_table(uint64_t inc_hi, uint64_t inc_lo, u128* tab) {
+    u128 cm{PCG_MULT_LO, PCG_MULT_HI}, cp{inc_lo, inc_hi};
+    for (int i = 0; i < 64; i++) {
+        tab[2 * i] = cm;
+        tab[2 * i + 1] = cp;
+        cp = mul128(add128(cm, u128{1, 0}), cp);
+        cm = mul128(cm, cm);
+    }
+}
+
+int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaStream_t st) {
+    const gids_config& c = h->cfg;
+    for (int l = 0; l < c.n_layers; l++)
+        if (c.fanouts[l] > MAX_FANOUT) {
+            gids_set_error("fanout above 1024 is not supported by the CUDA sampler");
+            return GIDS_E_INVALID;
+        }
+    if (!h->jump_valid || h->jump_inc_hi != w[2] || h->jump_inc_lo != w[3]) {
+        u128 tab[128];
+        build_jump_table(w[2], w[3], tab);
+        GIDS_CUDA_TRY(cudaMemcpyAsync(h->jump_tab, tab, sizeof(tab), cudaMemcpyHostToDevice, st));
+        // the table is staged from the stack: make the copy complete first
+        GIDS_CUDA_TRY(cudaStreamSynchronize(st));
+        h->jump_valid = true;
+        h->jump_inc_hi = w[2];
+        h->jump_inc_lo = w[3];
+    }
+    u128 s0{w[1], w[0]};
+
+    GIDS_CUDA_TRY(cudaMemsetAsync(h->sc, 0, sizeof(SampleCounters), st));
+    k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
+                                                                     h->bm_front, h->bm_all);
+    GIDS_LAUNCH_CHECK(h);
+    int rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
+                                 st);
+    if (rc) return rc;
+    for (int l = 0; l < c.n_layers; l++) {
+        int f = c.fanouts[l];
+        rc = gids_scan_take_draw(h, f, l, st);
+        if (rc) return rc;
+        size_t smem = f > 32 ? (size_t)SAMPLE_WARPS * f * sizeof(int64_t) : 0;
+        if (smem > 48 * 1024)
+            GIDS_CUDA_TRY(cudaFuncSetAttribute(k_sample_layer,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem));
+        int64_t bound = l == 0 ? n_seeds : h->front_cap;
+        int grid = gids_grid(bound, SAMPLE_WARPS, 16 * GIDS_SMS);
+        k_sample_layer<<<grid, SAMPLE_BLOCK, smem, st>>>(
+            h->indptr, h->indices, h->frontier, h->take_off, h->draw_off, h->sc, l, f, s0,
+            h->jump_tab, h->edges, h->bm_front, h->bm_all);
+        GIDS_LAUNCH_CHECK(h);
+        rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
+                                 st);
+        if (rc) return rc;
+    }
+    rc = gids_bitmap_compact(h, h->bm_all, h->unique32, &h->sc->n_unique, h->unique_cap, true, st);
+    if (rc) return rc;
+    rc = gids_launch_contribution(h, st);
+    if (rc) return rc;
+    GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
+                                  cudaMemcpyDeviceToHost, st));
+    return GIDS_OK;
+}
+
+int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st) {
+    k_widen<<<gids_grid(h->unique_cap, 256, 8 * GIDS_SMS), 256, 0, st>>>(h->unique32, h->sc,
+                                                                       unique_dev);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
+}

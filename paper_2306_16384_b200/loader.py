@@ -1,0 +1,359 @@
+"""GIDS Dataloader on the B200: the reference serving loop driving CUDA kernels.
+
+``Dataloader(cfg)`` / ``next_batch()`` / iteration / ``run()`` keep the
+reference API (dataloader.py:95-389): the same setup derivation from
+``cfg.seed`` (SeedSequence spawn order, dataloader.py:102-147), the same
+run-ahead accumulator and lookahead ring (:184-228), the same per-iteration
+accounting and CSV (:43-74,301-337).  What changes is where the work runs:
+
+* graph, cache lines, per-node metadata: HBM (libgids handle)
+* sampling, window_update, the cache policy, the tier chain and the gather:
+  CUDA kernels (csrc/) behind the C ABI (include/gids.h)
+* constant CPU buffer and storage tier: pinned host memory read zero-copy
+  by the gather kernel
+
+``next_batch`` returns ``(MiniBatch, rows, IterationStats)`` with the batch's
+layers / unique nodes and the gathered ``(U, dim)`` fp32 rows as CUDA
+tensors; the rows are ordered like ``unique_nodes`` (ascending), exactly as
+the reference orders its numpy result.
+"""
+from __future__ import annotations
+
+import math
+from collections import deque
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native
+from .csc import (FeatureStore, generate_synthetic, load_features, load_graph,
+                  pinned_feature_table)
+from .feature_cache import GpuCacheView, WindowBuffer
+from .hot_buffer import build_constant_buffer, reverse_pagerank
+from .sampling import MiniBatch, Sampler, batch_iterator, check_seeds, pcg_words
+from .settings import ConfigError, InfeasibleError, PipelineConfig
+from .storage_model import exact, fetch_total_us, required_accesses
+
+EMA_EPSILON = 1e-3
+
+CSV_HEADER = ("iteration,sampled_nodes,cache_hits,cpu_buffer_hits,ssd_accesses,"
+              "bypasses,redirect_fraction,fetch_time_us,effective_bandwidth_gbps,"
+              "cumulative_time_us")
+
+
+@dataclass(frozen=True)
+class IterationStats:
+    iteration: int
+    sampled_nodes: int
+    cache_hits: int
+    cpu_buffer_hits: int
+    ssd_accesses: int
+    bypasses: int
+    redirect_fraction: float
+    fetch_time_us: float
+    effective_bandwidth_bytes_per_s: float
+    cumulative_time_us: float
+
+    def csv_row(self) -> str:
+        return ",".join([
+            str(self.iteration), str(self.sampled_nodes), str(self.cache_hits),
+            str(self.cpu_buffer_hits), str(self.ssd_accesses), str(self.bypasses),
+            f"{self.redirect_fraction:.6f}", f"{self.fetch_time_us:.3f}",
+            f"{self.effective_bandwidth_bytes_per_s / 1e9:.6f}",
+            f"{self.cumulative_time_us:.3f}"])
+
+
+def stats_csv(stats: list[IterationStats]) -> str:
+    return "\n".join([CSV_HEADER, *(s.csv_row() for s in stats)]) + "\n"
+
+
+@dataclass(frozen=True)
+class RunSummary:
+    iterations_run: int
+    sampled_total: int
+    cache_hit_ratio: float
+    redirect_fraction: float
+    mean_bandwidth_bytes_per_s: float
+    total_fetch_us: float
+    total_train_us: float
+    total_time_us: float
+
+
+@dataclass
+class _Queued:
+    batch: MiniBatch
+    storage_accesses: int
+
+
+def _seed_stream(cfg: PipelineConfig, n: int, work_ss, shuffle_ss):
+    """Host seed supply (dataloader.py:163-180), then the data-parallel slice."""
+    if cfg.seed_mode == "permutation":
+        count = n if cfg.seed_count is None else min(cfg.seed_count, n)
+        it = batch_iterator(np.arange(n, dtype=np.int64)[:count], cfg.batch_size,
+                            shuffle=cfg.shuffle, rng=np.random.default_rng(shuffle_ss))
+    else:
+        rng = np.random.default_rng(work_ss)
+        count = ((cfg.warmup + cfg.iterations) * cfg.batch_size if cfg.seed_count is None
+                 else cfg.seed_count)
+        if cfg.seed_mode == "uniform":
+            seeds = rng.integers(0, n, size=count)
+        else:  # zipf over ids: low ids are hot
+            p = np.arange(1, n + 1, dtype=np.float64) ** (-cfg.zipf_a)
+            p /= p.sum()
+            seeds = rng.choice(n, size=count, p=p)
+        it = batch_iterator(seeds, cfg.batch_size, shuffle=False)
+    if cfg.gids_dp_world == 1:
+        return it
+    return (b for i, b in enumerate(it) if i % cfg.gids_dp_world == cfg.gids_dp_rank)
+
+
+class Dataloader:
+    """GIDS dataloader: sampling + tiered feature gather on one B200."""
+
+    def __init__(self, cfg: PipelineConfig):
+        if not cfg.gids:
+            raise ConfigError("gids=False selects the reference CPU simulator; this package "
+                              "implements the GIDS GPU path only")
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("the GIDS dataloader needs a CUDA device (none visible)")
+        _native.lib()  # fail loudly when the CUDA library is missing
+        self.cfg = cfg
+        self.spec = cfg.ssd_spec()
+        self.device = cfg.gids_device
+        self._torch_dev = torch.device("cuda", self.device)
+        torch.cuda.set_device(self.device)
+
+        graph_ss, feat_ss, sampler_ss, shuffle_ss, evict_ss, work_ss = \
+            np.random.SeedSequence(cfg.seed).spawn(6)
+        if cfg.graph_path is not None:
+            self.graph = load_graph(cfg.graph_path)
+            host = load_features(cfg.features_path, mmap=True)
+            if host.num_nodes != self.graph.num_nodes:
+                raise ConfigError("feature table and graph disagree on node count")
+            self.features = self._pin_table(host)
+        else:
+            self.graph = generate_synthetic(cfg.num_nodes, cfg.avg_degree, cfg.degree_model,
+                                            seed=int(graph_ss.generate_state(1)[0]),
+                                            exponent=cfg.degree_exponent)
+            self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim,
+                                                 int(feat_ss.generate_state(1)[0]), self.device)
+        row_bytes = self.features.row_bytes
+        if row_bytes > self.spec.page_bytes:
+            raise InfeasibleError(f"feature row ({row_bytes} B) exceeds one cache line / page "
+                                  f"({self.spec.page_bytes} B)")
+
+        budget = cfg.resolved_buffer_bytes(self.graph.num_nodes, row_bytes)
+        if budget // row_bytes > 0:
+            self.pagerank = reverse_pagerank(self.graph)
+            self.buffer = build_constant_buffer(self.pagerank.scores, self.features, budget,
+                                                pin_memory=True)
+        else:
+            self.pagerank = None
+            self.buffer = build_constant_buffer(np.empty(0), self.features, 0,
+                                                pinned=np.empty(0, dtype=np.int64))
+        self._pinned_mask = np.zeros(self.graph.num_nodes, dtype=bool)
+        self._pinned_mask[self.buffer.node_ids] = True
+
+        evict_seed = int(evict_ss.generate_state(1)[0])
+        self._h = _native.Handle(
+            num_nodes=self.graph.num_nodes, num_edges=self.graph.num_edges,
+            feature_dim=self.features.dim, device=self.device,
+            cache_lines=cfg.resolved_cache_lines(), policy=cfg.gids_policy, ways=32,
+            evict_key=evict_seed, window_depth=cfg.window_depth, fanouts=cfg.fanouts,
+            max_seeds=cfg.batch_size,
+            eviction_words=pcg_words(np.random.default_rng(evict_seed)))
+        self._h.load_graph(self.graph.indptr, self.graph.indices)
+        self._h.set_backing(self.features.pinned if self.features.pinned is not None
+                            else self.features.table, self.graph.num_nodes)
+        self._h.set_constant_buffer(self.buffer.node_ids,
+                                    self.buffer.pinned if self.buffer.pinned is not None
+                                    else self.buffer.rows)
+        self.cache = GpuCacheView(self._h, self.spec.page_bytes)
+        self.window = WindowBuffer(cfg.window_depth, self._h)
+        self._sampler = Sampler(self._h, self.graph.num_nodes, cfg.fanouts)
+
+        self.base_threshold = required_accesses(self.spec, cfg.target_fraction)
+        self.redirect_ema = 0.0
+        if cfg.gids_dp_world > 1:
+            self._sampler_rng = np.random.Generator(
+                np.random.PCG64(sampler_ss).jumped(cfg.gids_dp_rank))
+        else:
+            self._sampler_rng = np.random.default_rng(sampler_ss)
+        self._batches = _seed_stream(cfg, self.graph.num_nodes, work_ss, shuffle_ss)
+        self._exhausted = False
+        self._pending: deque[_Queued] = deque()
+        self._pending_storage = 0
+        self._ringed = 0
+
+        self._iteration = 0
+        self._clock_us = Fraction(0)
+        self._fetch_us_total = Fraction(0)
+        self._train_us_total = Fraction(0)
+        self._row_frac = Fraction(row_bytes)
+        self._cpu_bytes_per_s = exact(cfg.cpu_gbps) * 10**9
+        self.last_counts = None
+
+    def _pin_table(self, host: FeatureStore) -> FeatureStore:
+        import torch
+        buf = torch.empty((host.num_nodes, host.dim), dtype=torch.float32, pin_memory=True)
+        view = buf.numpy()
+        step = 1 << 18
+        for r in range(0, host.num_nodes, step):
+            view[r:r + step] = host.table[r:r + step]
+        return FeatureStore(num_nodes=host.num_nodes, dim=host.dim, table=view, pinned=buf)
+
+    def gids_init(self, offset: int = 24, cacheline_bytes: int | None = None,
+                  num_elements: int | None = None, n_ssd: int | None = None) -> dict:
+        """The GIDS init call: checks the backing-store layout.
+
+        offset: byte offset of row 0 in the backing file (the .gfea header is
+        24 B, graph.py:304-309); cacheline_bytes: cache line (page) size;
+        num_elements: N * dim fp32 elements.  Returns the resolved layout."""
+        layout = {"offset": 24, "cacheline_bytes": self.spec.page_bytes,
+                  "num_elements": self.graph.num_nodes * self.features.dim,
+                  "n_ssd": self.spec.n_ssd, "row_bytes": self.features.row_bytes}
+        for key, val in (("offset", offset), ("cacheline_bytes", cacheline_bytes),
+                         ("num_elements", num_elements), ("n_ssd", n_ssd)):
+            if val is not None and val != layout[key]:
+                raise ConfigError(f"gids_init {key}={val} disagrees with the loader "
+                                  f"({layout[key]})")
+        return layout
+
+    # -- run-ahead accumulator (dataloader.py:184-228)
+    def effective_threshold(self) -> int:
+        return math.ceil(self.base_threshold / max(EMA_EPSILON, 1.0 - self.redirect_ema))
+
+    def _sample_one(self) -> bool:
+        try:
+            seeds = next(self._batches)
+        except StopIteration:
+            self._exhausted = True
+            return False
+        seeds = check_seeds(seeds, self.graph.num_nodes)
+        st = _native.stream_ptr(self.device)
+        self._sampler.launch(seeds, self._sampler_rng, st)
+        batch, contrib = self._sampler.collect(seeds, self._sampler_rng, st)
+        self._pending.append(_Queued(batch, contrib))
+        self._pending_storage += contrib
+        return True
+
+    def run_ahead(self) -> None:
+        want = self.cfg.window_depth + 1
+        while not self._exhausted:
+            short_window = len(self._pending) < want
+            short_threshold = self._pending_storage < self.effective_threshold()
+            if not (short_window or short_threshold):
+                break
+            if len(self._pending) >= self.cfg.runahead_cap:
+                break
+            if not short_window and self._pending_storage == 0:
+                break
+            self._sample_one()
+        while self._ringed < min(self.window.depth, len(self._pending)):
+            self.window.push_iteration(self._pending[self._ringed].batch.unique_nodes,
+                                       trusted=True)
+            self._ringed += 1
+
+    # -- serving (dataloader.py:232-299)
+    def next_batch(self):
+        import torch
+        self.run_ahead()
+        if not self._pending:
+            raise StopIteration
+        inflight = self._pending_storage
+        entry = self._pending.popleft()
+        self._pending_storage -= entry.storage_accesses
+        if self._ringed > 0:
+            self.window.pop_iteration()
+            self._ringed -= 1
+        self.run_ahead()
+
+        batch = entry.batch
+        unique = batch.unique_nodes
+        rows = torch.empty((unique.numel(), self.features.dim), dtype=torch.float32,
+                           device=self._torch_dev)
+        self._h.serve(unique, self._iteration, rows, _native.stream_ptr(self.device))
+        c = self._h.serve_counts()
+        self.last_counts = c
+        if self.cfg.verify_gather:
+            self._verify(unique, rows)
+        stats = self._account(c.sampled, c.cache_hits, c.cpu_buffer_hits, c.storage,
+                              c.bypasses, inflight)
+        self._iteration += 1
+        return batch, rows, stats
+
+    def _verify(self, unique, rows) -> None:
+        if self.features.seed is not None:
+            bad = _native.verify_rows(self.device, self.features.seed, unique, rows,
+                                      _native.stream_ptr(self.device))
+        else:
+            expect = self.features.rows(unique.cpu().numpy())
+            bad = int((rows.cpu().numpy() != expect).any(axis=1).sum())
+        if bad:
+            raise AssertionError("gathered rows diverge from the feature table")
+
+    def _account(self, sampled, hits, buf_hits, ssd, bypasses, inflight) -> IterationStats:
+        ssd_us = Fraction(0)
+        if ssd > 0:
+            joint = max(inflight, ssd)
+            ssd_us = fetch_total_us(self.spec, joint) * Fraction(ssd, joint)
+        cpu_us = Fraction(buf_hits) * self._row_frac * 1_000_000 / self._cpu_bytes_per_s
+        fetch_us = ssd_us + cpu_us
+        train_us = (Fraction(sampled) * 1_000_000 / exact(self.cfg.consume_rate)
+                    if self.cfg.consume_rate > 0 else Fraction(0))
+        self._clock_us += max(fetch_us, train_us)
+        self._fetch_us_total += fetch_us
+        self._train_us_total += train_us
+        redirect = (hits + buf_hits) / sampled if sampled else 0.0
+        a = self.cfg.redirect_ema_alpha
+        self.redirect_ema = a * redirect + (1.0 - a) * self.redirect_ema
+        if fetch_us > 0:
+            bw = float(Fraction(sampled) * self._row_frac * 1_000_000 / fetch_us)
+        else:
+            bw = float("inf") if sampled else 0.0
+        return IterationStats(iteration=self._iteration, sampled_nodes=sampled, cache_hits=hits,
+                              cpu_buffer_hits=buf_hits, ssd_accesses=ssd, bypasses=bypasses,
+                              redirect_fraction=redirect, fetch_time_us=float(fetch_us),
+                              effective_bandwidth_bytes_per_s=bw,
+                              cumulative_time_us=float(self._clock_us))
+
+    def __iter__(self):
+        return self
+
+    def __next__(self):
+        return self.next_batch()
+
+    def close(self) -> None:
+        self._h.close()
+
+
+def run(dl: Dataloader, iterations: int | None = None, warmup: int | None = None):
+    """Warm-up then measured iterations; stops early when seeds run out."""
+    iterations = dl.cfg.iterations if iterations is None else iterations
+    warmup = dl.cfg.warmup if warmup is None else warmup
+    for _ in range(warmup):
+        try:
+            dl.next_batch()
+        except StopIteration:
+            break
+    c0, f0, t0 = dl._clock_us, dl._fetch_us_total, dl._train_us_total
+    measured: list[IterationStats] = []
+    for _ in range(iterations):
+        try:
+            measured.append(dl.next_batch()[2])
+        except StopIteration:
+            break
+    sampled = sum(s.sampled_nodes for s in measured)
+    hits = sum(s.cache_hits for s in measured)
+    redirected = hits + sum(s.cpu_buffer_hits for s in measured)
+    fetch = dl._fetch_us_total - f0
+    rb = dl.features.row_bytes
+    return measured, RunSummary(
+        iterations_run=len(measured), sampled_total=sampled,
+        cache_hit_ratio=hits / sampled if sampled else 0.0,
+        redirect_fraction=redirected / sampled if sampled else 0.0,
+        mean_bandwidth_bytes_per_s=float(sampled * rb * 1_000_000 / fetch) if fetch > 0 else 0.0,
+        total_fetch_us=float(fetch), total_train_us=float(dl._train_us_total - t0),
+        total_time_us=float(dl._clock_us - c0))
