@@ -1,0 +1,318 @@
+"""bench.py -- GIDS sampling + tiered feature gather on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl gids|reference]
+                  [--workload c2|c1|c4] [--policy exact|setassoc]
+
+A step is one ``Dataloader.next_batch()``: sample a minibatch (CSC walk in
+HBM), lookahead-window update, cache policy, and the tier-chain gather of
+every unique node's feature row into a (U, dim) fp32 tensor on the GPU.
+Prints ONE JSON line (rank 0).  Under torchrun each rank serves its own
+batch subsequence (data-parallel, no data-path collective, weak scaling).
+
+--impl reference times the reference algorithm on the host cores: the CPU
+oracle (oracle/, a C restatement pinned to the reference's own outputs) in
+one process per core, each serving its own batch stream.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "sampled+gathered minibatches/sec"
+WORKLOADS = {
+    # BASELINE.json configs[1]: IGB-small shape, 10% cache + 10% constant CPU buffer
+    "c2": dict(num_nodes=1_000_000, avg_degree=12.0, degree_model="uniform", feature_dim=1024,
+               fanouts=[10, 15], batch_size=1024, cache_lines=100_000, buffer_fraction=0.10,
+               window_depth=8, consume_rate=0.0, seed=42),
+    # configs[0]: 100K nodes, everything fits the GPU cache
+    "c1": dict(num_nodes=100_000, avg_degree=12.0, degree_model="uniform", feature_dim=1024,
+               fanouts=[10, 15], batch_size=1024, cache_lines=100_000, buffer_fraction=0.0,
+               window_depth=8, consume_rate=0.0, seed=42),
+}
+WORKLOAD_NAMES = {
+    "c2": "IGB-small-shaped 1M nodes / 12M edges (uniform), 1024-d fp32, fanout [10,15], "
+          "batch 1024, cache 100K lines (10%) + 10% constant CPU buffer, W=8",
+    "c1": "synthetic 100K nodes / 1.2M edges (uniform), 1024-d fp32, fanout [10,15], "
+          "batch 1024, all rows fit the GPU cache, W=8",
+}
+
+
+def load_peaks() -> dict:
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def start_clock_sampler(dev: int):
+    out = ROOT / "gpurun_out"
+    out.mkdir(exist_ok=True)
+    path = out / f"clocks_rank{dev}.csv"
+    try:
+        p = subprocess.Popen(
+            ["nvidia-smi", "-i", str(dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
+            stdout=open(path, "w"), stderr=subprocess.DEVNULL)
+    except FileNotFoundError:
+        return None, path
+    return p, path
+
+
+def stop_clock_sampler(p, path) -> dict:
+    if p is None:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+    p.terminate()
+    p.wait()
+    sm, smax, reasons = [], [], set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in Path(path).read_text().splitlines():
+        f = [x.strip() for x in line.split(",")]
+        if len(f) < 8:
+            continue
+        try:
+            sm.append(float(f[0]))
+            smax.append(float(f[1]))
+        except ValueError:
+            continue
+        for name, v in zip(names, f[4:8]):
+            if v.lower().startswith("active"):
+                reasons.add(name)
+    return {"sm_mhz": float(np.median(sm)) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def host_link_peak_gbs(dev: int) -> float:
+    """Pinned host -> HBM copy bandwidth (the storage / constant-buffer tier link)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(4):
+        d.copy_(h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize(dev)
+    bw = 4 * n / (s.elapsed_time(e) * 1e-3) / 1e9
+    del h, d
+    return bw
+
+
+def cpu_baseline_sample(cfg, seconds: float = 12.0, dl=None) -> dict:
+    """The oracle loader (C restatement of the reference path), 1 host thread,
+    on the same workload: batches served in ~``seconds``."""
+    from _setup import resolve
+    from oracle import oracle as O
+    r = resolve(cfg, with_table=dl is None)
+    table = dl.features.table if dl is not None else r["table"]
+    ld = O.OracleLoader(r["graph"].indptr, r["graph"].indices, table, r["buffer_nodes"],
+                        r["batches"], cfg.fanouts, r["sampler_words"], r["evict_words"],
+                        cfg.resolved_cache_lines(), cfg.window_depth, r["base_threshold"],
+                        policy=cfg.gids_policy, evict_key=r["evict_seed"])
+    ld.next_batch()  # warm
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < seconds:
+        ld.next_batch()
+        n += 1
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "minibatches/s", "cores": 1, "kind": "port",
+            "sample": f"{n} consecutive batches after 1 warm batch, {dt:.1f}s, "
+                      f"policy={cfg.gids_policy}"}
+
+
+def _ref_worker(args):
+    cfg_dict, proc, seconds, q = args
+    from paper_2306_16384_b200 import make_config
+    cfg = make_config({**cfg_dict, "seed": cfg_dict["seed"] + proc})
+    res = cpu_baseline_sample(cfg, seconds)
+    q.put(res["value"])
+
+
+def run_reference(args, cfg_dict) -> None:
+    """--impl reference: P = all host cores, one oracle loader per process."""
+    import multiprocessing as mp
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    seconds = float(os.environ.get("GIDS_REF_SECONDS", "8"))
+    per_step = []
+    ctx = mp.get_context("fork")
+    for step in range(args.warmup + args.steps):
+        q = ctx.Queue()
+        ps = [ctx.Process(target=_ref_worker, args=((cfg_dict, p, seconds, q),))
+              for p in range(procs)]
+        for p in ps:
+            p.start()
+        vals = [q.get() for _ in ps]
+        for p in ps:
+            p.join()
+        if step >= args.warmup:
+            per_step.append(sum(vals))
+        if step == 0 and args.steps + args.warmup > 1:
+            seconds = max(2.0, seconds / 2)
+    value = float(np.mean(per_step))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "minibatches/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / value * procs if value else None,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+            "data": "synthetic", "config": {"workload": WORKLOAD_NAMES[args.workload],
+                                            "policy": cfg_dict.get("gids_policy", "exact")},
+            "cpu_baseline": {"value": value, "unit": "minibatches/s", "cores": procs,
+                             "kind": "port",
+                             "sample": f"{procs} processes x ~{seconds:.0f}s of batches each, "
+                                       f"seeds 42+p"},
+            "e2e": {"value": value, "unit": "minibatches/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="gids", choices=["gids", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--policy", default="exact", choices=["exact", "setassoc"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg_dict = {**WORKLOADS[args.workload], "gids_policy": args.policy}
+
+    if args.impl == "reference":
+        run_reference(args, cfg_dict)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2306_16384_b200 import Dataloader, make_config
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    cfg = make_config({**cfg_dict, "gids_device": local, "gids_dp_rank": rank,
+                       "gids_dp_world": world})
+    t_setup = time.perf_counter()
+    dl = Dataloader(cfg)
+    setup_s = time.perf_counter() - t_setup
+    link_peak = host_link_peak_gbs(local)
+    h = dl._h
+
+    for _ in range(args.warmup):
+        dl.next_batch()
+    torch.cuda.synchronize(local)
+    if world > 1:
+        dist.barrier()
+    h.set_profiling(True)
+    launches0 = h.launch_count()
+    clk, clk_path = start_clock_sampler(local)
+    rows_host = rows_hbm = sampled = 0
+    tiers = np.zeros(4, np.int64)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(local)
+    t0 = time.perf_counter()
+    start.record()
+    for _ in range(args.steps):
+        mb, rows, st = dl.next_batch()
+        sampled += st.sampled_nodes
+        tiers += (st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses)
+    end.record()
+    torch.cuda.synchronize(local)
+    wall = time.perf_counter() - t0
+    clocks = stop_clock_sampler(clk, clk_path)
+    ms = start.elapsed_time(end)
+    launches = h.launch_count() - launches0
+    phases = h.phase_times()
+    h.set_profiling(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=local)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_max = float(t.item())
+
+    row_bytes = cfg.feature_dim * 4
+    host_rows = int(tiers[1] + tiers[2])
+    value = world * args.steps / (ms_max / 1e3)
+    gather_gbs = sampled * row_bytes / (ms / 1e3) / 1e9
+    # dominant kernel: the host-tier gather (zero-copy reads over the host link)
+    host_bytes_per_launch = host_rows * row_bytes / args.steps
+    host_ms = phases["gather_host_ms"] / max(1.0, phases["batches"])
+    achieved_link = host_bytes_per_launch / (host_ms / 1e3) / 1e9 if host_ms else None
+    peaks = load_peaks()
+    hbm_peak = peaks.get("hbm_gbs")
+    hit_ms = phases["gather_hits_ms"] / max(1.0, phases["batches"])
+    hit_bytes = 2 * tiers[0] * row_bytes / args.steps  # read line + write row
+    # tier-weighted roofline of the whole step: slower of host link and HBM
+    hbm_bytes_step = (2 * tiers[0] + host_rows + host_rows) * row_bytes / args.steps
+    t_roof = max(host_rows * row_bytes / args.steps / (link_peak * 1e9),
+                 hbm_bytes_step / (hbm_peak * 1e9) if hbm_peak else 0.0)
+    step_s = ms_max / 1e3 / args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": "minibatches/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic (reference generate_synthetic graph + synthetic_feature_rows table)",
+        "config": {"workload": WORKLOAD_NAMES[args.workload], "policy": args.policy,
+                   "parallelism": f"dp{world}", "global_batch": cfg.batch_size * world,
+                   "l2": "inputs larger than L2 (4.1 GB host table, 410 MB HBM cache)"},
+        "gather_gbps": gather_gbs,
+        "tiers_per_step": {"sampled": sampled / args.steps,
+                           "cache_hits": float(tiers[0]) / args.steps,
+                           "cpu_buffer": float(tiers[1]) / args.steps,
+                           "storage": float(tiers[2]) / args.steps,
+                           "bypasses": float(tiers[3]) / args.steps},
+        "phase_ms_per_step": {k: v / max(1.0, phases["batches"]) for k, v in phases.items()
+                              if k != "batches"},
+        "tier_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / step_s,
+                          "host_link_peak_gbs": link_peak, "hbm_peak_gbs": hbm_peak},
+        "roofline": {"bound": "host_link", "kernel": "k_gather_host",
+                     "achieved": achieved_link, "peak": link_peak, "unit": "GB/s",
+                     "frac": achieved_link / link_peak if achieved_link else None,
+                     "traffic": None,
+                     "peak_source": "pinned H2D cudaMemcpy measured in this run "
+                                    "(MEASURED_PEAKS.json has no host-link entry)",
+                     "hbm_kernel": {"kernel": "k_gather_hits",
+                                    "achieved": hit_bytes / (hit_ms / 1e3) / 1e9
+                                    if hit_ms else None,
+                                    "peak": hbm_peak, "unit": "GB/s"}},
+        "e2e": {"value": value, "unit": "minibatches/s",
+                "h2d_bytes_per_step": int(cfg.batch_size * 8 + host_bytes_per_launch),
+                "d2h_bytes_per_step": 256,
+                "note": "timed through Dataloader.next_batch (the public API): host seed "
+                        "batches in, host-tier rows over the link, per-step stats read back"},
+        "gpu_launches": launches, "clocks": clocks,
+        "setup_s": setup_s, "wall_s": wall,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_sample(cfg, 12.0, dl)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dl.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

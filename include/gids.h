@@ -153,6 +153,13 @@ GIDS_API int gids_synthesize_rows(int device, uint64_t seed, int64_t row0, int64
 GIDS_API int gids_verify_rows(int device, uint64_t seed, const int64_t* nodes_dev, int64_t n, int32_t dim,
                      const float* rows_dev, int64_t* bad, void* stream);
 
+/* Per-phase device time (CUDA events on the launching stream), accumulated
+ * while profiling is on: out_ms[0] sampling, [1] window + cache policy,
+ * [2] hit gather (HBM), [3] host-tier gather (zero-copy), [4] batches
+ * served.  gids_set_profiling(h, 1) resets the accumulators. */
+GIDS_API int gids_set_profiling(gids_handle* h, int on);
+GIDS_API int gids_phase_times(gids_handle* h, double out_ms[5]);
+
 /* Kernel launches issued by this handle since creation (evidence counter). */
 GIDS_API int64_t gids_launch_count(gids_handle* h);
 

@@ -82,6 +82,8 @@ def lib() -> C.CDLL:
         "gids_synthesize_rows": ([i32, u64, i64, i64, i32, vp, vp], C.c_int),
         "gids_verify_rows": ([i32, u64, vp, i64, i32, vp, vp, vp], C.c_int),
         "gids_launch_count": ([vp], i64),
+        "gids_set_profiling": ([vp, C.c_int], C.c_int),
+        "gids_phase_times": ([vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -100,7 +102,8 @@ def exported_symbols() -> list[str]:
             "gids_sample_sizes", "gids_sample_export", "gids_window_push", "gids_window_pop",
             "gids_serve", "gids_serve_counts", "gids_serve_decisions", "gids_cache_stats",
             "gids_cache_rng", "gids_cache_lines", "gids_cache_capacity",
-            "gids_synthesize_rows", "gids_verify_rows", "gids_launch_count"]
+            "gids_synthesize_rows", "gids_verify_rows", "gids_set_profiling",
+            "gids_phase_times", "gids_launch_count"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -241,6 +244,15 @@ class Handle:
 
     def capacity(self) -> int:
         return int(lib().gids_cache_capacity(self.h))
+
+    def set_profiling(self, on: bool) -> None:
+        check(lib().gids_set_profiling(self.h, 1 if on else 0), "set_profiling")
+
+    def phase_times(self) -> dict:
+        out = np.zeros(5, np.float64)
+        check(lib().gids_phase_times(self.h, out.ctypes.data), "phase_times")
+        return dict(zip(("sample_ms", "cache_ms", "gather_hits_ms", "gather_host_ms",
+                         "batches"), out.tolist()))
 
     def launch_count(self) -> int:
         return int(lib().gids_launch_count(self.h))

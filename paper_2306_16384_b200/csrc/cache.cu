@@ -491,6 +491,7 @@ size_t gids_exact_smem_bytes(int64_t L, bool with_bits) {
 int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t epoch, float* out,
                       cudaStream_t st) {
     const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
+    gids_mark(h, 2, st);
     GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
     if (n > 0) {
         k_window_consume<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
@@ -536,8 +537,10 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
             gids_set_error("set-associative cache without sets");
             return GIDS_E_STATE;
         }
+        gids_mark(h, 3, st);
         int rc = gids_launch_gather(h, uniq, n, out, st);
         if (rc) return rc;
+        h->serve_timed = h->profiling;
     }
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
                                   cudaMemcpyDeviceToHost, st));

@@ -198,6 +198,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         gids_destroy(h);
         return GIDS_E_INVALID;
     }
+    for (int i = 0; i < 8; i++) GIDS_CUDA_TRY(cudaEventCreate(&h->tev[i]));
     *out = h;
     return GIDS_OK;
 }
@@ -216,6 +217,8 @@ int gids_destroy(gids_handle* h) {
                     h->svc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    for (int i = 0; i < 8; i++)
+        if (h->tev[i]) cudaEventDestroy(h->tev[i]);
     if (h->sc_host) cudaFreeHost(h->sc_host);
     if (h->svc_host) cudaFreeHost(h->svc_host);
     if (h->backing_registered) cudaHostUnregister(const_cast<float*>(h->backing));
@@ -316,6 +319,11 @@ int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique, int
                       int64_t* contribution) {
     CHECK_H(h);
     GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    if (h->sample_timed) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, h->tev[0], h->tev[1]) == cudaSuccess) h->phase_ms[0] += ms;
+        h->sample_timed = false;
+    }
     const SampleCounters& c = *h->sc_host;
     if (c.overflow) {
         gids_set_error("sampler workspace bound exceeded");
@@ -368,6 +376,17 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
 int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
     CHECK_H(h);
     GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    if (h->serve_timed) {
+        float a = 0.f, b = 0.f, c2 = 0.f;
+        cudaEventElapsedTime(&a, h->tev[2], h->tev[3]);
+        cudaEventElapsedTime(&b, h->tev[3], h->tev[4]);
+        cudaEventElapsedTime(&c2, h->tev[4], h->tev[5]);
+        h->phase_ms[1] += a;
+        h->phase_ms[2] += b;
+        h->phase_ms[3] += c2;
+        h->phase_ms[4] += 1.0;
+        h->serve_timed = false;
+    }
     const ServeCounters& c = *h->svc_host;
     out->sampled = h->last_serve_n;
     out->cache_hits = c.tiers[0];
@@ -447,6 +466,20 @@ int gids_cache_lines(gids_handle* h, int64_t* node_host, int8_t* state_host) {
         bool safe = (bits[(size_t)(i >> 5)] >> (i & 31)) & 1u;
         state_host[i] = nodes[(size_t)i] < 0 ? 0 : (safe ? 1 : 2);
     }
+    return GIDS_OK;
+}
+
+int gids_set_profiling(gids_handle* h, int on) {
+    CHECK_H(h);
+    h->profiling = on != 0;
+    h->sample_timed = h->serve_timed = false;
+    for (int i = 0; i < 5; i++) h->phase_ms[i] = 0.0;
+    return GIDS_OK;
+}
+
+int gids_phase_times(gids_handle* h, double out_ms[5]) {
+    CHECK_H(h);
+    for (int i = 0; i < 5; i++) out_ms[i] = h->phase_ms[i];
     return GIDS_OK;
 }
 

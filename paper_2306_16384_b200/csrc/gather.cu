@@ -178,10 +178,12 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
     int grid = gids_grid(n, WARPS, 16 * GIDS_SMS);
     k_gather_hits<<<grid, BLOCK, 0, st>>>(n, h->kind, h->line, h->cache_rows, out, dim, h->svc);
     GIDS_LAUNCH_CHECK(h);
+    gids_mark(h, 4, st);
     k_gather_host<<<grid, BLOCK, 0, st>>>(uniq, n, h->kind, h->line, h->line_node, h->pinned_off,
                                           h->buffer_rows, h->backing, h->cache_rows, out, dim,
                                           h->svc);
     GIDS_LAUNCH_CHECK(h);
+    gids_mark(h, 5, st);
     return GIDS_OK;
 }
 

@@ -217,7 +217,17 @@ struct gids_handle {
     ServeCounters* svc_host;  // pinned mirror
     int64_t last_serve_n;
     bool exact_smem;       // exact-policy tables fit in shared memory
+
+    // phase timing (gids_set_profiling)
+    bool profiling;
+    cudaEvent_t tev[8];    // 0,1 sample; 2..5 serve phase boundaries
+    bool sample_timed, serve_timed;
+    double phase_ms[5];
 };
+
+inline void gids_mark(gids_handle* h, int i, cudaStream_t st) {
+    if (h->profiling) cudaEventRecord(h->tev[i], st);
+}
 
 // ------------------------------------------------------------- launchers
 // scan.cu

@@ -162,6 +162,7 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
     }
     u128 s0{w[1], w[0]};
 
+    gids_mark(h, 0, st);
     GIDS_CUDA_TRY(cudaMemsetAsync(h->sc, 0, sizeof(SampleCounters), st));
     k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
                                                                      h->bm_front, h->bm_all);
@@ -192,6 +193,8 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
     if (rc) return rc;
     rc = gids_launch_contribution(h, st);
     if (rc) return rc;
+    gids_mark(h, 1, st);
+    h->sample_timed = h->profiling;
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
                                   cudaMemcpyDeviceToHost, st));
     return GIDS_OK;

@@ -1,0 +1,123 @@
+"""Dataloader on the GPU vs the reference's golden runs (exact policy) and the
+oracle (set-associative policy).  Bit-exact per batch: seeds, unique nodes,
+every layer, the gathered rows, tier counts, the CSV row and cache counters."""
+import numpy as np
+import pytest
+
+from _setup import config_of, fixture, resolve, sha
+from oracle import oracle as O
+from paper_2306_16384_b200 import Dataloader, make_config, run, stats_csv
+
+pytestmark = pytest.mark.gpu
+
+LOADERS = ["c09", "alltiers", "edgeless", "c1small", "c2small", "desk", "locality_w0",
+           "locality_w8"]
+
+
+@pytest.mark.parametrize("name", LOADERS)
+def test_gpu_loader_matches_reference_run(name):
+    fx = fixture(name)
+    dl = Dataloader(config_of(fx))
+    assert np.array_equal(dl.buffer.node_ids, fx["buffer_nodes"])
+    assert dl.base_threshold == int(fx["base_threshold"])
+    for b in range(int(fx["n_batches"])):
+        mb, rows, st = dl.next_batch()
+        assert np.array_equal(mb.seeds, fx[f"b{b}_seeds"]), b
+        assert np.array_equal(mb.unique_nodes.cpu().numpy(), fx[f"b{b}_unique"]), b
+        assert [sha(l.cpu().numpy().astype("<i8")) for l in mb.layers] == \
+            list(fx[f"b{b}_layer_sha"]), b
+        assert sha(rows.cpu().numpy()) == str(fx[f"b{b}_rows_sha"]), b
+        assert [st.sampled_nodes, st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses,
+                st.bypasses] == fx["tiers"][b].tolist(), b
+        assert st.csv_row() == str(fx["csv"][b]), b
+        c = dl.cache
+        assert [c.hits, c.misses, c.bypasses, c.evictions, c.total_increments,
+                c.total_decrements, len(dl._pending)] == fx["cache_stats"][b].tolist(), b
+    dl.close()
+
+
+def test_gpu_c09_known_answer():
+    """test_acceptance.py:242-258: 1040/1351/1793/3012 and 84 evictions."""
+    fx = fixture("c09")
+    dl = Dataloader(config_of(fx, verify_gather=True))
+    tiers = np.zeros(4, np.int64)
+    for _ in range(27):
+        _, _, st = dl.next_batch()
+        tiers += (st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses)
+    assert tiers.tolist() == [1040, 1351, 1793, 3012]
+    assert dl.cache.evictions == 84
+
+
+def test_gpu_edgeless_runahead_arithmetic():
+    """test_dataloader.py:32-54: 855 threshold, 3 pending batches, 210 us."""
+    fx = fixture("edgeless")
+    dl = Dataloader(config_of(fx))
+    dl.run_ahead()
+    assert dl.base_threshold == 855 and len(dl._pending) == 3 and dl._pending_storage == 900
+    _, _, st = dl.next_batch()
+    assert st.fetch_time_us == 210.0 and st.bypasses == 300
+    measured, summary = run(dl, iterations=2, warmup=0)
+    assert summary.iterations_run == 2
+    assert stats_csv(measured).startswith("iteration,sampled_nodes")
+
+
+@pytest.mark.parametrize("name", ["alltiers", "c2small", "locality_w8"])
+def test_gpu_setassoc_matches_oracle(name):
+    fx = fixture(name)
+    cfg = config_of(fx, gids_policy="setassoc")
+    r = resolve(cfg)
+    ld = O.OracleLoader(r["graph"].indptr, r["graph"].indices, r["table"], r["buffer_nodes"],
+                        r["batches"], cfg.fanouts, r["sampler_words"], r["evict_words"],
+                        cfg.resolved_cache_lines(), cfg.window_depth, r["base_threshold"],
+                        policy="setassoc", evict_key=r["evict_seed"])
+    dl = Dataloader(cfg)
+    n = min(int(fx["n_batches"]), 40)
+    for b in range(n):
+        o = ld.next_batch()
+        mb, rows, st = dl.next_batch()
+        assert np.array_equal(mb.unique_nodes.cpu().numpy(), o["unique"]), b
+        assert [st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses] == \
+            o["tiers"].tolist(), b
+        assert np.array_equal(rows.cpu().numpy(), o["rows"]), b
+    os_ = ld.cache.stats()
+    c = dl.cache
+    assert [c.hits, c.misses, c.bypasses, c.evictions] == \
+        [os_["hits"], os_["misses"], os_["bypasses"], os_["evictions"]]
+    node, st = dl.cache.lines()
+    onode, ost = ld.cache.lines_snapshot()
+    assert np.array_equal(node, onode) and np.array_equal(st, ost)
+
+
+def test_gpu_exact_cache_state_matches_oracle_after_evictions():
+    fx = fixture("locality_w0")
+    cfg = config_of(fx)
+    r = resolve(cfg)
+    ld = O.OracleLoader(r["graph"].indptr, r["graph"].indices, r["table"], r["buffer_nodes"],
+                        r["batches"], cfg.fanouts, r["sampler_words"], r["evict_words"],
+                        cfg.resolved_cache_lines(), cfg.window_depth, r["base_threshold"])
+    dl = Dataloader(cfg)
+    for _ in range(60):
+        ld.next_batch()
+        dl.next_batch()
+    node, st = dl.cache.lines()
+    onode, ost = ld.cache.lines_snapshot()
+    assert np.array_equal(node, onode) and np.array_equal(st, ost)
+    assert dl.cache.eviction_rng_words().tolist() == ld.cache.rng_words().tolist()
+
+
+def test_gpu_c2_shape_properties():
+    """C2 shape (1M nodes / 12M edges, 1024-d, 10% cache + 10% buffer, W=8) at
+    full size: every gathered row re-derived on device (verify_gather), tier
+    identities per batch, ascending unique nodes."""
+    cfg = make_config(dict(num_nodes=1_000_000, avg_degree=12.0, degree_model="uniform",
+                           feature_dim=1024, fanouts=[10, 15], batch_size=1024,
+                           cache_lines=100_000, buffer_fraction=0.10, window_depth=8,
+                           consume_rate=0.0, seed=42, verify_gather=True))
+    dl = Dataloader(cfg)
+    for _ in range(6):
+        mb, rows, st = dl.next_batch()
+        u = mb.unique_nodes
+        assert bool((u[1:] > u[:-1]).all())
+        assert st.cache_hits + st.cpu_buffer_hits + st.ssd_accesses == st.sampled_nodes
+        assert rows.shape == (u.numel(), 1024)
+    assert dl.cache.evictions > 0 or dl.cache.bypasses > 0
