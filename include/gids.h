@@ -98,12 +98,14 @@ GIDS_API int gids_set_constant_buffer(gids_handle* h, const int64_t* node_ids, i
 
 /* sample_subgraph (sampler.py:87-112) into the handle's workspace.
  * seeds: host int64[n_seeds] (validated by the caller as sampler.py:91-96
- * does).  rng: 6-word PCG64 state of the sampler Generator at call time;
- * the draws are taken by per-node jump-ahead from it, so the caller
- * advances its Generator by the `draws` gids_sample_sizes reports
+ * does).  The sampler stream lives on the device: rng (6-word PCG64 state
+ * of the sampler Generator) seeds it; NULL continues from where the previous
+ * batch left it (the device advances its state by the batch's draws, so
+ * consecutive batches need no host round trip).  The caller advances its
+ * own Generator by the `draws` reported for each batch
  * (rng.bit_generator.advance(draws)) to stay in step with the reference. */
 GIDS_API int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds,
-                const uint64_t rng[6], void* stream);
+                const uint64_t* rng, void* stream);
 
 /* Sizes of the last gids_sample (synchronises the stream):
  * layer_len[n_layers], n_unique, draws (doubles consumed), and the run-ahead
@@ -116,6 +118,17 @@ GIDS_API int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_un
  * arrays back to back; unique_nodes int64[U] ascending.  Device pointers. */
 GIDS_API int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, void* stream);
 
+/* Asynchronous export of the last gids_sample, enqueued on `stream` without
+ * a host round trip: edges_dev / unique_dev must hold the workspace bounds
+ * (gids_sample_capacity); sizes_host (pinned, int64[n_layers + 5]) receives
+ * [layer_len..., n_unique, draws, contribution, overflow] when the stream
+ * gets there. */
+GIDS_API int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev,
+                                      int64_t* sizes_host, void* stream);
+GIDS_API int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* unique_cap);
+/* Device-resident sampler stream state (synchronises; for tests). */
+GIDS_API int gids_sampler_rng(gids_handle* h, uint64_t words_out[6]);
+
 /* WindowBuffer.push_iteration / pop_iteration (cache.py:66-91) for an
  * ascending unique device list. */
 GIDS_API int gids_window_push(gids_handle* h, const int64_t* nodes_dev, int64_t n, void* stream);
@@ -125,11 +138,14 @@ GIDS_API int gids_window_pop(gids_handle* h, const int64_t* nodes_dev, int64_t n
  * per-node CacheState.access in ascending order (cache.py:144-180) or the
  * set-associative policy, tier chain, gather into out_dev (U x dim fp32,
  * ascending unique order) and cache insertion.  epoch keys the
- * set-associative eviction draws. */
+ * set-associative eviction draws.  The decisions run on `stream`; the row
+ * movement runs on `gather_stream` (NULL = same stream) after them, so the
+ * next batch's decisions can overlap this batch's gather.  out_dev is
+ * complete when gather_stream reaches this point. */
 GIDS_API int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
-               float* out_dev, void* stream);
+               float* out_dev, void* stream, void* gather_stream);
 
-/* Tier counts of the last gids_serve (synchronises the stream). */
+/* Tier counts of the last gids_serve (synchronises `stream` only). */
 GIDS_API int gids_serve_counts(gids_handle* h, gids_tier_counts* out);
 
 /* Per-node decisions of the last gids_serve: kind int8[U] (GIDS_KIND_*) and

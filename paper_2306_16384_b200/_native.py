@@ -70,9 +70,12 @@ def lib() -> C.CDLL:
         "gids_sample": ([vp, vp, i64, vp, vp], C.c_int),
         "gids_sample_sizes": ([vp, vp, vp, vp, vp], C.c_int),
         "gids_sample_export": ([vp, vp, vp, vp], C.c_int),
+        "gids_sample_export_async": ([vp, vp, vp, vp, vp], C.c_int),
+        "gids_sample_capacity": ([vp, vp, vp], C.c_int),
+        "gids_sampler_rng": ([vp, vp], C.c_int),
         "gids_window_push": ([vp, vp, i64, vp], C.c_int),
         "gids_window_pop": ([vp, vp, i64, vp], C.c_int),
-        "gids_serve": ([vp, vp, i64, u64, vp, vp], C.c_int),
+        "gids_serve": ([vp, vp, i64, u64, vp, vp, vp], C.c_int),
         "gids_serve_counts": ([vp, C.POINTER(TierCounts)], C.c_int),
         "gids_serve_decisions": ([vp, vp, vp, vp], C.c_int),
         "gids_cache_stats": ([vp, C.POINTER(CacheCounters)], C.c_int),
@@ -99,7 +102,8 @@ def exported_symbols() -> list[str]:
     """Every entry point include/gids.h declares (checked by the CPU tests)."""
     return ["gids_abi_version", "gids_last_error", "gids_create", "gids_destroy",
             "gids_load_graph", "gids_set_backing", "gids_set_constant_buffer", "gids_sample",
-            "gids_sample_sizes", "gids_sample_export", "gids_window_push", "gids_window_pop",
+            "gids_sample_sizes", "gids_sample_export", "gids_sample_export_async",
+            "gids_sample_capacity", "gids_sampler_rng", "gids_window_push", "gids_window_pop",
             "gids_serve", "gids_serve_counts", "gids_serve_decisions", "gids_cache_stats",
             "gids_cache_rng", "gids_cache_lines", "gids_cache_capacity",
             "gids_synthesize_rows", "gids_verify_rows", "gids_set_profiling",
@@ -189,10 +193,27 @@ class Handle:
               "set_constant_buffer")
 
     # -- sampling
-    def sample(self, seeds: np.ndarray, words: np.ndarray, stream: int) -> None:
+    def sample(self, seeds: np.ndarray, words, stream: int) -> None:
+        """words: the Generator's 6-word state to (re)seed the device stream, or
+        None to continue the device-resident stream."""
         s = np.ascontiguousarray(seeds, dtype=np.int64)
-        w = np.ascontiguousarray(words, dtype=np.uint64)
-        check(lib().gids_sample(self.h, s.ctypes.data, len(s), w.ctypes.data, stream), "sample")
+        w = None if words is None else np.ascontiguousarray(words, dtype=np.uint64)
+        check(lib().gids_sample(self.h, s.ctypes.data, len(s),
+                                None if w is None else w.ctypes.data, stream), "sample")
+
+    def sample_export_async(self, edges, unique, sizes_host, stream: int) -> None:
+        check(lib().gids_sample_export_async(self.h, _p(edges), _p(unique), _p(sizes_host),
+                                             stream), "sample_export_async")
+
+    def sample_capacity(self) -> tuple[int, int]:
+        e, u = C.c_int64(), C.c_int64()
+        check(lib().gids_sample_capacity(self.h, C.byref(e), C.byref(u)), "sample_capacity")
+        return e.value, u.value
+
+    def sampler_rng(self) -> np.ndarray:
+        w = np.zeros(6, np.uint64)
+        check(lib().gids_sampler_rng(self.h, w.ctypes.data), "sampler_rng")
+        return w
 
     def sample_sizes(self):
         lens = np.zeros(self.n_layers, np.int64)
@@ -213,9 +234,9 @@ class Handle:
     def window_pop(self, nodes, stream: int) -> None:
         check(lib().gids_window_pop(self.h, _p(nodes), nodes.numel(), stream), "window_pop")
 
-    def serve(self, unique, epoch: int, out, stream: int) -> None:
-        check(lib().gids_serve(self.h, _p(unique), unique.numel(), epoch, _p(out), stream),
-              "serve")
+    def serve(self, unique, epoch: int, out, stream: int, gather_stream: int | None = None) -> None:
+        check(lib().gids_serve(self.h, _p(unique), unique.numel(), epoch, _p(out), stream,
+                               gather_stream), "serve")
 
     def serve_counts(self) -> TierCounts:
         t = TierCounts()

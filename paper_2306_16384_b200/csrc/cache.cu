@@ -163,12 +163,82 @@ __device__ __forceinline__ void tab_set_safe(const ExactTables& t, int64_t s) {
     t.blk[s >> 10]++;
     t.sup[s >> 15]++;
 }
+// several lanes may mark different lines of one word / block at once
+__device__ __forceinline__ void tab_set_safe_atomic(const ExactTables& t, int64_t s) {
+    atomicOr(&t.safe[s >> 5], 1u << (s & 31));
+    atomicAdd(&t.blk[s >> 10], 1u);
+    atomicAdd(&t.sup[s >> 15], 1u);
+}
 __device__ __forceinline__ void tab_clear_safe(const ExactTables& t, int64_t s) {
     t.safe[s >> 5] &= ~(1u << (s & 31));
     t.blk[s >> 10]--;
     t.sup[s >> 15]--;
 }
 
+// ascending list of SafeToEvict lines held one per lane (lane i = i-th
+// smallest), valid while there are at most 32 of them: in the steady state of
+// a window-protected cache almost every eviction sees 1-3 safe lines, and
+// then select(r) is a single shuffle instead of a three-level table walk
+constexpr int32_t NO_LINE = 0x7fffffff;
+constexpr int EV_AHEAD = 16;  // chunks of the event stream in flight
+constexpr int EV_RING = 32;
+
+__device__ __forceinline__ void list_insert(int32_t& sl, int32_t s) {
+    const int lane = threadIdx.x & 31;
+    const int at = __popc(__ballot_sync(0xffffffffu, sl < s));
+    const int32_t up = __shfl_up_sync(0xffffffffu, sl, 1);
+    sl = lane < at ? sl : (lane == at ? s : up);
+}
+__device__ __forceinline__ void list_remove(int32_t& sl, int r) {
+    const int lane = threadIdx.x & 31;
+    const int32_t down = __shfl_down_sync(0xffffffffu, sl, 1);
+    sl = lane < r ? sl : (lane == 31 ? NO_LINE : down);
+}
+
+// rebuild the list from the tables (<= 32 safe lines known to exist)
+__device__ __forceinline__ int32_t list_rebuild(const ExactTables& t, int64_t nw, int64_t nb) {
+    const int lane = threadIdx.x & 31;
+    int32_t sl = NO_LINE;
+    int k = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += 32) {
+        uint32_t c = b0 + lane < nb ? t.blk[b0 + lane] : 0u;
+        unsigned nz = __ballot_sync(0xffffffffu, c != 0u);
+        while (nz) {
+            const int64_t b = b0 + __ffs(nz) - 1;
+            nz &= nz - 1;
+            const int64_t w = b * 32 + lane;
+            uint32_t word = w < nw ? t.safe[w] : 0u;
+            unsigned has = __ballot_sync(0xffffffffu, word != 0u);
+            while (has) {
+                const int src = __ffs(has) - 1;
+                has &= has - 1;
+                uint32_t wv = __shfl_sync(0xffffffffu, word, src);
+                while (wv) {
+                    const int bit = __ffs(wv) - 1;
+                    wv &= wv - 1;
+                    if (lane == k) sl = (int32_t)((b * 32 + src) * 32 + bit);
+                    k++;
+                }
+            }
+        }
+    }
+    return sl;
+}
+
+// Sequential CacheState.access over the batch, 32 events per step.  Within a
+// chunk only two things are order-dependent: a miss that fills or evicts
+// (it moves the fill pointer / consumes a draw / may evict a later hit's
+// line) and, when the cache is full with no SafeToEvict line, the first hit
+// that makes a line safe (it ends a run of bypasses).  Everything between two
+// such events is decided in parallel from ballots:
+//   fill state (fill < L): hits and the misses that still find empty lines
+//     are decided at once, misses taking lines in order
+//   active state (safe lines exist): hits up to the next miss are HITs (their
+//     InUse->Safe flips commute); that miss then evicts the r-th safe line
+//   starved state (full, no safe line): misses up to the first safe-making hit
+//     are BYPASSes; that hit restores one safe line.
+// A lane's hit status only changes when its line is evicted, so the shared
+// tables are read once per chunk.
 __global__ void __launch_bounds__(32, 1)
 k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* meta,
             uint32_t* g_safe, uint32_t* g_evict, uint32_t* g_blk, uint32_t* g_sup, int smem_bits,
@@ -176,6 +246,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
             int32_t* __restrict__ log_pos, ServeCounters* svc) {
     extern __shared__ uint32_t sm[];
     const int lane = threadIdx.x;
+    const unsigned below = (1u << lane) - 1u;
     const int64_t nw = (L + 31) / 32, nb = (L + 1023) / 1024, ns = (L + 32767) / 32768;
     ExactTables t;
     uint32_t* p = sm;
@@ -204,62 +275,178 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                (uint32_t)meta->rng[4], (uint32_t)meta->rng[5]};
     int64_t fill = meta->fill, safe_count = meta->safe_count;
     int64_t hits = 0, misses = 0, byp = 0, evs = 0, nlog = 0;
+    bool list_ok = safe_count <= 32;
+    int32_t sl = list_ok ? list_rebuild(t, nw, nb) : NO_LINE;
 
-    for (int64_t base = 0; base < n; base += 32) {
-        uint32_t my_ev = base + lane < n ? ev[base + lane] : 0u;
-        int my_kind = GIDS_KIND_BYPASS, my_line = -1;
-        int cnt = n - base < 32 ? (int)(n - base) : 32;
-        for (int k = 0; k < cnt; k++) {
-            uint32_t e = __shfl_sync(0xffffffffu, my_ev, k);
-            int64_t s = (int64_t)(e >> 1) - 1;
-            bool inuse = e & 1u;
-            int kd, ln;
-            if (s >= 0 && !((t.evict[s >> 5] >> (s & 31)) & 1u)) {
-                kd = GIDS_KIND_HIT;
-                ln = (int)s;
-                hits++;
-                if (!inuse && !((t.safe[s >> 5] >> (s & 31)) & 1u)) {  // InUse -> Safe
-                    if (lane == 0) tab_set_safe(t, s);
-                    safe_count++;
-                }
-            } else if (fill < L) {
-                kd = GIDS_KIND_MISS;
-                ln = (int)fill++;
-                misses++;
-                if (!inuse) {
-                    if (lane == 0) tab_set_safe(t, ln);
-                    safe_count++;
-                }
-            } else if (safe_count > 0) {
-                uint32_t r = pcg_bounded32(g, (uint32_t)safe_count);
-                int64_t v = select_safe(t, nw, nb, ns, r);
-                kd = GIDS_KIND_MISS;
-                ln = (int)v;
-                misses++;
-                evs++;
-                if (lane == 0) {
-                    t.evict[v >> 5] |= 1u << (v & 31);
-                    if (inuse) tab_clear_safe(t, v);
-                }
-                if (inuse) safe_count--;
-            } else {
-                kd = GIDS_KIND_BYPASS;
-                ln = -1;
-                byp++;
+    // the event stream is staged through a shared-memory ring by cp.async,
+    // EV_AHEAD chunks ahead, so the sequential loop never waits on HBM
+    __shared__ uint32_t ev_ring[EV_RING][32];
+    const int64_t nchunks = (n + 31) / 32;
+    for (int c = 0; c < EV_AHEAD; c++) {
+        const int64_t i = (int64_t)c * 32 + lane;
+        if (i < n) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&ev_ring[c % EV_RING][lane]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(ev + i));
+        }
+        asm volatile("cp.async.commit_group;");
+    }
+    for (int64_t base = 0, chunk = 0; base < n; base += 32, chunk++) {
+        const int cnt = n - base < 32 ? (int)(n - base) : 32;
+        const unsigned valid = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+        asm volatile("cp.async.wait_group %0;" ::"n"(EV_AHEAD - 1));
+        __syncwarp();
+        const uint32_t my_ev = lane < cnt ? ev_ring[chunk % EV_RING][lane] : 0u;
+        {  // refill: chunk + EV_AHEAD goes where chunk - (EV_RING - EV_AHEAD) was
+            const int64_t nc = chunk + EV_AHEAD;
+            const int64_t i = nc * 32 + lane;
+            if (nc < nchunks && i < n) {
+                const uint32_t sa = (uint32_t)__cvta_generic_to_shared(&ev_ring[nc % EV_RING][lane]);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(ev + i));
             }
-            __syncwarp();
-            if (lane == k) {
-                my_kind = kd;
-                my_line = ln;
+            asm volatile("cp.async.commit_group;");
+        }
+        const int32_t my_s = (int32_t)(my_ev >> 1) - 1;
+        const bool my_inuse = my_ev & 1u;
+        bool hit = lane < cnt && my_s >= 0 && !((t.evict[my_s >> 5] >> (my_s & 31)) & 1u);
+        bool adds = hit && !my_inuse && !((t.safe[my_s >> 5] >> (my_s & 31)) & 1u);
+        int my_kind = GIDS_KIND_BYPASS, my_line = -1;
+        int pos = 0;
+        while (pos < cnt) {
+            const unsigned live = valid & ~((1u << pos) - 1u);
+            const unsigned H = __ballot_sync(0xffffffffu, hit) & live;
+            const unsigned A = __ballot_sync(0xffffffffu, adds) & live;
+            const unsigned M = live & ~H;
+            unsigned span;
+            if (fill < L) {
+                // the first min(#misses, L - fill) misses take empty lines in order
+                const int nm = __popc(M);
+                const int nf = (int64_t)nm < L - fill ? nm : (int)(L - fill);
+                const int stop = nf < nm ? __fns(M, 0, nf + 1) : cnt;
+                span = live & (stop >= 32 ? 0xffffffffu : ((1u << stop) - 1u));
+                const unsigned fm = M & span;
+                const bool mine = (span >> lane) & 1u;
+                if (mine && hit) {
+                    my_kind = GIDS_KIND_HIT;
+                    my_line = my_s;
+                } else if (mine) {
+                    my_kind = GIDS_KIND_MISS;
+                    my_line = (int)(fill + __popc(fm & below));
+                }
+                const bool mk = mine && (hit ? adds : !my_inuse);
+                if (mk) tab_set_safe_atomic(t, my_line);
+                unsigned added = __ballot_sync(0xffffffffu, mk);
+                safe_count += __popc(added);
+                if (list_ok) {
+                    if (safe_count > 32) {
+                        list_ok = false;
+                    } else {
+                        while (added) {
+                            const int l = __ffs(added) - 1;
+                            added &= added - 1;
+                            list_insert(sl, __shfl_sync(0xffffffffu, my_line, l));
+                        }
+                    }
+                }
+                hits += __popc(H & span);
+                misses += __popc(fm);
+                fill += __popc(fm);
+                pos = stop;
+            } else if (safe_count > 0 || A) {
+                // hits up to the next miss (all of them when starved: then the
+                // span ends at the first safe-making hit)
+                int stop;
+                if (safe_count > 0) {
+                    const int m = M ? __ffs(M) - 1 : cnt;
+                    stop = m;
+                } else {
+                    stop = __ffs(A);  // through the first safe-making hit
+                }
+                span = live & (stop >= 32 ? 0xffffffffu : ((1u << stop) - 1u));
+                const bool mine = (span >> lane) & 1u;
+                if (mine) {
+                    my_kind = hit ? GIDS_KIND_HIT : GIDS_KIND_BYPASS;
+                    my_line = hit ? my_s : -1;
+                }
+                const bool mk = mine && adds;
+                if (mk) tab_set_safe_atomic(t, my_s);
+                unsigned added = __ballot_sync(0xffffffffu, mk);
+                byp += __popc(M & span);
+                hits += __popc(H & span);
+                safe_count += __popc(added);
+                if (list_ok) {
+                    if (safe_count > 32) {
+                        list_ok = false;
+                    } else {
+                        while (added) {
+                            const int l = __ffs(added) - 1;
+                            added &= added - 1;
+                            list_insert(sl, __shfl_sync(0xffffffffu, my_s, l));
+                        }
+                    }
+                }
+                pos = stop;
+                if (safe_count > 0 && pos < cnt && ((M >> pos) & 1u)) {
+                    // the evicting miss at lane m = pos
+                    const int m = pos;
+                    const bool inuse_m = __shfl_sync(0xffffffffu, my_inuse, m);
+                    const uint32_t r = pcg_bounded32(g, (uint32_t)safe_count);
+                    int32_t v;
+                    if (list_ok) {
+                        v = __shfl_sync(0xffffffffu, sl, (int)r);
+                        if (inuse_m) list_remove(sl, (int)r);
+                    } else {
+                        __syncwarp();
+                        v = (int32_t)select_safe(t, nw, nb, ns, r);
+                    }
+                    if (lane == 0) {
+                        atomicOr(&t.evict[v >> 5], 1u << (v & 31));
+                        if (inuse_m) {
+                            atomicAnd(&t.safe[v >> 5], ~(1u << (v & 31)));
+                            atomicSub(&t.blk[v >> 10], 1u);
+                            atomicSub(&t.sup[v >> 15], 1u);
+                        }
+                    }
+                    if (my_s == v) {  // a later hit of this chunk lost its line
+                        hit = false;
+                        adds = false;
+                    }
+                    if (lane == m) {
+                        my_kind = GIDS_KIND_MISS;
+                        my_line = v;
+                    }
+                    if (inuse_m) {
+                        safe_count--;
+                        if (!list_ok && safe_count <= 16) {
+                            __syncwarp();
+                            sl = list_rebuild(t, nw, nb);
+                            list_ok = true;
+                        }
+                    }
+                    misses++;
+                    evs++;
+                    pos = m + 1;
+                }
+            } else {
+                // starved and no hit restores a line: the rest of the chunk
+                span = live;
+                const bool mine = (span >> lane) & 1u;
+                if (mine) {
+                    my_kind = hit ? GIDS_KIND_HIT : GIDS_KIND_BYPASS;
+                    my_line = hit ? my_s : -1;
+                }
+                byp += __popc(M);
+                hits += __popc(H);
+                pos = cnt;
             }
         }
+        __syncwarp();
         if (lane < cnt) {
             kind[base + lane] = (int8_t)my_kind;
             line[base + lane] = my_line;
         }
-        unsigned mm = __ballot_sync(0xffffffffu, lane < cnt && my_kind == GIDS_KIND_MISS);
+        const unsigned mm = __ballot_sync(0xffffffffu, lane < cnt && my_kind == GIDS_KIND_MISS);
         if (lane < cnt && my_kind == GIDS_KIND_MISS) {
-            int64_t at = nlog + __popc(mm & ((1u << lane) - 1u));
+            const int64_t at = nlog + __popc(mm & below);
             log_line[at] = my_line;
             log_pos[at] = (int32_t)(base + lane);
         }
@@ -305,16 +492,47 @@ __global__ void k_post_a(const int64_t* __restrict__ uniq, const ServeCounters* 
 // post-pass B: the final inserter owns the line
 __global__ void k_post_b(const int64_t* __restrict__ uniq, const ServeCounters* svc,
                          const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
-                         int32_t* line_node, int32_t* slot_of, const int32_t* __restrict__ last_ins) {
+                         int32_t* line_node, int32_t* slot_of, const int32_t* __restrict__ last_ins,
+                         int32_t* __restrict__ ins) {
     int64_t n = svc->n_log;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t t = log_line[i];
         if (last_ins[t] == (int32_t)i) {
-            int32_t x = (int32_t)uniq[log_pos[i]];
+            int32_t p = log_pos[i];
+            int32_t x = (int32_t)uniq[p];
             slot_of[x] = t;
             line_node[t] = x;
+            ins[p] = t;  // this row is the line's content after the batch
         }
+    }
+}
+
+// tier split of the batch (dataloader.py:262-277), decided before the gather
+__global__ void k_tier_count(const int64_t* __restrict__ uniq, int64_t n,
+                             const int8_t* __restrict__ kind, const int32_t* __restrict__ pinned_off,
+                             ServeCounters* svc) {
+    int64_t a = 0, b = 0, c = 0, d = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int k = kind[p];
+        if (k == GIDS_KIND_HIT) {
+            a++;
+            continue;
+        }
+        d += k == GIDS_KIND_BYPASS;
+        if (pinned_off[uniq[p]] >= 0) b++;
+        else c++;
+    }
+    a = warp_sum64(a);
+    b = warp_sum64(b);
+    c = warp_sum64(c);
+    d = warp_sum64(d);
+    if ((threadIdx.x & 31) == 0) {
+        if (a) atomicAdd((unsigned long long*)&svc->tiers[0], (unsigned long long)a);
+        if (b) atomicAdd((unsigned long long*)&svc->tiers[1], (unsigned long long)b);
+        if (c) atomicAdd((unsigned long long*)&svc->tiers[2], (unsigned long long)c);
+        if (d) atomicAdd((unsigned long long*)&svc->tiers[3], (unsigned long long)d);
     }
 }
 __global__ void k_post_c(const ServeCounters* svc, const int32_t* __restrict__ log_line,
@@ -358,7 +576,8 @@ __global__ void __launch_bounds__(BLOCK)
 k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, int64_t sets,
              const int32_t* __restrict__ set_cnt, const int64_t* __restrict__ set_off,
              int32_t* bucket, int32_t* line_node, int32_t* slot_of, uint32_t* safe_bits,
-             uint64_t key, uint64_t epoch, int8_t* kind, int32_t* line, CacheMeta* meta) {
+             uint64_t key, uint64_t epoch, int8_t* kind, int32_t* line, int32_t* ins,
+             CacheMeta* meta) {
     __shared__ int32_t order[SA_WARPS][SA_SORT_MAX];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int64_t hits = 0, misses = 0, byp = 0, evs = 0;
@@ -395,6 +614,7 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
         int32_t tag = line_node[s * 32 + lane];
         uint32_t safe = safe_bits[s];
         int32_t last = -1;
+        int32_t my_ins = -1;  // batch position of this way's latest insertion
         for (int q = 0; q < cnt; q++) {
             int32_t p;
             if (small) {
@@ -439,7 +659,10 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
                     kd = GIDS_KIND_MISS;
                     ln = (int)(s * 32 + w);
                     misses++;
-                    if (lane == w) tag = x;
+                    if (lane == w) {
+                        tag = x;
+                        my_ins = p;
+                    }
                     if (inuse) safe &= ~(1u << w);
                     else safe |= 1u << w;
                     if (lane == 0) slot_of[x] = ln;
@@ -455,6 +678,7 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
             }
         }
         line_node[s * 32 + lane] = tag;
+        if (my_ins >= 0) ins[my_ins] = (int32_t)(s * 32 + lane);
         if (lane == 0) safe_bits[s] = safe;
         __syncwarp();
     }
@@ -489,14 +713,24 @@ size_t gids_exact_smem_bytes(int64_t L, bool with_bits) {
 }
 
 int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t epoch, float* out,
-                      cudaStream_t st) {
+                      cudaStream_t st, cudaStream_t gst) {
     const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
+    // decision buffers: reuse the set of batch b-2 only after its gather finished
+    h->parity ^= 1;
+    const int par = h->parity;
+    h->kind = h->kind_buf[par];
+    h->line = h->line_buf[par];
+    h->ins = h->ins_buf[par];
+    if (h->gathered_valid[par]) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->gathered[par], 0));
+    gids_harvest_gather(h, par);  // batch b-2's gather timing (profiling only)
     gids_mark(h, 2, st);
     GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
     if (n > 0) {
-        k_window_consume<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
-            uniq, n, h->future, h->reuse, h->slot_of, h->safe_bits, h->blk_cnt, h->sup_cnt,
-            exact ? 1 : 0, h->meta, h->ev);
+        GIDS_CUDA_TRY(cudaMemsetAsync(h->ins, 0xff, sizeof(int32_t) * n, st));
+        int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
+        k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
+                                              h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
+                                              h->meta, h->ev);
         GIDS_LAUNCH_CHECK(h);
         if (exact) {
             size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
@@ -509,20 +743,18 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                                              h->exact_smem ? 1 : 0, h->kind, h->line,
                                              h->log_line, h->log_pos, h->svc);
             GIDS_LAUNCH_CHECK(h);
-            int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
             k_post_a<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
                                           h->slot_of, h->last_ins, h->evict_bits,
                                           h->exact_smem ? 0 : 1);
             GIDS_LAUNCH_CHECK(h);
             k_post_b<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
-                                          h->slot_of, h->last_ins);
+                                          h->slot_of, h->last_ins, h->ins);
             GIDS_LAUNCH_CHECK(h);
             k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
             GIDS_LAUNCH_CHECK(h);
-        } else if (h->sets > 0) {
+        } else {
             GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cnt, 0, sizeof(int32_t) * h->sets, st));
             GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cur, 0, sizeof(int32_t) * h->sets, st));
-            int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
             k_sa_hist<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_cnt);
             GIDS_LAUNCH_CHECK(h);
             int rc = gids_scan_i32_to_i64(h, h->set_cnt, h->sets, h->set_off, st);
@@ -531,19 +763,28 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
             GIDS_LAUNCH_CHECK(h);
             k_sa_process<<<gids_grid(h->sets, SA_WARPS, 16 * GIDS_SMS), BLOCK, 0, st>>>(
                 uniq, h->ev, h->sets, h->set_cnt, h->set_off, h->bucket, h->line_node, h->slot_of,
-                h->safe_bits, h->cfg.evict_key, epoch, h->kind, h->line, h->meta);
+                h->safe_bits, h->cfg.evict_key, epoch, h->kind, h->line, h->ins, h->meta);
             GIDS_LAUNCH_CHECK(h);
-        } else {  // zero lines: every access bypasses
-            gids_set_error("set-associative cache without sets");
-            return GIDS_E_STATE;
         }
-        gids_mark(h, 3, st);
-        int rc = gids_launch_gather(h, uniq, n, out, st);
-        if (rc) return rc;
-        h->serve_timed = h->profiling;
+        k_tier_count<<<g, BLOCK, 0, st>>>(uniq, n, h->kind, h->pinned_off, h->svc);
+        GIDS_LAUNCH_CHECK(h);
     }
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
                                   cudaMemcpyDeviceToHost, st));
+    gids_mark(h, 3, st);
     h->last_serve_n = n;
+    if (n > 0) {
+        if (gst != st) {
+            GIDS_CUDA_TRY(cudaEventRecord(h->decided, st));
+            GIDS_CUDA_TRY(cudaStreamWaitEvent(gst, h->decided, 0));
+        }
+        if (h->profiling) cudaEventRecord(h->gev[par][0], gst);
+        int rc = gids_launch_gather(h, uniq, n, out, gst);
+        if (rc) return rc;
+        GIDS_CUDA_TRY(cudaEventRecord(h->gathered[par], gst));
+        h->gathered_valid[par] = true;
+        h->gather_pending[par] = h->profiling;
+        h->serve_timed = h->profiling;
+    }
     return GIDS_OK;
 }

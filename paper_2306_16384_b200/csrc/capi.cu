@@ -1,4 +1,5 @@
 // capi.cu -- the extern "C" surface declared in include/gids.h.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -148,13 +149,17 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->edges, 2 * h->edge_cap);
     A(h->unique32, h->unique_cap);
     A(h->jump_tab, 128);
+    A(h->rng_dev, 2);
     A(h->sc, 1);
     h->scan_parts_cap = 1024;
     A(h->scan_parts, 2 * h->scan_parts_cap);
     A(h->word_parts, h->scan_parts_cap);
     A(h->ev, h->serve_cap);
-    A(h->kind, h->serve_cap);
-    A(h->line, h->serve_cap);
+    for (int b = 0; b < 2; b++) {
+        A(h->kind_buf[b], h->serve_cap);
+        A(h->line_buf[b], h->serve_cap);
+        A(h->ins_buf[b], h->serve_cap);
+    }
     A(h->log_line, h->serve_cap);
     A(h->log_pos, h->serve_cap);
     A(h->set_cnt, h->sets);
@@ -169,6 +174,8 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     }
     GIDS_CUDA_TRY(cudaMallocHost((void**)&h->sc_host, sizeof(SampleCounters)));
     GIDS_CUDA_TRY(cudaMallocHost((void**)&h->svc_host, sizeof(ServeCounters)));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->jump_host, sizeof(u128) * 128));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->rng_host, sizeof(u128) * 2));
     GIDS_CUDA_TRY(cudaMemset(h->pinned_off, 0xff, sizeof(int32_t) * N));
     GIDS_CUDA_TRY(cudaMemset(h->slot_of, 0xff, sizeof(int32_t) * N));
     GIDS_CUDA_TRY(cudaMemset(h->line_node, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
@@ -192,13 +199,32 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     GIDS_CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                          h->device));
     size_t with_bits = gids_exact_smem_bytes(L, true), without = gids_exact_smem_bytes(L, false);
-    h->exact_smem = with_bits <= (size_t)dev_smem;
-    if (!h->exact_smem && without > (size_t)dev_smem) {
+    const size_t static_smem = 4096;  // k_exact_seq's event ring
+    h->exact_smem = with_bits + static_smem <= (size_t)dev_smem;
+    if (!h->exact_smem && without + static_smem > (size_t)dev_smem) {
         gids_set_error("cache_lines too large for the exact policy (use the set-associative one)");
         gids_destroy(h);
         return GIDS_E_INVALID;
     }
     for (int i = 0; i < 8; i++) GIDS_CUDA_TRY(cudaEventCreate(&h->tev[i]));
+    // gather residency in warps per SM (GIDS_GATHER_WPS).  4 keeps ~1.2 MB of
+    // 16-B loads in flight -- several times the host link's bandwidth-delay
+    // product -- on half the SMs, leaving the rest to sampling and decisions
+    {
+        int wps = 4;
+        if (const char* e = getenv("GIDS_GATHER_WPS")) wps = atoi(e);
+        if (wps < 1) wps = 1;
+        int blocks = (wps * GIDS_SMS + 7) / 8;
+        h->gather_blocks = blocks;
+    }
+    for (int i = 0; i < 2; i++) {
+        GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->gathered[i], cudaEventDisableTiming));
+        for (int j = 0; j < 3; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->gev[i][j]));
+    }
+    GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->decided, cudaEventDisableTiming));
+    h->kind = h->kind_buf[0];
+    h->line = h->line_buf[0];
+    h->ins = h->ins_buf[0];
     *out = h;
     return GIDS_OK;
 }
@@ -211,15 +237,25 @@ int gids_destroy(gids_handle* h) {
                     h->line_node, h->safe_bits, h->evict_bits, h->blk_cnt,   h->sup_cnt,
                     h->reuse,     h->future,   h->meta,       h->last_ins,   h->bm_front,
                     h->bm_all,    h->frontier, h->seeds_dev,  h->take_off,   h->draw_off,
-                    h->edges,     h->unique32, h->jump_tab,   h->sc,         h->scan_parts,
-                    h->word_parts, h->ev,      h->kind,       h->line,       h->log_line,
+                    h->edges,     h->unique32, h->jump_tab,   h->rng_dev,    h->sc,
+                    h->scan_parts,
+                    h->word_parts, h->ev,      h->kind_buf[0], h->line_buf[0], h->ins_buf[0],
+                    h->kind_buf[1], h->line_buf[1], h->ins_buf[1],            h->log_line,
                     h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
                     h->svc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)
         if (h->tev[i]) cudaEventDestroy(h->tev[i]);
+    for (int i = 0; i < 2; i++) {
+        if (h->gathered[i]) cudaEventDestroy(h->gathered[i]);
+        for (int j = 0; j < 3; j++)
+            if (h->gev[i][j]) cudaEventDestroy(h->gev[i][j]);
+    }
+    if (h->decided) cudaEventDestroy(h->decided);
     if (h->sc_host) cudaFreeHost(h->sc_host);
+    if (h->jump_host) cudaFreeHost(h->jump_host);
+    if (h->rng_host) cudaFreeHost(h->rng_host);
     if (h->svc_host) cudaFreeHost(h->svc_host);
     if (h->backing_registered) cudaHostUnregister(const_cast<float*>(h->backing));
     if (h->buffer_registered) cudaHostUnregister(const_cast<float*>(h->buffer_rows));
@@ -301,7 +337,7 @@ int gids_set_constant_buffer(gids_handle* h, const int64_t* node_ids, int64_t k,
     return GIDS_OK;
 }
 
-int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds, const uint64_t rng[6],
+int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds, const uint64_t* rng,
                 void* stream) {
     CHECK_H(h);
     if (n_seeds < 1 || n_seeds > h->max_seeds) {
@@ -319,11 +355,7 @@ int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique, int
                       int64_t* contribution) {
     CHECK_H(h);
     GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
-    if (h->sample_timed) {
-        float ms = 0.f;
-        if (cudaEventElapsedTime(&ms, h->tev[0], h->tev[1]) == cudaSuccess) h->phase_ms[0] += ms;
-        h->sample_timed = false;
-    }
+    gids_harvest_sample(h);
     const SampleCounters& c = *h->sc_host;
     if (c.overflow) {
         gids_set_error("sampler workspace bound exceeded");
@@ -349,6 +381,48 @@ int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, 
     return GIDS_OK;
 }
 
+int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev,
+                             int64_t* sizes_host, void* stream) {
+    CHECK_H(h);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (edges_dev) TRY(gids_launch_export_edges(h, edges_dev, st));
+    if (unique_dev) TRY(gids_launch_export_unique(h, unique_dev, st));
+    if (sizes_host) {
+        // [layer_len[0..L), n_unique, draws, contribution, overflow]
+        const int L = h->cfg.n_layers;
+        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host, h->sc->layer_len, sizeof(int64_t) * L,
+                                      cudaMemcpyDeviceToHost, st));
+        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host + L, &h->sc->n_unique, sizeof(int64_t),
+                                      cudaMemcpyDeviceToHost, st));
+        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host + L + 1, &h->sc->layer_draw_base[L],
+                                      sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host + L + 2, &h->sc->contribution,
+                                      sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, st));
+    }
+    return GIDS_OK;
+}
+
+int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* unique_cap) {
+    CHECK_H(h);
+    *edge_cap = h->edge_cap;
+    *unique_cap = h->unique_cap;
+    return GIDS_OK;
+}
+
+int gids_sampler_rng(gids_handle* h, uint64_t words_out[6]) {
+    CHECK_H(h);
+    GIDS_CUDA_TRY(cudaDeviceSynchronize());
+    u128 st[2];
+    GIDS_CUDA_TRY(cudaMemcpy(st, h->rng_dev, sizeof(st), cudaMemcpyDeviceToHost));
+    words_out[0] = st[0].hi;
+    words_out[1] = st[0].lo;
+    words_out[2] = st[1].hi;
+    words_out[3] = st[1].lo;
+    words_out[4] = 0;
+    words_out[5] = 0;
+    return GIDS_OK;
+}
+
 int gids_window_push(gids_handle* h, const int64_t* nodes, int64_t n, void* stream) {
     CHECK_H(h);
     return gids_launch_window(h, nodes, n, +1, (cudaStream_t)stream);
@@ -359,7 +433,7 @@ int gids_window_pop(gids_handle* h, const int64_t* nodes, int64_t n, void* strea
 }
 
 int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
-               float* out_dev, void* stream) {
+               float* out_dev, void* stream, void* gather_stream) {
     CHECK_H(h);
     if (n < 0 || n > h->serve_cap) {
         gids_set_error("batch larger than the serving workspace");
@@ -370,20 +444,17 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
         return GIDS_E_STATE;
     }
     h->last_stream = (cudaStream_t)stream;
-    return gids_launch_serve(h, unique_dev, n, epoch, out_dev, (cudaStream_t)stream);
+    return gids_launch_serve(h, unique_dev, n, epoch, out_dev, (cudaStream_t)stream,
+                             gather_stream ? (cudaStream_t)gather_stream : (cudaStream_t)stream);
 }
 
 int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
     CHECK_H(h);
     GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
     if (h->serve_timed) {
-        float a = 0.f, b = 0.f, c2 = 0.f;
-        cudaEventElapsedTime(&a, h->tev[2], h->tev[3]);
-        cudaEventElapsedTime(&b, h->tev[3], h->tev[4]);
-        cudaEventElapsedTime(&c2, h->tev[4], h->tev[5]);
-        h->phase_ms[1] += a;
-        h->phase_ms[2] += b;
-        h->phase_ms[3] += c2;
+        float a = 0.f;
+        if (cudaEventElapsedTime(&a, h->tev[2], h->tev[3]) == cudaSuccess) h->phase_ms[1] += a;
+        cudaGetLastError();
         h->phase_ms[4] += 1.0;
         h->serve_timed = false;
     }
@@ -473,12 +544,18 @@ int gids_set_profiling(gids_handle* h, int on) {
     CHECK_H(h);
     h->profiling = on != 0;
     h->sample_timed = h->serve_timed = false;
+    h->gather_pending[0] = h->gather_pending[1] = false;
     for (int i = 0; i < 5; i++) h->phase_ms[i] = 0.0;
     return GIDS_OK;
 }
 
 int gids_phase_times(gids_handle* h, double out_ms[5]) {
     CHECK_H(h);
+    if (h->sample_timed) {
+        gids_harvest_sample(h);
+    }
+    gids_harvest_gather(h, 0);
+    gids_harvest_gather(h, 1);
     for (int i = 0; i < 5; i++) out_ms[i] = h->phase_ms[i];
     return GIDS_OK;
 }

@@ -66,70 +66,32 @@ __device__ __forceinline__ void copy_row(const float* __restrict__ src, float* _
     }
 }
 
-__device__ __forceinline__ void add_counts(int64_t* tiers, int64_t a, int64_t b, int64_t c,
-                                           int64_t d) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-        c += __shfl_xor_sync(0xffffffffu, c, o);
-        d += __shfl_xor_sync(0xffffffffu, d, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (a) atomicAdd((unsigned long long*)&tiers[0], (unsigned long long)a);
-        if (b) atomicAdd((unsigned long long*)&tiers[1], (unsigned long long)b);
-        if (c) atomicAdd((unsigned long long*)&tiers[2], (unsigned long long)c);
-        if (d) atomicAdd((unsigned long long*)&tiers[3], (unsigned long long)d);
-    }
-}
-
 __global__ void __launch_bounds__(BLOCK)
 k_gather_hits(int64_t n, const int8_t* __restrict__ kind, const int32_t* __restrict__ line,
-              const float* __restrict__ cache_rows, float* __restrict__ out, int64_t dim,
-              ServeCounters* svc) {
+              const float* __restrict__ cache_rows, float* __restrict__ out, int64_t dim) {
     const int lane = threadIdx.x & 31;
-    int64_t hits = 0;
     for (int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); p < n;
          p += (int64_t)gridDim.x * WARPS) {
         if (kind[p] != GIDS_KIND_HIT) continue;
         copy_row(cache_rows + (int64_t)line[p] * dim, out + p * dim, nullptr, dim, lane);
-        hits += lane == 0;
     }
-    add_counts(svc->tiers, hits, 0, 0, 0);
 }
 
 __global__ void __launch_bounds__(BLOCK)
 k_gather_host(const int64_t* __restrict__ uniq, int64_t n, const int8_t* __restrict__ kind,
-              const int32_t* __restrict__ line, const int32_t* __restrict__ line_node,
-              const int32_t* __restrict__ pinned_off, const float* __restrict__ buffer_rows,
-              const float* __restrict__ backing, float* __restrict__ cache_rows,
-              float* __restrict__ out, int64_t dim, ServeCounters* svc) {
+              const int32_t* __restrict__ ins_line, const int32_t* __restrict__ pinned_off,
+              const float* __restrict__ buffer_rows, const float* __restrict__ backing,
+              float* __restrict__ cache_rows, float* __restrict__ out, int64_t dim) {
     const int lane = threadIdx.x & 31;
-    int64_t nbuf = 0, nsto = 0, nbyp = 0;
     for (int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); p < n;
          p += (int64_t)gridDim.x * WARPS) {
-        const int k = kind[p];
-        if (k == GIDS_KIND_HIT) continue;
+        if (kind[p] == GIDS_KIND_HIT) continue;
         const int32_t x = (int32_t)uniq[p];
         const int32_t off = pinned_off[x];
-        const float* src;
-        if (off >= 0) {
-            src = buffer_rows + (int64_t)off * dim;
-            nbuf += lane == 0;
-        } else {
-            src = backing + (int64_t)x * dim;
-            nsto += lane == 0;
-        }
-        float* ins = nullptr;
-        if (k == GIDS_KIND_MISS) {
-            int32_t t = line[p];
-            if (line_node[t] == x) ins = cache_rows + (int64_t)t * dim;
-        } else {
-            nbyp += lane == 0;
-        }
-        copy_row(src, out + p * dim, ins, dim, lane);
+        const float* src = off >= 0 ? buffer_rows + (int64_t)off * dim : backing + (int64_t)x * dim;
+        const int32_t t = ins_line[p];
+        copy_row(src, out + p * dim, t >= 0 ? cache_rows + (int64_t)t * dim : nullptr, dim, lane);
     }
-    add_counts(svc->tiers, 0, nbuf, nsto, nbyp);
 }
 
 // synthetic_feature_rows (graph.py:256-275), one thread per cell
@@ -175,15 +137,17 @@ __global__ void k_verify(uint64_t seed_mix, const int64_t* __restrict__ nodes, i
 int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* out,
                        cudaStream_t st) {
     const int64_t dim = h->row_floats;
-    int grid = gids_grid(n, WARPS, 16 * GIDS_SMS);
-    k_gather_hits<<<grid, BLOCK, 0, st>>>(n, h->kind, h->line, h->cache_rows, out, dim, h->svc);
+    // grid sized by GIDS_GATHER_WPS (capi.cu): a few warps per SM already
+    // saturate the host link; the rest of the GPU stays free for the next
+    // batch's sampling and cache decisions on the control stream
+    int grid = gids_grid(n, WARPS, h->gather_blocks);
+    k_gather_hits<<<grid, BLOCK, 0, st>>>(n, h->kind, h->line, h->cache_rows, out, dim);
     GIDS_LAUNCH_CHECK(h);
-    gids_mark(h, 4, st);
-    k_gather_host<<<grid, BLOCK, 0, st>>>(uniq, n, h->kind, h->line, h->line_node, h->pinned_off,
-                                          h->buffer_rows, h->backing, h->cache_rows, out, dim,
-                                          h->svc);
+    if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
+    k_gather_host<<<grid, BLOCK, 0, st>>>(uniq, n, h->kind, h->ins, h->pinned_off,
+                                          h->buffer_rows, h->backing, h->cache_rows, out, dim);
     GIDS_LAUNCH_CHECK(h);
-    gids_mark(h, 5, st);
+    if (h->profiling) cudaEventRecord(h->gev[h->parity][2], st);
     return GIDS_OK;
 }
 

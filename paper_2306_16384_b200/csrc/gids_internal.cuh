@@ -194,6 +194,9 @@ struct gids_handle {
     int32_t* unique32;     // [front_cap_all]
     int64_t unique_cap;
     u128* jump_tab;        // [64][2] {A_i, H_i} for the sampler stream's inc
+    u128* jump_host;       // pinned staging of the table
+    u128* rng_dev;         // [2] device-resident sampler stream: state, inc
+    u128* rng_host;        // pinned staging
     uint64_t jump_inc_hi, jump_inc_lo;
     bool jump_valid;
     SampleCounters* sc;    // device
@@ -205,8 +208,18 @@ struct gids_handle {
     // serve workspace
     int64_t serve_cap;     // max unique per batch
     uint32_t* ev;          // [serve_cap] packed (line+1)<<1 | inuse_after
-    int8_t* kind;          // [serve_cap]
-    int32_t* line;         // [serve_cap]
+    // decisions are double-buffered: the gather of batch b reads set b&1
+    // while the decide phase of batch b+1 writes the other one
+    int8_t* kind_buf[2];   // [serve_cap] GIDS_KIND_*
+    int32_t* line_buf[2];  // [serve_cap] line read (hit) or taken (miss), -1
+    int32_t* ins_buf[2];   // [serve_cap] line this node's row must be written to, -1
+    int8_t* kind;          // current set (alias)
+    int32_t* line;
+    int32_t* ins;
+    int parity;
+    cudaEvent_t gathered[2];  // gather of the last batch that used each set
+    bool gathered_valid[2];
+    cudaEvent_t decided;      // decide phase of the last served batch
     int32_t* log_line;     // [serve_cap] exact-policy insertion log
     int32_t* log_pos;      // [serve_cap]
     int32_t* set_cnt;      // [sets]
@@ -217,13 +230,41 @@ struct gids_handle {
     ServeCounters* svc_host;  // pinned mirror
     int64_t last_serve_n;
     bool exact_smem;       // exact-policy tables fit in shared memory
+    int gather_blocks;     // gather grid (resident blocks of 8 warps)
 
     // phase timing (gids_set_profiling)
     bool profiling;
-    cudaEvent_t tev[8];    // 0,1 sample; 2..5 serve phase boundaries
+    cudaEvent_t tev[8];    // 0,1 sample; 2,3 decide phase
+    cudaEvent_t gev[2][3]; // per decision set: gather start, hits done, host rows done
+    bool gather_pending[2];
     bool sample_timed, serve_timed;
     double phase_ms[5];
 };
+
+// fold the finished gather timing of decision set `par` into phase_ms
+// (profiling only; timing failures are dropped and must not leave a sticky
+// error for the next launch check)
+inline void gids_harvest_gather(gids_handle* h, int par) {
+    if (!h->gather_pending[par]) return;
+    h->gather_pending[par] = false;
+    float b = 0.f, c = 0.f;
+    if (cudaEventSynchronize(h->gev[par][2]) == cudaSuccess &&
+        cudaEventElapsedTime(&b, h->gev[par][0], h->gev[par][1]) == cudaSuccess &&
+        cudaEventElapsedTime(&c, h->gev[par][1], h->gev[par][2]) == cudaSuccess) {
+        h->phase_ms[2] += b;
+        h->phase_ms[3] += c;
+    }
+    cudaGetLastError();
+}
+inline void gids_harvest_sample(gids_handle* h) {
+    if (!h->sample_timed) return;
+    h->sample_timed = false;
+    float ms = 0.f;
+    if (cudaEventSynchronize(h->tev[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, h->tev[0], h->tev[1]) == cudaSuccess)
+        h->phase_ms[0] += ms;
+    cudaGetLastError();
+}
 
 inline void gids_mark(gids_handle* h, int i, cudaStream_t st) {
     if (h->profiling) cudaEventRecord(h->tev[i], st);
@@ -240,9 +281,10 @@ int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* 
 int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_words,
                        cudaStream_t st);
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
+int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st);
 // cache.cu
 int gids_launch_serve(gids_handle* h, const int64_t* unique, int64_t n, uint64_t epoch,
-                      float* out, cudaStream_t st);
+                      float* out, cudaStream_t st, cudaStream_t gst);
 int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delta,
                        cudaStream_t st);
 int gids_launch_contribution(gids_handle* h, cudaStream_t st);

@@ -50,8 +50,9 @@ __global__ void __launch_bounds__(SAMPLE_BLOCK)
 k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                const int32_t* __restrict__ front, const int64_t* __restrict__ take_off,
                const int64_t* __restrict__ draw_off, const SampleCounters* __restrict__ sc,
-               int layer, int fanout, u128 s0, const u128* __restrict__ tab,
-               int64_t* __restrict__ edges, uint32_t* bm_front, uint32_t* bm_all) {
+               int layer, int fanout, const u128* __restrict__ rng_state,
+               const u128* __restrict__ tab, int64_t* __restrict__ edges, uint32_t* bm_front,
+               uint32_t* bm_all) {
     extern __shared__ int64_t j_smem[];  // fanout > 32: swap targets per warp
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -59,6 +60,7 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
     int64_t ebase = 0;
     for (int l = 0; l < layer; l++) ebase += sc->layer_len[l];
     const uint64_t dbase = (uint64_t)sc->layer_draw_base[layer];
+    const u128 s0 = rng_state[0];  // stream state at the start of this batch
     int64_t* jw = j_smem + (int64_t)wib * fanout;
 
     for (int64_t i = (int64_t)blockIdx.x * SAMPLE_WARPS + wib; i < nf;
@@ -121,6 +123,28 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
     }
 }
 
+__global__ void k_rng_set(u128* rng_state, u128 state, u128 inc) {
+    rng_state[0] = state;
+    rng_state[1] = inc;
+}
+
+// the batch consumed `draws` doubles: move the device-resident stream past them
+__global__ void k_rng_advance(u128* rng_state, const SampleCounters* sc, int n_layers,
+                              const u128* __restrict__ tab) {
+    rng_state[0] = jump(rng_state[0], (uint64_t)sc->layer_draw_base[n_layers], tab);
+}
+
+// edges of all layers (device-side count) into a caller buffer
+__global__ void k_copy_edges(const int64_t* __restrict__ src, const SampleCounters* sc,
+                             int n_layers, int64_t* __restrict__ dst) {
+    int64_t e = 0;
+    for (int l = 0; l < n_layers; l++) e += sc->layer_len[l];
+    const int64_t n = 2 * e;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
 // int32 ids -> int64 (export of unique_nodes)
 __global__ void k_widen(const int32_t* __restrict__ in, const SampleCounters* sc,
                         int64_t* __restrict__ out) {
@@ -150,19 +174,26 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
             gids_set_error("fanout above 1024 is not supported by the CUDA sampler");
             return GIDS_E_INVALID;
         }
-    if (!h->jump_valid || h->jump_inc_hi != w[2] || h->jump_inc_lo != w[3]) {
-        u128 tab[128];
-        build_jump_table(w[2], w[3], tab);
-        GIDS_CUDA_TRY(cudaMemcpyAsync(h->jump_tab, tab, sizeof(tab), cudaMemcpyHostToDevice, st));
-        // the table is staged from the stack: make the copy complete first
-        GIDS_CUDA_TRY(cudaStreamSynchronize(st));
-        h->jump_valid = true;
-        h->jump_inc_hi = w[2];
-        h->jump_inc_lo = w[3];
+    if (h->sample_timed) {  // previous batch's sampling time (profiling only)
+        gids_harvest_sample(h);
     }
-    u128 s0{w[1], w[0]};
+    if (w) {  // (re)seed the device-resident stream from the host Generator
+        if (!h->jump_valid || h->jump_inc_hi != w[2] || h->jump_inc_lo != w[3]) {
+            build_jump_table(w[2], w[3], h->jump_host);
+            GIDS_CUDA_TRY(cudaMemcpyAsync(h->jump_tab, h->jump_host, sizeof(u128) * 128,
+                                          cudaMemcpyHostToDevice, st));
+            GIDS_CUDA_TRY(cudaStreamSynchronize(st));  // staging buffer is reused
+            h->jump_valid = true;
+            h->jump_inc_hi = w[2];
+            h->jump_inc_lo = w[3];
+        }
+        k_rng_set<<<1, 1, 0, st>>>(h->rng_dev, u128{w[1], w[0]}, u128{w[3], w[2]});
+        GIDS_LAUNCH_CHECK(h);
+    } else if (!h->jump_valid) {
+        gids_set_error("sampler stream not seeded (pass the Generator state once)");
+        return GIDS_E_STATE;
+    }
 
-    gids_mark(h, 0, st);
     GIDS_CUDA_TRY(cudaMemsetAsync(h->sc, 0, sizeof(SampleCounters), st));
     k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
                                                                      h->bm_front, h->bm_all);
@@ -182,7 +213,7 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
         int64_t bound = l == 0 ? n_seeds : h->front_cap;
         int grid = gids_grid(bound, SAMPLE_WARPS, 16 * GIDS_SMS);
         k_sample_layer<<<grid, SAMPLE_BLOCK, smem, st>>>(
-            h->indptr, h->indices, h->frontier, h->take_off, h->draw_off, h->sc, l, f, s0,
+            h->indptr, h->indices, h->frontier, h->take_off, h->draw_off, h->sc, l, f, h->rng_dev,
             h->jump_tab, h->edges, h->bm_front, h->bm_all);
         GIDS_LAUNCH_CHECK(h);
         rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
@@ -193,10 +224,19 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
     if (rc) return rc;
     rc = gids_launch_contribution(h, st);
     if (rc) return rc;
+    k_rng_advance<<<1, 1, 0, st>>>(h->rng_dev, h->sc, c.n_layers, h->jump_tab);
+    GIDS_LAUNCH_CHECK(h);
     gids_mark(h, 1, st);
     h->sample_timed = h->profiling;
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
                                   cudaMemcpyDeviceToHost, st));
+    return GIDS_OK;
+}
+
+int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st) {
+    k_copy_edges<<<gids_grid(2 * h->edge_cap, 256, 8 * GIDS_SMS), 256, 0, st>>>(
+        h->edges, h->sc, h->cfg.n_layers, edges_dev);
+    GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }
 

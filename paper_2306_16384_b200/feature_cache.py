@@ -59,12 +59,17 @@ class CacheStats:
 class WindowBuffer:
     """Ring of up to ``depth`` future per-iteration unique-node lists."""
 
-    def __init__(self, depth: int, handle: _native.Handle | None = None):
+    def __init__(self, depth: int, handle: _native.Handle | None = None,
+                 stream: int | None = None):
         if depth < 0:
             raise ValueError("depth must be non-negative")
         self.depth = depth
         self.lists: deque = deque()
         self._h = handle
+        self._stream = stream
+
+    def _st(self) -> int:
+        return self._stream if self._stream is not None else _native.stream_ptr(self._h.device)
 
     def __len__(self) -> int:
         return len(self.lists)
@@ -77,14 +82,14 @@ class WindowBuffer:
             raise CacheProtocolError("iteration list must be ascending and unique")
         self.lists.append(nodes)
         if self._h is not None:
-            self._h.window_push(nodes, _native.stream_ptr(self._h.device))
+            self._h.window_push(nodes, self._st())
 
     def pop_iteration(self):
         if not self.lists:
             raise CacheProtocolError("window is empty")
         nodes = self.lists.popleft()
         if self._h is not None:
-            self._h.window_pop(nodes, _native.stream_ptr(self._h.device))
+            self._h.window_pop(nodes, self._st())
         return nodes
 
 

@@ -80,10 +80,38 @@ class RunSummary:
     total_time_us: float
 
 
-@dataclass
 class _Queued:
-    batch: MiniBatch
-    storage_accesses: int
+    """A sampled batch whose outputs may still be in flight on the control
+    stream; ``resolve()`` waits for them (normally long finished) and fixes
+    the sizes, the run-ahead contribution and the host Generator's offset."""
+
+    __slots__ = ("seeds", "edges", "unique", "sizes", "event", "batch", "storage_accesses")
+
+    def __init__(self, seeds, edges, unique, sizes, event):
+        self.seeds, self.edges, self.unique, self.sizes, self.event = \
+            seeds, edges, unique, sizes, event
+        self.batch = None
+        self.storage_accesses = None
+
+    def resolve(self, n_layers: int, rng) -> None:
+        if self.batch is not None:
+            return
+        self.event.synchronize()
+        sz = self.sizes.tolist()
+        lens, n_unique, draws, contrib, overflow = (sz[:n_layers], sz[n_layers],
+                                                    sz[n_layers + 1], sz[n_layers + 2],
+                                                    sz[n_layers + 3])
+        if overflow:
+            raise _native.GidsError("sampler workspace bound exceeded")
+        layers, off = [], 0
+        for ln in lens:
+            layers.append(self.edges[off:off + ln])
+            off += ln
+        if draws:
+            rng.bit_generator.advance(draws)
+        self.batch = MiniBatch(seeds=self.seeds, layers=layers,
+                               unique_nodes=self.unique[:n_unique])
+        self.storage_accesses = contrib
 
 
 def _seed_stream(cfg: PipelineConfig, n: int, work_ss, shuffle_ss):
@@ -170,8 +198,12 @@ class Dataloader:
         self._h.set_constant_buffer(self.buffer.node_ids,
                                     self.buffer.pinned if self.buffer.pinned is not None
                                     else self.buffer.rows)
+        # two streams: sampling + cache decisions (ctl) and row movement (gather);
+        # the decisions of batch b+1 overlap the host-link gather of batch b
+        self._ctl = torch.cuda.Stream(self.device, priority=-1)  # decisions first
+        self._gat = torch.cuda.Stream(self.device)
         self.cache = GpuCacheView(self._h, self.spec.page_bytes)
-        self.window = WindowBuffer(cfg.window_depth, self._h)
+        self.window = WindowBuffer(cfg.window_depth, self._h, self._ctl.cuda_stream)
         self._sampler = Sampler(self._h, self.graph.num_nodes, cfg.fanouts)
 
         self.base_threshold = required_accesses(self.spec, cfg.target_fraction)
@@ -184,8 +216,15 @@ class Dataloader:
         self._batches = _seed_stream(cfg, self.graph.num_nodes, work_ss, shuffle_ss)
         self._exhausted = False
         self._pending: deque[_Queued] = deque()
-        self._pending_storage = 0
+        self._resolved_storage = 0  # sum of resolved contributions of pending batches
         self._ringed = 0
+        self._rng_on_device = False
+        self._edge_cap, self._unique_cap = self._h.sample_capacity()
+        ring = cfg.runahead_cap + 4
+        self._sizes = torch.zeros((ring, len(cfg.fanouts) + 5), dtype=torch.int64,
+                                  pin_memory=True)
+        self._sizes_np = self._sizes.numpy()
+        self._sizes_next = 0
 
         self._iteration = 0
         self._clock_us = Fraction(0)
@@ -225,35 +264,70 @@ class Dataloader:
     def effective_threshold(self) -> int:
         return math.ceil(self.base_threshold / max(EMA_EPSILON, 1.0 - self.redirect_ema))
 
+    @property
+    def _pending_storage(self) -> int:
+        """Sum of the pending batches' contributions (resolves them all)."""
+        for q in self._pending:
+            self._resolve(q)
+        return self._resolved_storage
+
+    def _resolve(self, q: _Queued) -> None:
+        if q.batch is None:
+            q.resolve(len(self.cfg.fanouts), self._sampler_rng)
+            self._resolved_storage += q.storage_accesses
+
+    def _storage_at_least(self, bound: int) -> bool:
+        """pending_storage >= bound, resolving (oldest first) only as needed."""
+        if self._resolved_storage >= bound:
+            return True
+        for q in self._pending:
+            if q.batch is None:
+                self._resolve(q)
+                if self._resolved_storage >= bound:
+                    return True
+        return False
+
     def _sample_one(self) -> bool:
+        """Launch one batch on the control stream; sizes are read lazily."""
+        import torch
         try:
             seeds = next(self._batches)
         except StopIteration:
             self._exhausted = True
             return False
         seeds = check_seeds(seeds, self.graph.num_nodes)
-        st = _native.stream_ptr(self.device)
-        self._sampler.launch(seeds, self._sampler_rng, st)
-        batch, contrib = self._sampler.collect(seeds, self._sampler_rng, st)
-        self._pending.append(_Queued(batch, contrib))
-        self._pending_storage += contrib
+        st = self._ctl.cuda_stream
+        words = None if self._rng_on_device else pcg_words(self._sampler_rng)
+        self._h.sample(seeds, words, st)
+        self._rng_on_device = True
+        with torch.cuda.stream(self._ctl):
+            edges = torch.empty((self._edge_cap, 2), dtype=torch.int64, device=self._torch_dev)
+            unique = torch.empty(self._unique_cap, dtype=torch.int64, device=self._torch_dev)
+        sizes = self._sizes[self._sizes_next]
+        self._sizes_next = (self._sizes_next + 1) % len(self._sizes)
+        self._h.sample_export_async(edges, unique, sizes, st)
+        ev = torch.cuda.Event()
+        ev.record(self._ctl)
+        self._pending.append(_Queued(seeds, edges, unique, sizes, ev))
         return True
 
     def run_ahead(self) -> None:
         want = self.cfg.window_depth + 1
         while not self._exhausted:
             short_window = len(self._pending) < want
-            short_threshold = self._pending_storage < self.effective_threshold()
-            if not (short_window or short_threshold):
+            # need_threshold = pending_storage < effective_threshold(); only
+            # resolved as far as the comparison requires
+            if not short_window and self._storage_at_least(self.effective_threshold()):
                 break
             if len(self._pending) >= self.cfg.runahead_cap:
                 break
-            if not short_window and self._pending_storage == 0:
+            if not short_window and not self._storage_at_least(1):
                 break
             self._sample_one()
         while self._ringed < min(self.window.depth, len(self._pending)):
-            self.window.push_iteration(self._pending[self._ringed].batch.unique_nodes,
-                                       trusted=True)
+            q = self._pending[self._ringed]
+            self._resolve(q)
+            self.window.push_iteration(q.batch.unique_nodes, trusted=True)
             self._ringed += 1
 
     # -- serving (dataloader.py:232-299)
@@ -264,7 +338,7 @@ class Dataloader:
             raise StopIteration
         inflight = self._pending_storage
         entry = self._pending.popleft()
-        self._pending_storage -= entry.storage_accesses
+        self._resolved_storage -= entry.storage_accesses
         if self._ringed > 0:
             self.window.pop_iteration()
             self._ringed -= 1
@@ -272,11 +346,20 @@ class Dataloader:
 
         batch = entry.batch
         unique = batch.unique_nodes
-        rows = torch.empty((unique.numel(), self.features.dim), dtype=torch.float32,
-                           device=self._torch_dev)
-        self._h.serve(unique, self._iteration, rows, _native.stream_ptr(self.device))
-        c = self._h.serve_counts()
+        with torch.cuda.stream(self._gat):
+            rows = torch.empty((unique.numel(), self.features.dim), dtype=torch.float32,
+                               device=self._torch_dev)
+        unique.record_stream(self._gat)
+        self._h.serve(unique, self._iteration, rows, self._ctl.cuda_stream,
+                      self._gat.cuda_stream)
+        c = self._h.serve_counts()  # waits for the decisions only, not the gather
         self.last_counts = c
+        # hand the batch to the caller's stream without blocking the host
+        cur = torch.cuda.current_stream(self.device)
+        cur.wait_stream(self._gat)
+        cur.wait_stream(self._ctl)
+        for t in (rows, unique, *batch.layers):
+            t.record_stream(cur)
         if self.cfg.verify_gather:
             self._verify(unique, rows)
         stats = self._account(c.sampled, c.cache_hits, c.cpu_buffer_hits, c.storage,
@@ -287,7 +370,7 @@ class Dataloader:
     def _verify(self, unique, rows) -> None:
         if self.features.seed is not None:
             bad = _native.verify_rows(self.device, self.features.seed, unique, rows,
-                                      _native.stream_ptr(self.device))
+                                      self._gat.cuda_stream)
         else:
             expect = self.features.rows(unique.cpu().numpy())
             bad = int((rows.cpu().numpy() != expect).any(axis=1).sum())
@@ -326,6 +409,8 @@ class Dataloader:
         return self.next_batch()
 
     def close(self) -> None:
+        import torch
+        torch.cuda.synchronize(self.device)
         self._h.close()
 
 

@@ -83,14 +83,22 @@ class Sampler:
     def launch(self, seeds: np.ndarray, rng, stream: int) -> None:
         self.h.sample(seeds, pcg_words(rng), stream)
 
-    def collect(self, seeds: np.ndarray, rng, stream: int):
-        """Sizes -> tensors -> export; advances rng.  Returns (MiniBatch, contribution)."""
+    def collect(self, seeds: np.ndarray, rng, stream: int, torch_stream=None):
+        """Sizes -> tensors -> export; advances rng.  Returns (MiniBatch, contribution).
+
+        ``torch_stream`` (the torch.cuda.Stream behind ``stream``) owns the
+        output tensors when given; otherwise the current stream does."""
+        import contextlib
+
         import torch
         lens, n_unique, draws, contrib = self.h.sample_sizes()
         dev = torch.device("cuda", self.h.device)
         total = int(lens.sum())
-        edges = torch.empty((total, 2), dtype=torch.int64, device=dev)
-        unique = torch.empty(n_unique, dtype=torch.int64, device=dev)
+        ctx = torch.cuda.stream(torch_stream) if torch_stream is not None else \
+            contextlib.nullcontext()
+        with ctx:
+            edges = torch.empty((total, 2), dtype=torch.int64, device=dev)
+            unique = torch.empty(n_unique, dtype=torch.int64, device=dev)
         self.h.sample_export(edges, unique, stream)
         layers, off = [], 0
         for ln in lens.tolist():
