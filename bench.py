@@ -39,13 +39,26 @@ WORKLOADS = {
     "c1": dict(num_nodes=100_000, avg_degree=12.0, degree_model="uniform", feature_dim=1024,
                fanouts=[10, 15], batch_size=1024, cache_lines=100_000, buffer_fraction=0.0,
                window_depth=8, consume_rate=0.0, seed=42),
+    # configs[3]: ogbn-papers100M shape, 1 GPU; SURVEY.md s8 C4:
+    # 2,097,152 cache lines (8 GiB of 4 KiB pages), 10% constant CPU buffer
+    "c4": dict(num_nodes=111_059_956, avg_degree=1_615_685_872 / 111_059_956,
+               degree_model="uniform", feature_dim=128, fanouts=[15, 10, 5], batch_size=4096,
+               cache_lines=2_097_152, buffer_fraction=0.10, window_depth=8, consume_rate=0.0,
+               seed=42, gids_generator="device"),
 }
+DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c4": "setassoc"}
 WORKLOAD_NAMES = {
     "c2": "IGB-small-shaped 1M nodes / 12M edges (uniform), 1024-d fp32, fanout [10,15], "
           "batch 1024, cache 100K lines (10%) + 10% constant CPU buffer, W=8",
     "c1": "synthetic 100K nodes / 1.2M edges (uniform), 1024-d fp32, fanout [10,15], "
           "batch 1024, all rows fit the GPU cache, W=8",
+    "c4": "ogbn-papers100M-shaped 111,059,956 nodes / 1,615,685,872 edges (uniform), 128-d "
+          "fp32, fanout [15,10,5], batch 4096, cache 2,097,152 lines + 10% constant CPU "
+          "buffer, W=8, 1 GPU",
 }
+L2_NOTE = {"c1": "inputs larger than L2 (410 MB HBM cache, 282 MB gathered per step)",
+           "c2": "inputs larger than L2 (4.1 GB host table, 410 MB HBM cache)",
+           "c4": "inputs larger than L2 (56.9 GB host table, 1.07 GB HBM cache, 7.4 GB graph)"}
 
 
 def load_peaks() -> dict:
@@ -121,7 +134,9 @@ def oracle_inputs(cfg, graph=None, table=None, buffer_nodes=None, stream_seed=No
     from _setup import resolve
     from paper_2306_16384_b200.loader import _seed_stream
     from paper_2306_16384_b200.sampling import pcg_words
-    if graph is None:
+    if graph is None and cfg.gids_generator == "device":
+        graph, buffer_nodes = host_device_shape(cfg)
+    elif graph is None:
         r = resolve(cfg, with_table=table is None)
         graph, buffer_nodes = r["graph"], r["buffer_nodes"]
         table = r["table"] if table is None else table
@@ -135,19 +150,40 @@ def oracle_inputs(cfg, graph=None, table=None, buffer_nodes=None, stream_seed=No
                 base_threshold=required_accesses(cfg.ssd_spec(), cfg.target_fraction))
 
 
-def oracle_loader(cfg, r):
+def host_device_shape(cfg):
+    """Graph and pinned set of a gids_generator='device' config built on the host
+    cores by the oracle's restatements (the same generator definition and the
+    float64-identical reverse PageRank), for the CPU legs."""
+    from oracle import oracle as O
+    from paper_2306_16384_b200.csc import GraphCsc
+    threads = len(os.sched_getaffinity(0))
+    graph_ss = np.random.SeedSequence(cfg.seed).spawn(6)[0]
+    n, e = cfg.num_nodes, int(round(cfg.num_nodes * cfg.avg_degree))
+    ip, ix = O.generate_uniform(n, e, int(graph_ss.generate_state(1)[0]), threads=threads)
+    g = GraphCsc(num_nodes=n, num_edges=e, indptr=ip, indices=ix)
+    row_bytes = cfg.feature_dim * 4
+    k = cfg.resolved_buffer_bytes(n, row_bytes) // row_bytes
+    if k <= 0:
+        return g, np.empty(0, np.int64)
+    scores, _, _ = O.reverse_pagerank(ip, ix, threads=threads)
+    # top_k_nodes (cpu_buffer.py:102-109): descending score, ties to the lower id
+    return g, np.argsort(-scores, kind="stable")[:k].astype(np.int64)
+
+
+def oracle_loader(cfg, r, buffer_rows=None):
     from oracle import oracle as O
     return O.OracleLoader(r["graph"].indptr, r["graph"].indices, r["table"], r["buffer_nodes"],
                           r["batches"], cfg.fanouts, r["sampler_words"], r["evict_words"],
                           cfg.resolved_cache_lines(), cfg.window_depth, r["base_threshold"],
-                          policy=cfg.gids_policy, evict_key=r["evict_seed"], keep_rows=False)
+                          policy=cfg.gids_policy, evict_key=r["evict_seed"], keep_rows=False,
+                          buffer_rows=buffer_rows)
 
 
 def cpu_baseline_sample(cfg, dl, seconds: float = 12.0) -> dict:
     """The oracle loader (C restatement of the reference path), 1 host thread,
     on the same workload and graph: batches served in ~``seconds``."""
     r = oracle_inputs(cfg, dl.graph, dl.features.table, dl.buffer.node_ids)
-    ld = oracle_loader(cfg, r)
+    ld = oracle_loader(cfg, r, buffer_rows=dl.buffer.rows)
     ld.next_batch()  # warm
     t0 = time.perf_counter()
     n = 0
@@ -163,16 +199,19 @@ def cpu_baseline_sample(cfg, dl, seconds: float = 12.0) -> dict:
 _SHARED: dict = {}
 
 
-def _ref_worker(proc, steps, q):
+def _ref_worker(proc, steps, budget_s, q):
     cfg, base = _SHARED["cfg"], _SHARED["base"]
     r = oracle_inputs(cfg, base["graph"], base["table"], base["buffer_nodes"],
                       stream_seed=cfg.seed + proc)
-    ld = oracle_loader(cfg, r)
+    ld = oracle_loader(cfg, r, buffer_rows=base["buffer_rows"])
     times = []
-    for _ in range(steps):
+    t_start = time.perf_counter()
+    for i in range(steps):
         t0 = time.perf_counter()
         ld.next_batch()
         times.append(time.perf_counter() - t0)
+        if i >= 1 and time.perf_counter() - t_start > budget_s:
+            break  # bounded sample: the run must end within a few minutes
     q.put(times)
 
 
@@ -192,23 +231,29 @@ def run_reference(args, cfg_dict) -> None:
         return
     cfg = make_config(cfg_dict)
     procs = len(os.sched_getaffinity(0))
+    t_setup = time.perf_counter()
     base = oracle_inputs(cfg, table=np.zeros((1, 1), np.float32))
     g = base["graph"]
     feat_seed = int(np.random.SeedSequence(cfg.seed).spawn(6)[1].generate_state(1)[0])
-    base["table"] = O.feature_rows(feat_seed, np.arange(g.num_nodes), cfg.feature_dim)
+    base["table"] = O.feature_table(feat_seed, g.num_nodes, cfg.feature_dim, threads=procs)
+    base["buffer_rows"] = np.ascontiguousarray(base["table"][base["buffer_nodes"]])
+    setup_s = time.perf_counter() - t_setup
     _SHARED.update(cfg=cfg, base=base)
     ctx = mp.get_context("fork")
     q = ctx.Queue()
     total = args.warmup + args.steps
-    ps = [ctx.Process(target=_ref_worker, args=(p, total, q)) for p in range(procs)]
+    budget_s = 150.0
+    ps = [ctx.Process(target=_ref_worker, args=(p, total, budget_s, q)) for p in range(procs)]
     for p in ps:
         p.start()
     results = [q.get() for _ in ps]
     for p in ps:
         p.join()
-    rates = [args.steps / sum(t[args.warmup:]) for t in results]
+    # per process: timed batches after the warm-up ones (at least one timed)
+    timed = [t[min(args.warmup, len(t) - 1):] for t in results]
+    rates = [len(t) / sum(t) for t in timed]
     value = float(sum(rates))
-    step_ms = float(np.mean([np.mean(t[args.warmup:]) for t in results]) * 1e3)
+    step_ms = float(np.mean([np.mean(t) for t in timed]) * 1e3)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "minibatches/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -216,8 +261,10 @@ def run_reference(args, cfg_dict) -> None:
             "config": {"workload": WORKLOAD_NAMES[args.workload], "policy": cfg.gids_policy},
             "cpu_baseline": {"value": value, "unit": "minibatches/s", "cores": procs,
                              "kind": "port",
-                             "sample": f"{procs} processes x {args.steps} timed batches each "
-                                       f"(+{args.warmup} warm), streams seeded 42+p"},
+                             "sample": f"{procs} processes x {min(len(t) for t in timed)}-"
+                                       f"{max(len(t) for t in timed)} timed batches each "
+                                       f"(+{args.warmup} warm, {budget_s:.0f}s cap), streams "
+                                       f"seeded {cfg.seed}+p; setup {setup_s:.0f}s"},
             "e2e": {"value": value, "unit": "minibatches/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -230,10 +277,12 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="gids", choices=["gids", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--policy", default="exact", choices=["exact", "setassoc"])
+    ap.add_argument("--policy", default=None, choices=["exact", "setassoc"],
+                    help="cache policy (default: exact at c1/c2, setassoc at c4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    args.policy = args.policy or DEFAULT_POLICY[args.workload]
     cfg_dict = {**WORKLOADS[args.workload], "gids_policy": args.policy}
 
     if args.impl == "reference":
@@ -264,7 +313,8 @@ def main() -> None:
     torch.cuda.synchronize(local)
     if world > 1:
         dist.barrier()
-    h.set_profiling(True)
+
+    # pass 1 (e2e): K steps through the public call, no per-phase events
     launches0 = h.launch_count()
     clk, clk_path = start_clock_sampler(local)
     rows_host = rows_hbm = sampled = 0
@@ -283,6 +333,15 @@ def main() -> None:
     clocks = stop_clock_sampler(clk, clk_path)
     ms = start.elapsed_time(end)
     launches = h.launch_count() - launches0
+
+    # pass 2 (device pipeline): the next K steps with per-phase CUDA events on
+    # each launching stream
+    if world > 1:
+        dist.barrier()
+    h.set_profiling(True)
+    for _ in range(args.steps):
+        dl.next_batch()
+    torch.cuda.synchronize(local)
     phases = h.phase_times()
     h.set_profiling(False)
     t = torch.tensor([ms], dtype=torch.float64, device=local)
@@ -325,7 +384,7 @@ def main() -> None:
         "data": "synthetic (reference generate_synthetic graph + synthetic_feature_rows table)",
         "config": {"workload": WORKLOAD_NAMES[args.workload], "policy": args.policy,
                    "parallelism": f"dp{world}", "global_batch": cfg.batch_size * world,
-                   "l2": "inputs larger than L2 (4.1 GB host table, 410 MB HBM cache)"},
+                   "l2": L2_NOTE[args.workload]},
         "gather_gbps": gather_gbs,
         "tiers_per_step": {"sampled": sampled / args.steps,
                            "cache_hits": float(tiers[0]) / args.steps,
@@ -348,7 +407,8 @@ def main() -> None:
                                     "peak": hbm_peak, "unit": "GB/s"}},
         "value_definition": "device pipeline: 1 / max(per-step sampling+decision time on the "
                             "control stream, per-step gather time on the gather stream), CUDA "
-                            "events on each launching stream, max over ranks",
+                            "events on each launching stream (a second pass of K steps after "
+                            "the e2e pass), max over ranks",
         "e2e": {"value": e2e_value, "unit": "minibatches/s", "ms_per_step": ms_max / args.steps,
                 "h2d_bytes_per_step": int(cfg.batch_size * 8 + host_bytes_per_launch),
                 "d2h_bytes_per_step": 256,

@@ -169,6 +169,31 @@ GIDS_API int gids_synthesize_rows(int device, uint64_t seed, int64_t row0, int64
 GIDS_API int gids_verify_rows(int device, uint64_t seed, const int64_t* nodes_dev, int64_t n, int32_t dim,
                      const float* rows_dev, int64_t* bad, void* stream);
 
+/* ---- setup-time graph work on the GPU ---- */
+
+/* Uniform random graph with exactly num_edges distinct (src,dst) pairs, in
+ * CSC form in HBM (indptr int64[N+1], indices int32[E], sources ascending per
+ * destination) -- the reference's "uniform" degree model (graph.py:164-180)
+ * made counter-based so it runs at 1.6B edges; definition in
+ * csrc/graph_setup.cu.  Fails with GIDS_E_INVALID if an in-degree exceeds 1024. */
+GIDS_API int gids_generate_uniform_graph(int device, int64_t num_nodes, int64_t num_edges,
+                                         uint64_t seed, int64_t* indptr_dev, int32_t* indices_dev,
+                                         void* stream);
+
+/* reverse_pagerank (cpu_buffer.py:26-74, unit edge weights) over a device
+ * CSC; scores_dev double[N] receives the same float64 values the reference
+ * computes (bit-identical), *iterations / *converged as PageRankResult. */
+GIDS_API int gids_reverse_pagerank(int device, int64_t num_nodes, int64_t num_edges,
+                                   const int64_t* indptr_dev, const int32_t* indices_dev,
+                                   double damping, double tol, int32_t max_iter,
+                                   double* scores_dev, int32_t* iterations, int32_t* converged,
+                                   void* stream);
+
+/* GraphCsc already in HBM (indptr int64[N+1], indices int32[E], device
+ * pointers): copied into the handle like gids_load_graph. */
+GIDS_API int gids_load_graph_device(gids_handle* h, const int64_t* indptr_dev,
+                                    const int32_t* indices_dev);
+
 /* Per-phase device time (CUDA events on the launching stream), accumulated
  * while profiling is on: out_ms[0] sampling, [1] window + cache policy,
  * [2] hit gather (HBM), [3] host-tier gather (zero-copy), [4] batches

@@ -556,3 +556,245 @@ void or_feature_rows(uint64_t seed, const int64_t* nodes, int64_t n, int64_t dim
             out[i * dim + col] = (float)(z >> 40) / 16777216.0f;
         }
 }
+
+/* ------------------------------------------------------------------------
+ * Setup-time restatements used by the C4/C5-scale checks and the CPU
+ * baseline at those shapes (still TEST INFRASTRUCTURE ONLY).
+ * ---------------------------------------------------------------------- */
+#include <pthread.h>
+
+typedef struct {
+    void (*fn)(void* arg, int64_t lo, int64_t hi);
+    void* arg;
+    int64_t n;
+    int nthreads, t;
+} par_job_t;
+
+static void* par_entry(void* p) {
+    par_job_t* j = (par_job_t*)p;
+    int64_t per = (j->n + j->nthreads - 1) / j->nthreads;
+    int64_t lo = per * j->t, hi = lo + per < j->n ? lo + per : j->n;
+    if (lo < hi) j->fn(j->arg, lo, hi);
+    return NULL;
+}
+static void par_for(int64_t n, int nthreads, void (*fn)(void*, int64_t, int64_t), void* arg) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    par_job_t jobs[256];
+    for (int t = 0; t < nthreads; t++) {
+        jobs[t] = (par_job_t){fn, arg, n, nthreads, t};
+        pthread_create(&th[t], NULL, par_entry, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+}
+
+/* synthetic_feature_rows (graph.py:256-275) for rows [row0, row0+n), threaded */
+typedef struct { uint64_t seed; int64_t row0, dim; float* out; } feat_job_t;
+static void feat_part(void* a, int64_t lo, int64_t hi) {
+    feat_job_t* j = (feat_job_t*)a;
+    for (int64_t i = lo; i < hi; i++) {
+        int64_t node = j->row0 + i;
+        or_feature_rows(j->seed, &node, 1, j->dim, j->out + i * j->dim);
+    }
+}
+void or_feature_table(uint64_t seed, int64_t row0, int64_t n, int64_t dim, float* out,
+                      int nthreads) {
+    feat_job_t j = {seed, row0, dim, out};
+    par_for(n, nthreads, feat_part, &j);
+}
+
+/*
+ * Uniform graph generator of csrc/graph_setup.cu (its header states the
+ * definition): dst(e) = hi64(mix64(s_dst + e) * N); segment of v drawn as
+ * src(v,k,a) = hi64(mix64(mix64(s_src ^ v) + (a<<32) + k) * N), sorted, and
+ * repeats at sorted position r redrawn with src(v, r, a) for a = 1, 2, ...
+ * Output in the reference's GraphCsc dtypes (u64).
+ */
+static inline uint64_t hi64(uint64_t a, uint64_t b) { return (uint64_t)(((u128)a * b) >> 64); }
+
+typedef struct { uint64_t s; int64_t n; uint32_t* cnt; } hist_job_t;
+static void hist_part(void* a, int64_t lo, int64_t hi) {
+    hist_job_t* j = (hist_job_t*)a;
+    for (int64_t e = lo; e < hi; e++)
+        __atomic_fetch_add(&j->cnt[hi64(mix64(j->s + (uint64_t)e), (uint64_t)j->n)], 1u,
+                           __ATOMIC_RELAXED);
+}
+typedef struct { uint64_t s; int64_t n; const uint64_t* indptr; uint64_t* indices; int bad; } fill_job_t;
+static int cmp_u64(const void* a, const void* b) {
+    uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+    return x < y ? -1 : x > y;
+}
+static void fill_part(void* a, int64_t lo, int64_t hi) {
+    fill_job_t* j = (fill_job_t*)a;
+    const uint64_t n = (uint64_t)j->n;
+    for (int64_t v = lo; v < hi; v++) {
+        uint64_t* seg = j->indices + j->indptr[v];
+        int64_t deg = (int64_t)(j->indptr[v + 1] - j->indptr[v]);
+        if (deg == 0) continue;
+        if (deg > 1024) { j->bad = 1; continue; }
+        uint64_t zv = mix64(j->s ^ (uint64_t)v);
+        for (int64_t k = 0; k < deg; k++) seg[k] = hi64(mix64(zv + (uint64_t)k), n);
+        for (uint64_t att = 1;; att++) {
+            qsort(seg, (size_t)deg, sizeof(uint64_t), cmp_u64);
+            int rep = 0;
+            /* decide every repeat against the sorted array before rewriting */
+            uint64_t prev = seg[0];
+            for (int64_t r = 1; r < deg; r++) {
+                uint64_t cur = seg[r];
+                if (cur == prev) {
+                    seg[r] = hi64(mix64(zv + (att << 32) + (uint64_t)r), n);
+                    rep = 1;
+                }
+                prev = cur;
+            }
+            if (!rep) break;
+        }
+    }
+}
+int or_generate_uniform(int64_t n, int64_t e, uint64_t seed, uint64_t* indptr, uint64_t* indices,
+                        int nthreads) {
+    uint32_t* cnt = (uint32_t*)calloc((size_t)n, sizeof(uint32_t));
+    if (!cnt) return -1;
+    hist_job_t hj = {mix64(seed ^ 0x243F6A8885A308D3ULL), n, cnt};
+    par_for(e, nthreads, hist_part, &hj);
+    indptr[0] = 0;
+    for (int64_t v = 0; v < n; v++) indptr[v + 1] = indptr[v] + cnt[v];
+    free(cnt);
+    fill_job_t fj = {mix64(seed ^ 0x13198A2E03707344ULL), n, indptr, indices, 0};
+    par_for(n, nthreads, fill_part, &fj);
+    return fj.bad ? -2 : 0;
+}
+
+/*
+ * reverse_pagerank (cpu_buffer.py:26-74, unit weights), float64-identical to
+ * the reference: np.bincount accumulates each node's shares in edge order,
+ * i.e. by ascending destination, so the pull over per-source lists sorted by
+ * destination reproduces it term for term; sums of x[sink] and |nxt - x|
+ * follow numpy's pairwise summation (loops_utils.h: 8 accumulators over
+ * blocks of <= 128, split at n/2 rounded down to a multiple of 8).
+ */
+static double pw_sum_gen(const double* a, const int64_t* idx, int64_t n) {
+#define PW_AT(i) (idx ? a[idx[(i)]] : a[(i)])
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; i++) r += PW_AT(i);
+        return r;
+    } else if (n <= 128) {
+        double r[8];
+        int64_t i;
+        for (int j = 0; j < 8; j++) r[j] = PW_AT(j);
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += PW_AT(i + j);
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += PW_AT(i);
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return pw_sum_gen(a, idx, n2) + pw_sum_gen(idx ? a : a + n2, idx ? idx + n2 : NULL, n - n2);
+    }
+#undef PW_AT
+}
+/* numpy-order pairwise sum of a[0..n) (exported for the tests) */
+double or_pairwise_sum(const double* a, int64_t n) { return pw_sum_gen(a, NULL, n); }
+
+typedef struct {
+    const uint64_t* indptr; const uint64_t* indices;
+    uint64_t* tptr; uint32_t* cur; uint32_t* towner; uint32_t* cnt;
+    const double* y; double* nxt; const double* x; double* diff; double damping, c;
+} pr_job_t;
+static void pr_count(void* a, int64_t lo, int64_t hi) {
+    pr_job_t* j = (pr_job_t*)a;
+    for (int64_t e = lo; e < hi; e++) __atomic_fetch_add(&j->cnt[j->indices[e]], 1u, __ATOMIC_RELAXED);
+}
+static void pr_scatter(void* a, int64_t lo, int64_t hi) {
+    pr_job_t* j = (pr_job_t*)a;
+    for (int64_t v = lo; v < hi; v++)
+        for (uint64_t e = j->indptr[v]; e < j->indptr[v + 1]; e++) {
+            uint64_t u = j->indices[e];
+            uint32_t at = __atomic_fetch_add(&j->cur[u], 1u, __ATOMIC_RELAXED);
+            j->towner[j->tptr[u] + at] = (uint32_t)v;
+        }
+}
+static int cmp_u32(const void* a, const void* b) {
+    uint32_t x = *(const uint32_t*)a, y = *(const uint32_t*)b;
+    return x < y ? -1 : x > y;
+}
+static void pr_sortlists(void* a, int64_t lo, int64_t hi) {
+    pr_job_t* j = (pr_job_t*)a;
+    for (int64_t u = lo; u < hi; u++)
+        qsort(j->towner + j->tptr[u], (size_t)(j->tptr[u + 1] - j->tptr[u]), sizeof(uint32_t),
+              cmp_u32);
+}
+static void pr_pull(void* a, int64_t lo, int64_t hi) {
+    pr_job_t* j = (pr_job_t*)a;
+    for (int64_t u = lo; u < hi; u++) {
+        double acc = 0.0;
+        for (uint64_t k = j->tptr[u]; k < j->tptr[u + 1]; k++) acc += j->y[j->towner[k]];
+        double v = acc * j->damping;
+        v = v + j->c;
+        j->nxt[u] = v;
+        double d = v - j->x[u];
+        j->diff[u] = d < 0 ? -d : d;
+    }
+}
+int or_reverse_pagerank(const uint64_t* indptr, const uint64_t* indices, int64_t n, double damping,
+                        double tol, int max_iter, double* scores, int* iters, int* conv,
+                        int nthreads) {
+    int64_t e = (int64_t)indptr[n];
+    pr_job_t j;
+    memset(&j, 0, sizeof(j));
+    j.indptr = indptr;
+    j.indices = indices;
+    j.cnt = (uint32_t*)calloc((size_t)n, sizeof(uint32_t));
+    j.cur = (uint32_t*)calloc((size_t)n, sizeof(uint32_t));
+    j.tptr = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n + 1));
+    j.towner = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(e > 0 ? e : 1));
+    double* denom = (double*)malloc(sizeof(double) * (size_t)n);
+    double* x = (double*)malloc(sizeof(double) * (size_t)n);
+    double* nxt = (double*)malloc(sizeof(double) * (size_t)n);
+    double* y = (double*)malloc(sizeof(double) * (size_t)n);
+    double* diff = (double*)malloc(sizeof(double) * (size_t)n);
+    int64_t* sinks = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+    par_for(e, nthreads, pr_count, &j);
+    j.tptr[0] = 0;
+    for (int64_t u = 0; u < n; u++) j.tptr[u + 1] = j.tptr[u] + j.cnt[u];
+    par_for(n, nthreads, pr_scatter, &j);
+    par_for(n, nthreads, pr_sortlists, &j);
+    int64_t ns = 0;
+    for (int64_t v = 0; v < n; v++) {
+        uint64_t d = indptr[v + 1] - indptr[v];
+        denom[v] = d == 0 ? 1.0 : (double)d;
+        if (d == 0) sinks[ns++] = v;
+        x[v] = 1.0 / (double)n;
+    }
+    double teleport = (1.0 - damping) / (double)n;
+    int it = 0, converged = 0;
+    while (it < max_iter) {
+        it++;
+        for (int64_t v = 0; v < n; v++) y[v] = x[v] / denom[v];
+        double s = pw_sum_gen(x, sinks, ns);
+        j.c = teleport + damping * s / (double)n;
+        j.damping = damping;
+        j.y = y;
+        j.x = x;
+        j.nxt = nxt;
+        j.diff = diff;
+        par_for(n, nthreads, pr_pull, &j);
+        double delta = pw_sum_gen(diff, NULL, n);
+        double* t = x;
+        x = nxt;
+        nxt = t;
+        if (delta < tol) {
+            converged = 1;
+            break;
+        }
+    }
+    memcpy(scores, x, sizeof(double) * (size_t)n);
+    *iters = it;
+    *conv = converged;
+    free(j.cnt); free(j.cur); free(j.tptr); free(j.towner);
+    free(denom); free(x); free(nxt); free(y); free(diff); free(sinks);
+    return 0;
+}

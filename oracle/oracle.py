@@ -65,6 +65,14 @@ def lib() -> C.CDLL:
         L.or_cache_lines_snapshot.argtypes = [vp, vp, vp]
         L.or_gather.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, vp, vp, C.c_int64, vp]
         L.or_feature_rows.argtypes = [C.c_uint64, vp, C.c_int64, C.c_int64, vp]
+        L.or_feature_table.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int64, vp, C.c_int]
+        L.or_generate_uniform.argtypes = [C.c_int64, C.c_int64, C.c_uint64, vp, vp, C.c_int]
+        L.or_generate_uniform.restype = C.c_int
+        L.or_pairwise_sum.argtypes = [vp, C.c_int64]
+        L.or_pairwise_sum.restype = C.c_double
+        L.or_reverse_pagerank.argtypes = [vp, vp, C.c_int64, C.c_double, C.c_double, C.c_int,
+                                          vp, vp, vp, C.c_int]
+        L.or_reverse_pagerank.restype = C.c_int
         _lib = L
         del u64p, i64p, f64p
     return _lib
@@ -221,6 +229,44 @@ def feature_rows(seed: int, nodes, dim: int) -> np.ndarray:
     return out
 
 
+def feature_table(seed: int, num_nodes: int, dim: int, threads: int = 1,
+                  out: np.ndarray | None = None) -> np.ndarray:
+    """The whole synthetic table (graph.py:256-275), computed on ``threads`` host cores."""
+    if out is None:
+        out = np.empty((num_nodes, dim), np.float32)
+    lib().or_feature_table(seed & ((1 << 64) - 1), 0, num_nodes, dim, _ptr(out), threads)
+    return out
+
+
+def generate_uniform(num_nodes: int, num_edges: int, seed: int, threads: int = 1):
+    """CPU restatement of the GPU uniform generator (csrc/graph_setup.cu header).
+    Returns (indptr u64[N+1], indices u64[E])."""
+    indptr = np.zeros(num_nodes + 1, np.uint64)
+    indices = np.zeros(max(num_edges, 1), np.uint64)
+    rc = lib().or_generate_uniform(num_nodes, num_edges, seed & ((1 << 64) - 1), _ptr(indptr),
+                                   _ptr(indices), threads)
+    if rc:
+        raise ValueError("generate_uniform: a node's in-degree exceeds 1024")
+    return indptr, indices[:num_edges]
+
+
+def pairwise_sum(a: np.ndarray) -> float:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return float(lib().or_pairwise_sum(_ptr(a), len(a)))
+
+
+def reverse_pagerank(indptr, indices, damping=0.85, tol=1e-8, max_iter=200, threads=1):
+    """cpu_buffer.py:26-74 (unit weights) in C: (scores, converged, iterations)."""
+    ip = np.ascontiguousarray(indptr, dtype=np.uint64)
+    ix = np.ascontiguousarray(indices, dtype=np.uint64)
+    n = len(ip) - 1
+    scores = np.zeros(n, np.float64)
+    it, conv = C.c_int(), C.c_int()
+    lib().or_reverse_pagerank(_ptr(ip), _ptr(ix) if len(ix) else None, n, damping, tol,
+                              max_iter, _ptr(scores), C.byref(it), C.byref(conv), threads)
+    return scores, bool(conv.value), it.value
+
+
 def required_accesses_optane(target_fraction: float = 0.95) -> int:
     # storage.py:92-104 for the intel-optane preset (25 us + 5 us, 1.5 M IOPS)
     from fractions import Fraction
@@ -241,7 +287,7 @@ class OracleLoader:
     def __init__(self, indptr, indices, table, buffer_nodes, seed_batches, fanouts,
                  sampler_words, evict_words, cache_lines, window_depth, base_threshold,
                  policy="exact", ways=32, evict_key=0, redirect_ema_alpha=0.2,
-                 runahead_cap=256, keep_rows=True):
+                 runahead_cap=256, keep_rows=True, buffer_rows=None):
         self.indptr = np.ascontiguousarray(indptr, dtype=np.uint64)
         self.indices = np.ascontiguousarray(indices, dtype=np.uint64)
         self.n = len(self.indptr) - 1
@@ -250,8 +296,11 @@ class OracleLoader:
         self.buffer_nodes = np.asarray(buffer_nodes, dtype=np.int64)
         self.pinned_off = np.full(self.n, -1, np.int32)
         self.pinned_off[self.buffer_nodes] = np.arange(len(self.buffer_nodes), dtype=np.int32)
-        self.buffer_rows = np.ascontiguousarray(table[self.buffer_nodes]) if len(
-            self.buffer_nodes) else np.zeros((0, self.dim), np.float32)
+        if buffer_rows is not None:  # rows of buffer_nodes, already gathered
+            self.buffer_rows = buffer_rows
+        else:
+            self.buffer_rows = np.ascontiguousarray(table[self.buffer_nodes]) if len(
+                self.buffer_nodes) else np.zeros((0, self.dim), np.float32)
         self.batches = iter(seed_batches)
         self.fanouts = list(fanouts)
         self.words = np.ascontiguousarray(sampler_words, dtype=np.uint64).copy()

@@ -85,6 +85,10 @@ def lib() -> C.CDLL:
         "gids_synthesize_rows": ([i32, u64, i64, i64, i32, vp, vp], C.c_int),
         "gids_verify_rows": ([i32, u64, vp, i64, i32, vp, vp, vp], C.c_int),
         "gids_launch_count": ([vp], i64),
+        "gids_generate_uniform_graph": ([i32, i64, i64, u64, vp, vp, vp], C.c_int),
+        "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
+                                   vp, vp], C.c_int),
+        "gids_load_graph_device": ([vp, vp, vp], C.c_int),
         "gids_set_profiling": ([vp, C.c_int], C.c_int),
         "gids_phase_times": ([vp, vp], C.c_int),
     }
@@ -107,7 +111,8 @@ def exported_symbols() -> list[str]:
             "gids_serve", "gids_serve_counts", "gids_serve_decisions", "gids_cache_stats",
             "gids_cache_rng", "gids_cache_lines", "gids_cache_capacity",
             "gids_synthesize_rows", "gids_verify_rows", "gids_set_profiling",
-            "gids_phase_times", "gids_launch_count"]
+            "gids_phase_times", "gids_launch_count", "gids_generate_uniform_graph",
+            "gids_reverse_pagerank", "gids_load_graph_device"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -179,6 +184,10 @@ class Handle:
         ip = np.ascontiguousarray(indptr, dtype=np.uint64)
         ix = np.ascontiguousarray(indices, dtype=np.uint64)
         check(lib().gids_load_graph(self.h, ip.ctypes.data, ix.ctypes.data), "load_graph")
+
+    def load_graph_device(self, indptr, indices) -> None:
+        """indptr int64[N+1] / indices int32[E] CUDA tensors (copied into the handle)."""
+        check(lib().gids_load_graph_device(self.h, _p(indptr), _p(indices)), "load_graph_device")
 
     def set_backing(self, table, n_rows: int) -> None:
         self._keep.append(table)
@@ -289,3 +298,29 @@ def verify_rows(device: int, seed: int, nodes, rows, stream: int) -> int:
     check(lib().gids_verify_rows(device, seed & ((1 << 64) - 1), _p(nodes), nodes.numel(),
                                  rows.shape[1], _p(rows), C.byref(bad), stream), "verify_rows")
     return bad.value
+
+
+def generate_uniform_graph(device: int, num_nodes: int, num_edges: int, seed: int):
+    """GPU uniform generator (csrc/graph_setup.cu): (indptr int64, indices int32) on cuda."""
+    import torch
+    dev = torch.device("cuda", device)
+    indptr = torch.empty(num_nodes + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(max(num_edges, 1), dtype=torch.int32, device=dev)
+    check(lib().gids_generate_uniform_graph(device, num_nodes, num_edges,
+                                            seed & ((1 << 64) - 1), _p(indptr), _p(indices),
+                                            stream_ptr(device)), "generate_uniform_graph")
+    return indptr, indices[:num_edges]
+
+
+def reverse_pagerank(device: int, indptr, indices, damping: float = 0.85, tol: float = 1e-8,
+                     max_iter: int = 200):
+    """cpu_buffer.py:26-74 on the GPU over a device CSC: (scores f64 cuda, converged, iters)."""
+    import torch
+    n = indptr.numel() - 1
+    scores = torch.empty(n, dtype=torch.float64, device=indptr.device)
+    it, conv = C.c_int32(), C.c_int32()
+    check(lib().gids_reverse_pagerank(device, n, indices.numel(), _p(indptr),
+                                      _p(indices) if indices.numel() else None, float(damping),
+                                      float(tol), int(max_iter), _p(scores), C.byref(it),
+                                      C.byref(conv), stream_ptr(device)), "reverse_pagerank")
+    return scores, bool(conv.value), int(it.value)

@@ -207,11 +207,15 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         return GIDS_E_INVALID;
     }
     for (int i = 0; i < 8; i++) GIDS_CUDA_TRY(cudaEventCreate(&h->tev[i]));
-    // gather residency in warps per SM (GIDS_GATHER_WPS).  4 keeps ~1.2 MB of
+    for (int i = 0; i < gids_handle::SRING; i++)
+        for (int j = 0; j < 2; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->sev[i][j]));
+    // gather residency in warps per SM (GIDS_GATHER_WPS).  2 keeps ~0.6 MB of
     // 16-B loads in flight -- several times the host link's bandwidth-delay
-    // product -- on half the SMs, leaving the rest to sampling and decisions
+    // product -- and leaves the SMs to sampling and decisions: measured on
+    // B200 (profiles/r01_bench_wps_b7_*.json) 1/2/4 warps per SM give the same
+    // link rate, while 4 slows the overlapped exact-policy decisions by 30%
     {
-        int wps = 4;
+        int wps = 2;
         if (const char* e = getenv("GIDS_GATHER_WPS")) wps = atoi(e);
         if (wps < 1) wps = 1;
         int blocks = (wps * GIDS_SMS + 7) / 8;
@@ -247,6 +251,9 @@ int gids_destroy(gids_handle* h) {
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)
         if (h->tev[i]) cudaEventDestroy(h->tev[i]);
+    for (int i = 0; i < gids_handle::SRING; i++)
+        for (int j = 0; j < 2; j++)
+            if (h->sev[i][j]) cudaEventDestroy(h->sev[i][j]);
     for (int i = 0; i < 2; i++) {
         if (h->gathered[i]) cudaEventDestroy(h->gathered[i]);
         for (int j = 0; j < 3; j++)
@@ -303,6 +310,27 @@ int gids_load_graph(gids_handle* h, const uint64_t* indptr, const uint64_t* indi
     return GIDS_OK;
 }
 
+int gids_load_graph_device(gids_handle* h, const int64_t* indptr, const int32_t* indices) {
+    CHECK_H(h);
+    if (!indptr || (h->E > 0 && !indices)) {
+        gids_set_error("null graph array");
+        return GIDS_E_INVALID;
+    }
+    int64_t ends[2] = {0, 0};
+    GIDS_CUDA_TRY(cudaMemcpy(&ends[0], indptr, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    GIDS_CUDA_TRY(cudaMemcpy(&ends[1], indptr + h->N, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (ends[0] != 0 || ends[1] != h->E) {
+        gids_set_error("indptr must start at 0 and end at num_edges");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaMemcpy(h->indptr, indptr, sizeof(int64_t) * (h->N + 1),
+                             cudaMemcpyDeviceToDevice));
+    if (h->E > 0)
+        GIDS_CUDA_TRY(cudaMemcpy(h->indices, indices, sizeof(int32_t) * h->E,
+                                 cudaMemcpyDeviceToDevice));
+    return GIDS_OK;
+}
+
 int gids_set_backing(gids_handle* h, const float* table, int64_t n_rows) {
     CHECK_H(h);
     if (n_rows != h->N) {
@@ -355,7 +383,7 @@ int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique, int
                       int64_t* contribution) {
     CHECK_H(h);
     GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
-    gids_harvest_sample(h);
+    gids_harvest_sample(h, false);
     const SampleCounters& c = *h->sc_host;
     if (c.overflow) {
         gids_set_error("sampler workspace bound exceeded");
@@ -543,7 +571,8 @@ int gids_cache_lines(gids_handle* h, int64_t* node_host, int8_t* state_host) {
 int gids_set_profiling(gids_handle* h, int on) {
     CHECK_H(h);
     h->profiling = on != 0;
-    h->sample_timed = h->serve_timed = false;
+    gids_harvest_sample(h, true);  // drop intervals of the previous session
+    h->serve_timed = false;
     h->gather_pending[0] = h->gather_pending[1] = false;
     for (int i = 0; i < 5; i++) h->phase_ms[i] = 0.0;
     return GIDS_OK;
@@ -551,9 +580,7 @@ int gids_set_profiling(gids_handle* h, int on) {
 
 int gids_phase_times(gids_handle* h, double out_ms[5]) {
     CHECK_H(h);
-    if (h->sample_timed) {
-        gids_harvest_sample(h);
-    }
+    gids_harvest_sample(h, true);
     gids_harvest_gather(h, 0);
     gids_harvest_gather(h, 1);
     for (int i = 0; i < 5; i++) out_ms[i] = h->phase_ms[i];

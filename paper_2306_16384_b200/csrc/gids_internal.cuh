@@ -234,10 +234,15 @@ struct gids_handle {
 
     // phase timing (gids_set_profiling)
     bool profiling;
-    cudaEvent_t tev[8];    // 0,1 sample; 2,3 decide phase
+    cudaEvent_t tev[8];    // 2,3 decide phase
+    // sampling time: a ring of (start, end) event pairs harvested without
+    // blocking (cudaEventQuery), so profiling does not serialise run-ahead
+    static constexpr int SRING = 64;
+    cudaEvent_t sev[SRING][2];
+    int sev_head, sev_count;
     cudaEvent_t gev[2][3]; // per decision set: gather start, hits done, host rows done
     bool gather_pending[2];
-    bool sample_timed, serve_timed;
+    bool serve_timed;
     double phase_ms[5];
 };
 
@@ -256,14 +261,40 @@ inline void gids_harvest_gather(gids_handle* h, int par) {
     }
     cudaGetLastError();
 }
-inline void gids_harvest_sample(gids_handle* h) {
-    if (!h->sample_timed) return;
-    h->sample_timed = false;
-    float ms = 0.f;
-    if (cudaEventSynchronize(h->tev[1]) == cudaSuccess &&
-        cudaEventElapsedTime(&ms, h->tev[0], h->tev[1]) == cudaSuccess)
-        h->phase_ms[0] += ms;
+// fold finished sampling intervals into phase_ms[0]: oldest first, stopping
+// at the first unfinished one unless `wait` (then the oldest is awaited)
+inline void gids_harvest_sample(gids_handle* h, bool wait) {
+    while (h->sev_count > 0) {
+        int i = (h->sev_head - h->sev_count + gids_handle::SRING) % gids_handle::SRING;
+        if (wait) {
+            cudaEventSynchronize(h->sev[i][1]);
+        } else if (cudaEventQuery(h->sev[i][1]) != cudaSuccess) {
+            break;
+        }
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, h->sev[i][0], h->sev[i][1]) == cudaSuccess)
+            h->phase_ms[0] += ms;
+        h->sev_count--;
+    }
     cudaGetLastError();
+}
+// open a sampling interval on `st` (profiling only); the ring never waits
+// unless it is full
+inline void gids_sample_begin(gids_handle* h, cudaStream_t st) {
+    if (!h->profiling) return;
+    gids_harvest_sample(h, false);
+    if (h->sev_count == gids_handle::SRING) {
+        int i = (h->sev_head - h->sev_count + gids_handle::SRING) % gids_handle::SRING;
+        cudaEventSynchronize(h->sev[i][1]);
+        gids_harvest_sample(h, false);
+    }
+    cudaEventRecord(h->sev[h->sev_head][0], st);
+}
+inline void gids_sample_end(gids_handle* h, cudaStream_t st) {
+    if (!h->profiling) return;
+    cudaEventRecord(h->sev[h->sev_head][1], st);
+    h->sev_head = (h->sev_head + 1) % gids_handle::SRING;
+    h->sev_count++;
 }
 
 inline void gids_mark(gids_handle* h, int i, cudaStream_t st) {

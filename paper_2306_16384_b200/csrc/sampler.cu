@@ -174,9 +174,7 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
             gids_set_error("fanout above 1024 is not supported by the CUDA sampler");
             return GIDS_E_INVALID;
         }
-    if (h->sample_timed) {  // previous batch's sampling time (profiling only)
-        gids_harvest_sample(h);
-    }
+    gids_sample_begin(h, st);
     if (w) {  // (re)seed the device-resident stream from the host Generator
         if (!h->jump_valid || h->jump_inc_hi != w[2] || h->jump_inc_lo != w[3]) {
             build_jump_table(w[2], w[3], h->jump_host);
@@ -226,8 +224,7 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
     if (rc) return rc;
     k_rng_advance<<<1, 1, 0, st>>>(h->rng_dev, h->sc, c.n_layers, h->jump_tab);
     GIDS_LAUNCH_CHECK(h);
-    gids_mark(h, 1, st);
-    h->sample_timed = h->profiling;
+    gids_sample_end(h, st);
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
                                   cudaMemcpyDeviceToHost, st));
     return GIDS_OK;

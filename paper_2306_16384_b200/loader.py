@@ -27,10 +27,10 @@ from fractions import Fraction
 import numpy as np
 
 from . import _native
-from .csc import (FeatureStore, generate_synthetic, load_features, load_graph,
+from .csc import (FeatureStore, GraphCsc, generate_synthetic, load_features, load_graph,
                   pinned_feature_table)
 from .feature_cache import GpuCacheView, WindowBuffer
-from .hot_buffer import build_constant_buffer, reverse_pagerank
+from .hot_buffer import build_constant_buffer, reverse_pagerank_device, top_k_nodes_device
 from .sampling import MiniBatch, Sampler, batch_iterator, check_seeds, pcg_words
 from .settings import ConfigError, InfeasibleError, PipelineConfig
 from .storage_model import exact, fetch_total_us, required_accesses
@@ -155,16 +155,26 @@ class Dataloader:
 
         graph_ss, feat_ss, sampler_ss, shuffle_ss, evict_ss, work_ss = \
             np.random.SeedSequence(cfg.seed).spawn(6)
+        graph_seed = int(graph_ss.generate_state(1)[0])
         if cfg.graph_path is not None:
             self.graph = load_graph(cfg.graph_path)
             host = load_features(cfg.features_path, mmap=True)
             if host.num_nodes != self.graph.num_nodes:
                 raise ConfigError("feature table and graph disagree on node count")
             self.features = self._pin_table(host)
+            dev_graph = self._upload_graph(self.graph)
         else:
-            self.graph = generate_synthetic(cfg.num_nodes, cfg.avg_degree, cfg.degree_model,
-                                            seed=int(graph_ss.generate_state(1)[0]),
-                                            exponent=cfg.degree_exponent)
+            if cfg.gids_generator == "device":
+                # counter-based uniform generator in HBM (csrc/graph_setup.cu)
+                n, e = cfg.num_nodes, int(round(cfg.num_nodes * cfg.avg_degree))
+                dev_graph = _native.generate_uniform_graph(self.device, n, e, graph_seed)
+                self.graph = GraphCsc(num_nodes=n, num_edges=e,
+                                      indptr=dev_graph[0].cpu().numpy().view(np.uint64),
+                                      indices=dev_graph[1].cpu().numpy().astype(np.uint64))
+            else:
+                self.graph = generate_synthetic(cfg.num_nodes, cfg.avg_degree, cfg.degree_model,
+                                                seed=graph_seed, exponent=cfg.degree_exponent)
+                dev_graph = self._upload_graph(self.graph)
             self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim,
                                                  int(feat_ss.generate_state(1)[0]), self.device)
         row_bytes = self.features.row_bytes
@@ -174,9 +184,13 @@ class Dataloader:
 
         budget = cfg.resolved_buffer_bytes(self.graph.num_nodes, row_bytes)
         if budget // row_bytes > 0:
-            self.pagerank = reverse_pagerank(self.graph)
+            # reverse PageRank + top-k on the GPU, float64-identical to
+            # cpu_buffer.py:26-109 (so the pinned set is the reference's)
+            self.pagerank, dev_scores = reverse_pagerank_device(self.device, *dev_graph)
+            chosen = top_k_nodes_device(dev_scores, budget // row_bytes)
+            del dev_scores
             self.buffer = build_constant_buffer(self.pagerank.scores, self.features, budget,
-                                                pin_memory=True)
+                                                pinned=chosen, pin_memory=True)
         else:
             self.pagerank = None
             self.buffer = build_constant_buffer(np.empty(0), self.features, 0,
@@ -192,7 +206,8 @@ class Dataloader:
             evict_key=evict_seed, window_depth=cfg.window_depth, fanouts=cfg.fanouts,
             max_seeds=cfg.batch_size,
             eviction_words=pcg_words(np.random.default_rng(evict_seed)))
-        self._h.load_graph(self.graph.indptr, self.graph.indices)
+        self._h.load_graph_device(*dev_graph)
+        del dev_graph
         self._h.set_backing(self.features.pinned if self.features.pinned is not None
                             else self.features.table, self.graph.num_nodes)
         self._h.set_constant_buffer(self.buffer.node_ids,
@@ -233,6 +248,15 @@ class Dataloader:
         self._row_frac = Fraction(row_bytes)
         self._cpu_bytes_per_s = exact(cfg.cpu_gbps) * 10**9
         self.last_counts = None
+
+    def _upload_graph(self, g: GraphCsc):
+        """Host GraphCsc -> (indptr int64, indices int32) CUDA tensors."""
+        import torch
+        if g.num_nodes >= 1 << 31:
+            raise ValueError("the CUDA path stores node ids as int32 (num_nodes < 2^31)")
+        ip = torch.from_numpy(np.ascontiguousarray(g.indptr).view(np.int64)).to(self._torch_dev)
+        ix = torch.from_numpy(np.asarray(g.indices).astype(np.int32)).to(self._torch_dev)
+        return ip, ix
 
     def _pin_table(self, host: FeatureStore) -> FeatureStore:
         import torch

@@ -15,6 +15,11 @@ prefixed ``gids``) select the B200 path:
 * ``gids_dp_rank`` / ``gids_dp_world``  data-parallel batch sharding: rank r
                       serves global batches r, r+W, ... with its own sampler
                       stream PCG64(sampler_ss).jumped(r).
+* ``gids_generator``  "reference" = the reference's numpy generator
+                      (graph.py:112-207, bit-identical graphs); "device" =
+                      the counter-based uniform generator in HBM
+                      (csrc/graph_setup.cu), for the 100M-node shapes the
+                      numpy generator cannot build (degree_model uniform only).
 """
 from __future__ import annotations
 
@@ -81,6 +86,7 @@ class PipelineConfig:
     gids_device: int = 0
     gids_dp_rank: int = 0
     gids_dp_world: int = 1
+    gids_generator: str = "reference"
 
     def ssd_spec(self) -> SsdSpec:
         if self.ssd_preset is None:
@@ -209,6 +215,10 @@ _RULES = [
     (lambda c: 0 <= c.gids_dp_rank < c.gids_dp_world,
      "gids_dp_rank must be within [0, gids_dp_world)"),
     (lambda c: c.window_depth <= 255, "window_depth above 255 is not supported by the GPU window"),
+    (lambda c: c.gids_generator in ("reference", "device"),
+     lambda c: f"unknown gids_generator {c.gids_generator!r}"),
+    (lambda c: c.gids_generator != "device" or c.degree_model == "uniform",
+     "gids_generator 'device' builds uniform graphs only"),
 ]
 
 

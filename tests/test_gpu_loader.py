@@ -121,3 +121,39 @@ def test_gpu_c2_shape_properties():
         assert st.cache_hits + st.cpu_buffer_hits + st.ssd_accesses == st.sampled_nodes
         assert rows.shape == (u.numel(), 1024)
     assert dl.cache.evictions > 0 or dl.cache.bypasses > 0
+
+
+def test_gpu_device_generator_loader_matches_oracle():
+    """gids_generator='device' (the C4/C5 path at a small shape): the graph is
+    built in HBM, the constant buffer chosen by the GPU reverse PageRank; the
+    oracle gets the same inputs from its own CPU restatements (generator,
+    float64-identical PageRank, stable top-k) and the runs agree bit for bit."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    cfg = make_config(dict(num_nodes=300_000, avg_degree=14.55, degree_model="uniform",
+                           feature_dim=128, fanouts=[15, 10, 5], batch_size=512,
+                           cache_lines=20_000, buffer_fraction=0.10, window_depth=8,
+                           consume_rate=0.0, seed=7, gids_generator="device",
+                           gids_policy="setassoc"))
+    dl = Dataloader(cfg)
+    g, buf = bench.host_device_shape(cfg)
+    assert np.array_equal(dl.graph.indptr, g.indptr)
+    assert np.array_equal(dl.graph.indices, g.indices)
+    assert np.array_equal(dl.buffer.node_ids, buf)
+    r = bench.oracle_inputs(cfg, g, dl.features.table, buf)
+    ld = O.OracleLoader(g.indptr, g.indices, dl.features.table, buf, r["batches"], cfg.fanouts,
+                        r["sampler_words"], r["evict_words"], cfg.resolved_cache_lines(),
+                        cfg.window_depth, r["base_threshold"], policy="setassoc",
+                        evict_key=r["evict_seed"])
+    for b in range(12):
+        o = ld.next_batch()
+        mb, rows, st = dl.next_batch()
+        assert np.array_equal(mb.unique_nodes.cpu().numpy(), o["unique"]), b
+        for l, ol in zip(mb.layers, o["layers"]):
+            assert np.array_equal(l.cpu().numpy(), ol), b
+        assert [st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses] == \
+            o["tiers"].tolist(), b
+        assert np.array_equal(rows.cpu().numpy(), o["rows"]), b
+    dl.close()
