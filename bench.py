@@ -280,10 +280,15 @@ def main() -> None:
     ap.add_argument("--policy", default=None, choices=["exact", "setassoc"],
                     help="cache policy (default: exact at c1/c2, setassoc at c4)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
+                    help="override a PipelineConfig key of the workload (experiments)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     args.policy = args.policy or DEFAULT_POLICY[args.workload]
     cfg_dict = {**WORKLOADS[args.workload], "gids_policy": args.policy}
+    for kv in args.set:
+        k, v = kv.split("=", 1)
+        cfg_dict[k] = json.loads(v) if v[:1] in "[{0123456789-tfn" else v
 
     if args.impl == "reference":
         run_reference(args, cfg_dict)

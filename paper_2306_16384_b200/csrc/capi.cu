@@ -159,7 +159,12 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         A(h->kind_buf[b], h->serve_cap);
         A(h->line_buf[b], h->serve_cap);
         A(h->ins_buf[b], h->serve_cap);
+        A(h->hit_list_buf[b], h->serve_cap);
+        A(h->host_list_buf[b], h->serve_cap);
+        A(h->list_cnt_buf[b], 2);
     }
+    A(h->flag_hit, h->serve_cap);
+    A(h->flag_host, h->serve_cap);
     A(h->log_line, h->serve_cap);
     A(h->log_pos, h->serve_cap);
     A(h->set_cnt, h->sets);
@@ -215,11 +220,16 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     // B200 (profiles/r01_bench_wps_b7_*.json) 1/2/4 warps per SM give the same
     // link rate, while 4 slows the overlapped exact-policy decisions by 30%
     {
-        int wps = 2;
+        int wps = 2;  // with gather_unroll 2: ~300 KB of loads in flight (tools/run12.sh)
         if (const char* e = getenv("GIDS_GATHER_WPS")) wps = atoi(e);
         if (wps < 1) wps = 1;
         int blocks = (wps * GIDS_SMS + 7) / 8;
         h->gather_blocks = blocks;
+        h->gather_unroll = 2;
+        if (const char* e = getenv("GIDS_GATHER_UNROLL")) {
+            int u = atoi(e);
+            h->gather_unroll = u >= 8 ? 8 : u >= 4 ? 4 : u >= 2 ? 2 : 1;
+        }
     }
     for (int i = 0; i < 2; i++) {
         GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->gathered[i], cudaEventDisableTiming));
@@ -229,6 +239,9 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     h->kind = h->kind_buf[0];
     h->line = h->line_buf[0];
     h->ins = h->ins_buf[0];
+    h->hit_list = h->hit_list_buf[0];
+    h->host_list = h->host_list_buf[0];
+    h->list_cnt = h->list_cnt_buf[0];
     *out = h;
     return GIDS_OK;
 }
@@ -246,7 +259,9 @@ int gids_destroy(gids_handle* h) {
                     h->word_parts, h->ev,      h->kind_buf[0], h->line_buf[0], h->ins_buf[0],
                     h->kind_buf[1], h->line_buf[1], h->ins_buf[1],            h->log_line,
                     h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
-                    h->svc};
+                    h->svc,       h->hit_list_buf[0], h->hit_list_buf[1], h->host_list_buf[0],
+                    h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
+                    h->flag_host, h->sel_tmp};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)

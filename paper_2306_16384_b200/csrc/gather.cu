@@ -66,31 +66,105 @@ __device__ __forceinline__ void copy_row(const float* __restrict__ src, float* _
     }
 }
 
+// Work is a flat range of 16-byte chunks over the compacted row list: chunk
+// i is chunk (i % cpr) of list row (i / cpr), cpr = chunks per row.  Every
+// lane keeps UNROLL loads in flight before it stores, so a warp has
+// UNROLL x 512 B outstanding whatever the row width (a 128-d row is exactly
+// one warp-wide load; a 1024-d row is eight).
+template <typename T>
+__device__ __forceinline__ T ld_nc(const T* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ int4 ld_nc<int4>(const int4* p) { return ld_stream(p); }
+template <typename T>
+__device__ __forceinline__ void st_cs(T* p, T v) { *p = v; }
+template <>
+__device__ __forceinline__ void st_cs<int4>(int4* p, int4 v) { st_stream(p, v); }
+
+struct ChunkIdx {
+    uint32_t shift, mask, cpr;  // shift/mask when cpr is a power of two
+    __device__ __forceinline__ void split(uint32_t i, uint32_t& r, uint32_t& c) const {
+        if (mask) {
+            r = i >> shift;
+            c = i & mask;
+        } else if (cpr == 1) {
+            r = i;
+            c = 0;
+        } else {
+            r = i / cpr;
+            c = i - r * cpr;
+        }
+    }
+};
+
+// cache hits: out[p] = cache_rows[line[p]]   (HBM -> HBM, before any insert)
+template <typename T, int UNROLL>
 __global__ void __launch_bounds__(BLOCK)
-k_gather_hits(int64_t n, const int8_t* __restrict__ kind, const int32_t* __restrict__ line,
-              const float* __restrict__ cache_rows, float* __restrict__ out, int64_t dim) {
+k_gather_hits(const int32_t* __restrict__ hit_list, const int64_t* __restrict__ list_cnt,
+              const int32_t* __restrict__ line, const T* __restrict__ cache_rows,
+              T* __restrict__ out, ChunkIdx ci) {
+    const uint32_t total = (uint32_t)list_cnt[0] * ci.cpr;
     const int lane = threadIdx.x & 31;
-    for (int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); p < n;
-         p += (int64_t)gridDim.x * WARPS) {
-        if (kind[p] != GIDS_KIND_HIT) continue;
-        copy_row(cache_rows + (int64_t)line[p] * dim, out + p * dim, nullptr, dim, lane);
+    const uint32_t warp = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * BLOCK) >> 5;
+    for (uint32_t base = warp * UNROLL * 32; base < total; base += nwarps * UNROLL * 32) {
+        T v[UNROLL];
+        int64_t dst[UNROLL];
+#pragma unroll
+        for (int k = 0; k < UNROLL; k++) {
+            const uint32_t i = base + k * 32 + lane;
+            dst[k] = -1;
+            if (i < total) {
+                uint32_t r, c;
+                ci.split(i, r, c);
+                const int32_t p = hit_list[r];
+                v[k] = ld_nc(cache_rows + (int64_t)line[p] * ci.cpr + c);
+                dst[k] = (int64_t)p * ci.cpr + c;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNROLL; k++)
+            if (dst[k] >= 0) st_cs(out + dst[k], v[k]);
     }
 }
 
+// host tiers: out[p] = constant-buffer or backing row (zero-copy over the
+// host link); the row also lands in its cache line when p inserts (ins[p])
+template <typename T, int UNROLL>
 __global__ void __launch_bounds__(BLOCK)
-k_gather_host(const int64_t* __restrict__ uniq, int64_t n, const int8_t* __restrict__ kind,
-              const int32_t* __restrict__ ins_line, const int32_t* __restrict__ pinned_off,
-              const float* __restrict__ buffer_rows, const float* __restrict__ backing,
-              float* __restrict__ cache_rows, float* __restrict__ out, int64_t dim) {
+k_gather_host(const int2* __restrict__ host_list, const int64_t* __restrict__ list_cnt,
+              const int32_t* __restrict__ ins, const T* __restrict__ buffer_rows,
+              const T* __restrict__ backing, T* __restrict__ cache_rows, T* __restrict__ out,
+              ChunkIdx ci) {
+    const uint32_t total = (uint32_t)list_cnt[1] * ci.cpr;
     const int lane = threadIdx.x & 31;
-    for (int64_t p = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5); p < n;
-         p += (int64_t)gridDim.x * WARPS) {
-        if (kind[p] == GIDS_KIND_HIT) continue;
-        const int32_t x = (int32_t)uniq[p];
-        const int32_t off = pinned_off[x];
-        const float* src = off >= 0 ? buffer_rows + (int64_t)off * dim : backing + (int64_t)x * dim;
-        const int32_t t = ins_line[p];
-        copy_row(src, out + p * dim, t >= 0 ? cache_rows + (int64_t)t * dim : nullptr, dim, lane);
+    const uint32_t warp = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * BLOCK) >> 5;
+    for (uint32_t base = warp * UNROLL * 32; base < total; base += nwarps * UNROLL * 32) {
+        T v[UNROLL];
+        int64_t dst[UNROLL], dst2[UNROLL];
+#pragma unroll
+        for (int k = 0; k < UNROLL; k++) {
+            const uint32_t i = base + k * 32 + lane;
+            dst[k] = -1;
+            if (i < total) {
+                uint32_t r, c;
+                ci.split(i, r, c);
+                const int2 it = host_list[r];
+                const T* src = it.y >= 0 ? buffer_rows + (int64_t)it.y * ci.cpr
+                                         : backing + (int64_t)(-(it.y + 1)) * ci.cpr;
+                v[k] = ld_nc(src + c);
+                dst[k] = (int64_t)it.x * ci.cpr + c;
+                const int32_t t = ins[it.x];
+                dst2[k] = t >= 0 ? (int64_t)t * ci.cpr + c : -1;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < UNROLL; k++) {
+            if (dst[k] >= 0) {
+                st_cs(out + dst[k], v[k]);
+                if (dst2[k] >= 0) cache_rows[dst2[k]] = v[k];
+            }
+        }
     }
 }
 
@@ -134,19 +208,56 @@ __global__ void k_verify(uint64_t seed_mix, const int64_t* __restrict__ nodes, i
 
 }  // namespace
 
+static ChunkIdx chunk_idx(int64_t cpr) {
+    ChunkIdx ci{0, 0, (uint32_t)cpr};
+    if (cpr > 1 && (cpr & (cpr - 1)) == 0) {
+        while (((int64_t)1 << ci.shift) < cpr) ci.shift++;
+        ci.mask = (uint32_t)(cpr - 1);
+    }
+    return ci;
+}
+
 int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* out,
                        cudaStream_t st) {
+    (void)uniq;
     const int64_t dim = h->row_floats;
-    // grid sized by GIDS_GATHER_WPS (capi.cu): a few warps per SM already
-    // saturate the host link; the rest of the GPU stays free for the next
-    // batch's sampling and cache decisions on the control stream
-    int grid = gids_grid(n, WARPS, h->gather_blocks);
-    k_gather_hits<<<grid, BLOCK, 0, st>>>(n, h->kind, h->line, h->cache_rows, out, dim);
-    GIDS_LAUNCH_CHECK(h);
-    if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
-    k_gather_host<<<grid, BLOCK, 0, st>>>(uniq, n, h->kind, h->ins, h->pinned_off,
-                                          h->buffer_rows, h->backing, h->cache_rows, out, dim);
-    GIDS_LAUNCH_CHECK(h);
+    if ((dim & 3) == 0 ? (n * (dim >> 2) >= ((int64_t)1 << 32)) : (n * dim >= ((int64_t)1 << 32))) {
+        gids_set_error("batch too large for the gather's 32-bit chunk index");
+        return GIDS_E_CAPACITY;
+    }
+    // hits: HBM -> HBM, the whole GPU for the few microseconds it takes;
+    // host rows: grid sized by GIDS_GATHER_WPS (capi.cu) -- a few warps per SM
+    // with 8 loads in flight per lane saturate the host link and leave the
+    // rest of the GPU to the next batch's sampling and cache decisions
+    const int hit_grid = gids_grid(n, WARPS, 4 * GIDS_SMS);
+    const int host_grid = gids_grid(n, WARPS, h->gather_blocks);
+    if ((dim & 3) == 0) {
+        ChunkIdx ci = chunk_idx(dim >> 2);
+        k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(
+            h->hit_list, h->list_cnt, h->line, reinterpret_cast<const int4*>(h->cache_rows),
+            reinterpret_cast<int4*>(out), ci);
+        GIDS_LAUNCH_CHECK(h);
+        if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
+        auto kh = h->gather_unroll == 1   ? k_gather_host<int4, 1>
+                  : h->gather_unroll == 2 ? k_gather_host<int4, 2>
+                  : h->gather_unroll == 4 ? k_gather_host<int4, 4>
+                                          : k_gather_host<int4, 8>;
+        kh<<<host_grid, BLOCK, 0, st>>>(
+            h->host_list, h->list_cnt, h->ins, reinterpret_cast<const int4*>(h->buffer_rows),
+            reinterpret_cast<const int4*>(h->backing), reinterpret_cast<int4*>(h->cache_rows),
+            reinterpret_cast<int4*>(out), ci);
+        GIDS_LAUNCH_CHECK(h);
+    } else {
+        ChunkIdx ci = chunk_idx(dim);
+        k_gather_hits<float, 4><<<hit_grid, BLOCK, 0, st>>>(h->hit_list, h->list_cnt, h->line,
+                                                            h->cache_rows, out, ci);
+        GIDS_LAUNCH_CHECK(h);
+        if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
+        k_gather_host<float, 8><<<host_grid, BLOCK, 0, st>>>(h->host_list, h->list_cnt, h->ins,
+                                                             h->buffer_rows, h->backing,
+                                                             h->cache_rows, out, ci);
+        GIDS_LAUNCH_CHECK(h);
+    }
     if (h->profiling) cudaEventRecord(h->gev[h->parity][2], st);
     return GIDS_OK;
 }

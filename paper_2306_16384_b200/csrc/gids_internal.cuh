@@ -213,9 +213,22 @@ struct gids_handle {
     int8_t* kind_buf[2];   // [serve_cap] GIDS_KIND_*
     int32_t* line_buf[2];  // [serve_cap] line read (hit) or taken (miss), -1
     int32_t* ins_buf[2];   // [serve_cap] line this node's row must be written to, -1
+    // compacted work lists of the gather, per decision set: positions of the
+    // cache hits, and (position, source row) of the host-tier rows where the
+    // source is a constant-buffer row (>= 0) or backing row x (encoded -(x+1))
+    int32_t* hit_list_buf[2];   // [serve_cap]
+    int2* host_list_buf[2];     // [serve_cap]
+    int64_t* list_cnt_buf[2];   // [2] hits, host rows
+    uint8_t* flag_hit;          // [serve_cap] compaction flags (decide phase only)
+    uint8_t* flag_host;
+    void* sel_tmp;              // CUB select scratch (lazily sized for serve_cap)
+    size_t sel_tmp_bytes;
     int8_t* kind;          // current set (alias)
     int32_t* line;
     int32_t* ins;
+    int32_t* hit_list;
+    int2* host_list;
+    int64_t* list_cnt;
     int parity;
     cudaEvent_t gathered[2];  // gather of the last batch that used each set
     bool gathered_valid[2];
@@ -231,6 +244,7 @@ struct gids_handle {
     int64_t last_serve_n;
     bool exact_smem;       // exact-policy tables fit in shared memory
     int gather_blocks;     // gather grid (resident blocks of 8 warps)
+    int gather_unroll;     // 16-B loads in flight per lane in the host gather (1,2,4,8)
 
     // phase timing (gids_set_profiling)
     bool profiling;

@@ -210,13 +210,19 @@ class Dataloader:
         del dev_graph
         self._h.set_backing(self.features.pinned if self.features.pinned is not None
                             else self.features.table, self.graph.num_nodes)
-        self._h.set_constant_buffer(self.buffer.node_ids,
-                                    self.buffer.pinned if self.buffer.pinned is not None
-                                    else self.buffer.rows)
+        if self.buffer.pinned is not None:
+            self._h.set_constant_buffer(self.buffer.device_ids, self.buffer.pinned)
+        else:
+            self._h.set_constant_buffer(self.buffer.node_ids, self.buffer.rows)
         # two streams: sampling + cache decisions (ctl) and row movement (gather);
         # the decisions of batch b+1 overlap the host-link gather of batch b
-        self._ctl = torch.cuda.Stream(self.device, priority=-1)  # decisions first
-        self._gat = torch.cuda.Stream(self.device)
+        # stream priority: the host link is the bottleneck resource, so by
+        # default the gather's blocks are dispatched first when SM slots free
+        # up (GIDS_PRIORITY=ctl flips it, for experiments)
+        import os
+        gather_first = os.environ.get("GIDS_PRIORITY", "gather") != "ctl"
+        self._ctl = torch.cuda.Stream(self.device, priority=0 if gather_first else -1)
+        self._gat = torch.cuda.Stream(self.device, priority=-1 if gather_first else 0)
         self.cache = GpuCacheView(self._h, self.spec.page_bytes)
         self.window = WindowBuffer(cfg.window_depth, self._h, self._ctl.cuda_stream)
         self._sampler = Sampler(self._h, self.graph.num_nodes, cfg.fanouts)
