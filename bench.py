@@ -45,8 +45,14 @@ WORKLOADS = {
                degree_model="uniform", feature_dim=128, fanouts=[15, 10, 5], batch_size=4096,
                cache_lines=2_097_152, buffer_fraction=0.10, window_depth=8, consume_rate=0.0,
                seed=42, gids_generator="device"),
+    # configs[4]: IGB-large shape, 409.6 GB table sharded over the
+    # ranks' HBM, remote rows read over NVLink; needs >= 3 GPUs
+    "c5": dict(num_nodes=100_000_000, avg_degree=1_223_571_364 / 100_000_000,
+               degree_model="uniform", feature_dim=1024, fanouts=[10, 15], batch_size=1024,
+               cache_lines=0, buffer_fraction=0.0, window_depth=8, consume_rate=0.0, seed=42,
+               gids_generator="device", gids_sharded_table=True),
 }
-DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c4": "setassoc"}
+DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c4": "setassoc", "c5": "exact"}
 WORKLOAD_NAMES = {
     "c2": "IGB-small-shaped 1M nodes / 12M edges (uniform), 1024-d fp32, fanout [10,15], "
           "batch 1024, cache 100K lines (10%) + 10% constant CPU buffer, W=8",
@@ -55,15 +61,28 @@ WORKLOAD_NAMES = {
     "c4": "ogbn-papers100M-shaped 111,059,956 nodes / 1,615,685,872 edges (uniform), 128-d "
           "fp32, fanout [15,10,5], batch 4096, cache 2,097,152 lines + 10% constant CPU "
           "buffer, W=8, 1 GPU",
+    "c5": "IGB-large-shaped 100M nodes / 1,223,571,364 edges (uniform), 1024-d fp32 "
+          "(409.6 GB) sharded over the ranks' HBM, NVLink peer loads, fanout [10,15], "
+          "batch 1024 per GPU",
 }
 L2_NOTE = {"c1": "inputs larger than L2 (410 MB HBM cache, 282 MB gathered per step)",
            "c2": "inputs larger than L2 (4.1 GB host table, 410 MB HBM cache)",
-           "c4": "inputs larger than L2 (56.9 GB host table, 1.07 GB HBM cache, 7.4 GB graph)"}
+           "c4": "inputs larger than L2 (56.9 GB host table, 1.07 GB HBM cache, 7.4 GB graph)",
+           "c5": "inputs larger than L2 (409.6 GB table in HBM shards, 5.7 GB graph)"}
 
 
 def load_peaks() -> dict:
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def load_traffic() -> dict:
+    """dram read+write bytes per launch of each workload's dominant kernel,
+    from one committed `ncu --set full` capture (profiles/ncu_traffic.json)."""
+    try:
+        return json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
     except Exception:
         return {}
 
@@ -302,6 +321,13 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload == "c5" and world < 3:
+        # 409.6 GB of rows need the HBM of at least three B200s
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "workload": WORKLOAD_NAMES["c5"],
+                              "n_gpus": world, "unavailable": "C5 shards a 409.6 GB table over "
+                              "the ranks' HBM; it needs >= 3 GPUs"}), flush=True)
+        return
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
@@ -320,10 +346,14 @@ def main() -> None:
         dist.barrier()
 
     # pass 1 (e2e): K steps through the public call, no per-phase events
+    steady_profile = os.environ.get("BENCH_PROFILE_STEADY") == "1"
+    if steady_profile:  # `ncu --profile-from-start off` captures pass 1 only (warm cache)
+        torch.cuda.profiler.start()
     launches0 = h.launch_count()
     clk, clk_path = start_clock_sampler(local)
     rows_host = rows_hbm = sampled = 0
     tiers = np.zeros(4, np.int64)
+    shard_rows = np.zeros(2, np.int64)  # sharded table: local, remote
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(local)
     t0 = time.perf_counter()
@@ -332,9 +362,13 @@ def main() -> None:
         mb, rows, st = dl.next_batch()
         sampled += st.sampled_nodes
         tiers += (st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses)
+        if dl.sharded is not None:
+            shard_rows += dl.shard_counts()
     end.record()
     torch.cuda.synchronize(local)
     wall = time.perf_counter() - t0
+    if steady_profile:
+        torch.cuda.profiler.stop()
     clocks = stop_clock_sampler(clk, clk_path)
     ms = start.elapsed_time(end)
     launches = h.launch_count() - launches0
@@ -382,6 +416,38 @@ def main() -> None:
     t_roof = max(host_rows * row_bytes / args.steps / (link_peak * 1e9),
                  hbm_bytes_step / (hbm_peak * 1e9) if hbm_peak else 0.0)
     step_s = ms_max / 1e3 / args.steps
+    traffic = load_traffic().get(args.workload)
+    if dl.sharded is None:
+        roofline = {"bound": "host_link", "kernel": "k_gather_host",
+                    "achieved": achieved_link, "peak": link_peak, "unit": "GB/s",
+                    "frac": achieved_link / link_peak if achieved_link else None,
+                    "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                    "traffic_source": traffic["source"] if traffic else None,
+                    "algorithmic_bytes_per_launch": host_bytes_per_launch,
+                    "peak_source": "pinned H2D cudaMemcpy measured in this run "
+                                   "(MEASURED_PEAKS.json has no host-link entry); GPU-initiated "
+                                   "reads top out at 51.4 GB/s on this link "
+                                   "(profiles/r01_hostread_microbench_*.txt)",
+                    "hbm_kernel": {"kernel": "k_gather_hits",
+                                   "achieved": hit_bytes / (hit_ms / 1e3) / 1e9 if hit_ms else None,
+                                   "peak": hbm_peak, "unit": "GB/s"}}
+    else:
+        # C5: rows come from the owners' HBM; the remote share crosses NVLink
+        nvl_peak = peaks.get("nvlink_gbs") or 900.0
+        remote_bytes = shard_rows[1] * row_bytes / args.steps
+        gat_s = gat_ms / 1e3
+        t_roof = max(remote_bytes / (nvl_peak * 1e9),
+                     (sampled * 2 * row_bytes / args.steps) / (hbm_peak * 1e9) if hbm_peak else 0)
+        roofline = {"bound": "nvlink", "kernel": "k_gather_shards",
+                    "achieved": remote_bytes / gat_s / 1e9 if gat_s else None, "peak": nvl_peak,
+                    "unit": "GB/s",
+                    "frac": remote_bytes / gat_s / 1e9 / nvl_peak if gat_s else None,
+                    "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                    "algorithmic_bytes_per_launch": remote_bytes,
+                    "peak_source": "MEASURED_PEAKS.json nvlink_gbs" if peaks.get("nvlink_gbs")
+                                   else "NVLink 5 nominal 900 GB/s per direction (not measured)",
+                    "rows_local_per_step": float(shard_rows[0]) / args.steps,
+                    "rows_remote_per_step": float(shard_rows[1]) / args.steps}
     line = {
         "metric": METRIC, "value": value, "unit": "minibatches/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
@@ -400,16 +466,7 @@ def main() -> None:
                               if k != "batches"},
         "tier_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / step_s,
                           "host_link_peak_gbs": link_peak, "hbm_peak_gbs": hbm_peak},
-        "roofline": {"bound": "host_link", "kernel": "k_gather_host",
-                     "achieved": achieved_link, "peak": link_peak, "unit": "GB/s",
-                     "frac": achieved_link / link_peak if achieved_link else None,
-                     "traffic": None,
-                     "peak_source": "pinned H2D cudaMemcpy measured in this run "
-                                    "(MEASURED_PEAKS.json has no host-link entry)",
-                     "hbm_kernel": {"kernel": "k_gather_hits",
-                                    "achieved": hit_bytes / (hit_ms / 1e3) / 1e9
-                                    if hit_ms else None,
-                                    "peak": hbm_peak, "unit": "GB/s"}},
+        "roofline": roofline,
         "value_definition": "device pipeline: 1 / max(per-step sampling+decision time on the "
                             "control stream, per-step gather time on the gather stream), CUDA "
                             "events on each launching stream (a second pass of K steps after "

@@ -194,6 +194,36 @@ GIDS_API int gids_reverse_pagerank(int device, int64_t num_nodes, int64_t num_ed
 GIDS_API int gids_load_graph_device(gids_handle* h, const int64_t* indptr_dev,
                                     const int32_t* indices_dev);
 
+/* ---- HBM-sharded feature table across data-parallel ranks ----
+ * SURVEY.md section 8(e), config C5 (a 409.6 GB table over 8 GPUs): node v
+ * lives in shard v % n_shards at row v / n_shards; every rank samples its own
+ * batches and gathers rows from the owners' HBM -- its own shard over HBM,
+ * the others as peer loads over NVLink (no collective on the data path).
+ * Replaces, for tables larger than one GPU, the FeatureStore lookups of the
+ * tier chain (dataloader.py:279-290): with the whole table resident every
+ * access is a cache hit. */
+
+/* A shard's own device allocation (IPC handles name whole allocations). */
+GIDS_API int gids_device_alloc(int device, int64_t bytes, void** dev_ptr_out);
+GIDS_API int gids_device_free(int device, void* dev_ptr);
+/* CUDA IPC: export a gids_device_alloc'd shard / open a peer's (64-byte handles). */
+GIDS_API int gids_ipc_handle(int device, const void* dev_ptr, uint8_t handle_out[64]);
+GIDS_API int gids_ipc_open(int device, const uint8_t handle[64], void** dev_ptr_out);
+GIDS_API int gids_ipc_close(int device, void* dev_ptr);
+
+/* shard_ptrs: n_shards device addresses (own or IPC-opened peer memory),
+ * each a dense fp32 [rows x feature_dim] shard; switches the handle to the
+ * sharded mode (gids_serve then reads rows from the shards). */
+GIDS_API int gids_set_sharded_table(gids_handle* h, const uint64_t* shard_ptrs, int32_t n_shards,
+                                    int32_t my_shard);
+/* rows of the last gids_serve read from this rank's shard / from peers */
+GIDS_API int gids_shard_counts(gids_handle* h, int64_t* local, int64_t* remote);
+
+/* synthetic_feature_rows (graph.py:256-275) for rows row0 + i*stride,
+ * i < n, written densely to dst (a shard) */
+GIDS_API int gids_synthesize_rows_strided(int device, uint64_t seed, int64_t row0, int64_t stride,
+                                          int64_t n, int32_t dim, float* dst, void* stream);
+
 /* Per-phase device time (CUDA events on the launching stream), accumulated
  * while profiling is on: out_ms[0] sampling, [1] window + cache policy,
  * [2] hit gather (HBM), [3] host-tier gather (zero-copy), [4] batches

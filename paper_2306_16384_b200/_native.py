@@ -89,6 +89,14 @@ def lib() -> C.CDLL:
         "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
                                    vp, vp], C.c_int),
         "gids_load_graph_device": ([vp, vp, vp], C.c_int),
+        "gids_device_alloc": ([i32, i64, C.POINTER(vp)], C.c_int),
+        "gids_device_free": ([i32, vp], C.c_int),
+        "gids_ipc_handle": ([i32, vp, vp], C.c_int),
+        "gids_ipc_open": ([i32, vp, C.POINTER(vp)], C.c_int),
+        "gids_ipc_close": ([i32, vp], C.c_int),
+        "gids_set_sharded_table": ([vp, vp, i32, i32], C.c_int),
+        "gids_shard_counts": ([vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
+        "gids_synthesize_rows_strided": ([i32, u64, i64, i64, i64, i32, vp, vp], C.c_int),
         "gids_set_profiling": ([vp, C.c_int], C.c_int),
         "gids_phase_times": ([vp, vp], C.c_int),
     }
@@ -112,7 +120,10 @@ def exported_symbols() -> list[str]:
             "gids_cache_rng", "gids_cache_lines", "gids_cache_capacity",
             "gids_synthesize_rows", "gids_verify_rows", "gids_set_profiling",
             "gids_phase_times", "gids_launch_count", "gids_generate_uniform_graph",
-            "gids_reverse_pagerank", "gids_load_graph_device"]
+            "gids_reverse_pagerank", "gids_load_graph_device", "gids_device_alloc",
+            "gids_device_free", "gids_ipc_handle",
+            "gids_ipc_open", "gids_ipc_close", "gids_set_sharded_table", "gids_shard_counts",
+            "gids_synthesize_rows_strided"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -188,6 +199,16 @@ class Handle:
     def load_graph_device(self, indptr, indices) -> None:
         """indptr int64[N+1] / indices int32[E] CUDA tensors (copied into the handle)."""
         check(lib().gids_load_graph_device(self.h, _p(indptr), _p(indices)), "load_graph_device")
+
+    def set_sharded_table(self, shard_ptrs, my_shard: int) -> None:
+        ptrs = np.ascontiguousarray(shard_ptrs, dtype=np.uint64)
+        check(lib().gids_set_sharded_table(self.h, ptrs.ctypes.data, len(ptrs), my_shard),
+              "set_sharded_table")
+
+    def shard_counts(self) -> tuple[int, int]:
+        a, b = C.c_int64(), C.c_int64()
+        check(lib().gids_shard_counts(self.h, C.byref(a), C.byref(b)), "shard_counts")
+        return a.value, b.value
 
     def set_backing(self, table, n_rows: int) -> None:
         self._keep.append(table)
@@ -324,3 +345,41 @@ def reverse_pagerank(device: int, indptr, indices, damping: float = 0.85, tol: f
                                       float(tol), int(max_iter), _p(scores), C.byref(it),
                                       C.byref(conv), stream_ptr(device)), "reverse_pagerank")
     return scores, bool(conv.value), int(it.value)
+
+
+def device_alloc(device: int, nbytes: int) -> int:
+    ptr = C.c_void_p()
+    check(lib().gids_device_alloc(device, nbytes, C.byref(ptr)), "device_alloc")
+    return int(ptr.value)
+
+
+def device_free(device: int, ptr: int) -> None:
+    check(lib().gids_device_free(device, C.c_void_p(ptr)), "device_free")
+
+
+def ipc_handle(device: int, ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a gids_device_alloc allocation."""
+    buf = (C.c_uint8 * 64)()
+    check(lib().gids_ipc_handle(device, C.c_void_p(ptr), buf), "ipc_handle")
+    return bytes(buf)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    if len(handle) != 64:
+        raise ValueError("CUDA IPC handles are 64 bytes")
+    buf = (C.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = C.c_void_p()
+    check(lib().gids_ipc_open(device, buf, C.byref(ptr)), "ipc_open")
+    return int(ptr.value)
+
+
+def ipc_close(device: int, ptr: int) -> None:
+    check(lib().gids_ipc_close(device, C.c_void_p(ptr)), "ipc_close")
+
+
+def synthesize_rows_strided(device: int, seed: int, row0: int, stride: int, n: int, dim: int,
+                            dst, stream: int) -> None:
+    """dst: a tensor or a raw device address."""
+    check(lib().gids_synthesize_rows_strided(device, seed & ((1 << 64) - 1), row0, stride, n,
+                                             dim, dst if isinstance(dst, int) else _p(dst),
+                                             stream), "synthesize_rows_strided")

@@ -722,6 +722,7 @@ int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delt
 }
 
 int gids_launch_contribution(gids_handle* h, cudaStream_t st) {
+    if (h->n_shards > 0) return GIDS_OK;  // whole table resident in HBM shards
     k_contribution<<<gids_grid(h->unique_cap, BLOCK, 4 * GIDS_SMS), BLOCK, 0, st>>>(
         h->unique32, h->sc, h->pinned_off, h->slot_of);
     GIDS_LAUNCH_CHECK(h);
@@ -748,6 +749,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     if (h->gathered_valid[par]) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->gathered[par], 0));
     gids_harvest_gather(h, par);  // batch b-2's gather timing (profiling only)
     gids_mark(h, 2, st);
+    if (h->n_shards > 0) return gids_launch_shard_serve(h, uniq, n, out, st, gst, par);
     GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
     if (n > 0) {
         GIDS_CUDA_TRY(cudaMemsetAsync(h->ins, 0xff, sizeof(int32_t) * n, st));

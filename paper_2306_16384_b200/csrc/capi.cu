@@ -261,7 +261,7 @@ int gids_destroy(gids_handle* h) {
                     h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
                     h->svc,       h->hit_list_buf[0], h->hit_list_buf[1], h->host_list_buf[0],
                     h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
-                    h->flag_host, h->sel_tmp};
+                    h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)
@@ -482,7 +482,7 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
         gids_set_error("batch larger than the serving workspace");
         return GIDS_E_CAPACITY;
     }
-    if (n > 0 && (!h->backing)) {
+    if (n > 0 && !h->backing && h->n_shards == 0) {
         gids_set_error("no backing store attached (gids_set_backing)");
         return GIDS_E_STATE;
     }

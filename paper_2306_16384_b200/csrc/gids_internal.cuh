@@ -138,6 +138,7 @@ struct SampleCounters {
 struct ServeCounters {
     int64_t tiers[4];      // hits, buffer, storage, bypasses (this batch)
     int64_t n_log;         // insertions logged by the exact policy this batch
+    int64_t shard_local, shard_remote;  // sharded-table mode: rows from own / peer HBM
 };
 
 struct CacheMeta {  // persistent cache counters (CacheState)
@@ -246,6 +247,13 @@ struct gids_handle {
     int gather_blocks;     // gather grid (resident blocks of 8 warps)
     int gather_unroll;     // 16-B loads in flight per lane in the host gather (1,2,4,8)
 
+    // HBM-sharded feature table: node v lives in
+    // shard v % n_shards at row v / n_shards; shard pointers may be peer
+    // (NVLink) addresses opened from CUDA IPC handles
+    int32_t n_shards;      // 0 = tiered mode (cache + host tiers)
+    int32_t my_shard;
+    const float** shard_ptrs;  // device array [n_shards]
+
     // phase timing (gids_set_profiling)
     bool profiling;
     cudaEvent_t tev[8];    // 2,3 decide phase
@@ -333,6 +341,9 @@ int gids_launch_serve(gids_handle* h, const int64_t* unique, int64_t n, uint64_t
 int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delta,
                        cudaStream_t st);
 int gids_launch_contribution(gids_handle* h, cudaStream_t st);
+// shard.cu
+int gids_launch_shard_serve(gids_handle* h, const int64_t* uniq, int64_t n, float* out,
+                            cudaStream_t st, cudaStream_t gst, int par);
 // gather.cu
 int gids_launch_gather(gids_handle* h, const int64_t* unique, int64_t n, float* out,
                        cudaStream_t st);

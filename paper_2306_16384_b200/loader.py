@@ -32,6 +32,7 @@ from .csc import (FeatureStore, GraphCsc, generate_synthetic, load_features, loa
 from .feature_cache import GpuCacheView, WindowBuffer
 from .hot_buffer import build_constant_buffer, reverse_pagerank_device, top_k_nodes_device
 from .sampling import MiniBatch, Sampler, batch_iterator, check_seeds, pcg_words
+from .sharded_table import ShardedTable
 from .settings import ConfigError, InfeasibleError, PipelineConfig
 from .storage_model import exact, fetch_total_us, required_accesses
 
@@ -156,6 +157,7 @@ class Dataloader:
         graph_ss, feat_ss, sampler_ss, shuffle_ss, evict_ss, work_ss = \
             np.random.SeedSequence(cfg.seed).spawn(6)
         graph_seed = int(graph_ss.generate_state(1)[0])
+        self.sharded = None
         if cfg.graph_path is not None:
             self.graph = load_graph(cfg.graph_path)
             host = load_features(cfg.features_path, mmap=True)
@@ -175,8 +177,19 @@ class Dataloader:
                 self.graph = generate_synthetic(cfg.num_nodes, cfg.avg_degree, cfg.degree_model,
                                                 seed=graph_seed, exponent=cfg.degree_exponent)
                 dev_graph = self._upload_graph(self.graph)
-            self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim,
-                                                 int(feat_ss.generate_state(1)[0]), self.device)
+            feat_seed = int(feat_ss.generate_state(1)[0])
+            if cfg.gids_sharded_table:
+                # C5: the table lives in the ranks' HBM (sharded_table.py)
+                virtual = cfg.gids_virtual_shards > 0
+                g = cfg.gids_virtual_shards if virtual else cfg.gids_dp_world
+                self.sharded = ShardedTable(cfg.num_nodes, cfg.feature_dim, feat_seed,
+                                            self.device, 0 if virtual else cfg.gids_dp_rank, g,
+                                            virtual=virtual)
+                self.features = FeatureStore(num_nodes=cfg.num_nodes, dim=cfg.feature_dim,
+                                             table=None, seed=feat_seed)
+            else:
+                self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim, feat_seed,
+                                                     self.device)
         row_bytes = self.features.row_bytes
         if row_bytes > self.spec.page_bytes:
             raise InfeasibleError(f"feature row ({row_bytes} B) exceeds one cache line / page "
@@ -202,14 +215,18 @@ class Dataloader:
         self._h = _native.Handle(
             num_nodes=self.graph.num_nodes, num_edges=self.graph.num_edges,
             feature_dim=self.features.dim, device=self.device,
-            cache_lines=cfg.resolved_cache_lines(), policy=cfg.gids_policy, ways=32,
+            cache_lines=0 if self.sharded else cfg.resolved_cache_lines(),
+            policy="exact" if self.sharded else cfg.gids_policy, ways=32,
             evict_key=evict_seed, window_depth=cfg.window_depth, fanouts=cfg.fanouts,
             max_seeds=cfg.batch_size,
             eviction_words=pcg_words(np.random.default_rng(evict_seed)))
         self._h.load_graph_device(*dev_graph)
         del dev_graph
-        self._h.set_backing(self.features.pinned if self.features.pinned is not None
-                            else self.features.table, self.graph.num_nodes)
+        if self.sharded is not None:
+            self._h.set_sharded_table(self.sharded.ptrs, self.sharded.rank)
+        else:
+            self._h.set_backing(self.features.pinned if self.features.pinned is not None
+                                else self.features.table, self.graph.num_nodes)
         if self.buffer.pinned is not None:
             self._h.set_constant_buffer(self.buffer.device_ids, self.buffer.pinned)
         else:
@@ -438,10 +455,20 @@ class Dataloader:
     def __next__(self):
         return self.next_batch()
 
+    def shard_counts(self) -> tuple[int, int]:
+        """Sharded-table mode: rows of the last batch read from this rank's
+        shard (HBM) and from peers (NVLink)."""
+        return self._h.shard_counts()
+
     def close(self) -> None:
         import torch
         torch.cuda.synchronize(self.device)
         self._h.close()
+        if self.sharded is not None:
+            import torch.distributed as dist
+            if self.cfg.gids_dp_world > 1 and dist.is_available() and dist.is_initialized():
+                dist.barrier()  # no peer may still be reading this rank's shard
+            self.sharded.close()
 
 
 def run(dl: Dataloader, iterations: int | None = None, warmup: int | None = None):

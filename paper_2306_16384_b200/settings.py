@@ -20,6 +20,11 @@ prefixed ``gids``) select the B200 path:
                       the counter-based uniform generator in HBM
                       (csrc/graph_setup.cu), for the 100M-node shapes the
                       numpy generator cannot build (degree_model uniform only).
+* ``gids_sharded_table``  C5: the synthetic feature table lives in the HBM of
+                      the data-parallel ranks, node v in shard v % G, read by
+                      peer loads over NVLink (sharded_table.py); no host tiers.
+* ``gids_virtual_shards`` G > 0 keeps all G shards on this process's GPU
+                      (single-GPU runs of the sharded path).
 """
 from __future__ import annotations
 
@@ -87,6 +92,8 @@ class PipelineConfig:
     gids_dp_rank: int = 0
     gids_dp_world: int = 1
     gids_generator: str = "reference"
+    gids_sharded_table: bool = False
+    gids_virtual_shards: int = 0
 
     def ssd_spec(self) -> SsdSpec:
         if self.ssd_preset is None:
@@ -219,6 +226,13 @@ _RULES = [
      lambda c: f"unknown gids_generator {c.gids_generator!r}"),
     (lambda c: c.gids_generator != "device" or c.degree_model == "uniform",
      "gids_generator 'device' builds uniform graphs only"),
+    (lambda c: not c.gids_sharded_table or c.graph_path is None,
+     "gids_sharded_table shards the synthetic feature table (no features_path)"),
+    (lambda c: not c.gids_sharded_table or (c.buffer_fraction == 0.0 and not c.buffer_bytes),
+     "gids_sharded_table keeps every row in HBM: buffer_fraction must be 0"),
+    (lambda c: c.gids_virtual_shards >= 0, "gids_virtual_shards must be non-negative"),
+    (lambda c: c.gids_virtual_shards == 0 or c.gids_dp_world == 1,
+     "gids_virtual_shards is for single-process runs (gids_dp_world 1)"),
 ]
 
 

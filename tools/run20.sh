@@ -1,0 +1,12 @@
+cd $GRAFT_REPO_ROOT
+summ() { python - "$1" "$2" <<'PY'
+import json,sys
+d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); print(sys.argv[2], round(d['value'],1), round(d['e2e']['value'],1), {k: round(v,3) for k,v in d['phase_ms_per_step'].items()}, round(d['roofline']['achieved'],2), flush=True)
+PY
+}
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -8
+timeout 600 python bench.py --steps 80 --warmup 5 > gpurun_out/b20_c2.json 2>&1; summ gpurun_out/b20_c2.json "c2"
+timeout 600 python bench.py --workload c5 --steps 5 --warmup 3 2>&1 | tail -1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gather_host" -s 20 -c 1 -o gpurun_out/prof_c2_gather_host python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/c2_ncu.log 2>&1; tail -1 gpurun_out/c2_ncu.log
+KS='regex:k_sample_layer|k_seed_mark|k_bm_|k_td_|k_rng|k_contribution|k_copy_edges|k_widen|k_window|k_sa_|k_tier_count|k_gather|k_i32|k_i64|DeviceSelect|k_post|k_exact'
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KS" -c 3000 --csv --log-file gpurun_out/c2_launches.csv python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c2_ncu1.log 2>&1; tail -1 gpurun_out/c2_ncu1.log | cut -c1-100
