@@ -18,7 +18,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 from pathlib import Path
@@ -87,44 +86,52 @@ def load_traffic() -> dict:
         return {}
 
 
-def start_clock_sampler(dev: int):
-    out = ROOT / "gpurun_out"
-    out.mkdir(exist_ok=True)
-    path = out / f"clocks_rank{dev}.csv"
-    try:
-        p = subprocess.Popen(
-            ["nvidia-smi", "-i", str(dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "200"],
-            stdout=open(path, "w"), stderr=subprocess.DEVNULL)
-    except FileNotFoundError:
-        return None, path
-    return p, path
+class _ClockSampler:
+    """SM clock and throttle reasons sampled in-process through NVML every
+    250 ms while the timed region runs (nvidia-smi as a polling subprocess
+    takes driver locks often enough to disturb the e2e pass)."""
 
+    NAMES = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+             "sw_power_cap": 0x4}
 
-def stop_clock_sampler(p, path) -> dict:
-    if p is None:
-        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-    p.terminate()
-    p.wait()
-    sm, smax, reasons = [], [], set()
-    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-    for line in Path(path).read_text().splitlines():
-        f = [x.strip() for x in line.split(",")]
-        if len(f) < 8:
-            continue
+    def __init__(self, dev: int):
+        import threading
+        self.sm, self.smax, self.reasons, self.err = [], [], set(), None
+        self._stop = threading.Event()
         try:
-            sm.append(float(f[0]))
-            smax.append(float(f[1]))
-        except ValueError:
-            continue
-        for name, v in zip(names, f[4:8]):
-            if v.lower().startswith("active"):
-                reasons.add(name)
-    return {"sm_mhz": float(np.median(sm)) if sm else None,
-            "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons),
-            "samples": len(sm)}
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        except Exception as e:  # no NVML: report it, keep timing
+            self._nv, self.err = None, repr(e)[:120]
+            return
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.smax.append(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.NAMES.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception as e:
+                self.err = repr(e)[:120]
+            self._stop.wait(0.25)
+
+    def stop(self) -> dict:
+        if self._nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"]}
+        self._stop.set()
+        self._t.join()
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None,
+                "sm_max_mhz": max(self.smax) if self.smax else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm),
+                "source": "NVML in-process, 250 ms"}
 
 
 def host_link_peak_gbs(dev: int) -> float:
@@ -350,7 +357,7 @@ def main() -> None:
     if steady_profile:  # `ncu --profile-from-start off` captures pass 1 only (warm cache)
         torch.cuda.profiler.start()
     launches0 = h.launch_count()
-    clk, clk_path = start_clock_sampler(local)
+    clk = _ClockSampler(local)
     rows_host = rows_hbm = sampled = 0
     tiers = np.zeros(4, np.int64)
     shard_rows = np.zeros(2, np.int64)  # sharded table: local, remote
@@ -369,7 +376,7 @@ def main() -> None:
     wall = time.perf_counter() - t0
     if steady_profile:
         torch.cuda.profiler.stop()
-    clocks = stop_clock_sampler(clk, clk_path)
+    clocks = clk.stop()
     ms = start.elapsed_time(end)
     launches = h.launch_count() - launches0
 
