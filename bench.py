@@ -365,8 +365,12 @@ def main() -> None:
     torch.cuda.synchronize(local)
     t0 = time.perf_counter()
     start.record()
+    call_ms = []  # host time per next_batch call (diagnostic: outliers in the e2e pass)
+    tr0 = len(dl._trace) if dl._trace is not None else 0
     for _ in range(args.steps):
+        th = time.perf_counter()
         mb, rows, st = dl.next_batch()
+        call_ms.append((time.perf_counter() - th) * 1e3)
         sampled += st.sampled_nodes
         tiers += (st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses)
         if dl.sharded is not None:
@@ -374,6 +378,7 @@ def main() -> None:
     end.record()
     torch.cuda.synchronize(local)
     wall = time.perf_counter() - t0
+    trace1 = dl._trace[tr0:] if dl._trace is not None else None
     if steady_profile:
         torch.cuda.profiler.stop()
     clocks = clk.stop()
@@ -484,6 +489,11 @@ def main() -> None:
                 "note": "timed through Dataloader.next_batch (the public API): host seed "
                         "batches in, host-tier rows over the link, per-step stats read back"},
         "gpu_launches": launches, "clocks": clocks,
+        "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),
+        "e2e_host_ms_per_call": {"min": float(np.min(call_ms)), "median": float(np.median(call_ms)),
+                                 "p90": float(np.percentile(call_ms, 90)),
+                                 "max": float(np.max(call_ms)),
+                                 "first5": [round(x, 2) for x in call_ms[:5]]},
         "setup_s": setup_s, "wall_s": wall,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

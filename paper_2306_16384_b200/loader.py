@@ -20,6 +20,8 @@ the reference orders its numpy result.
 from __future__ import annotations
 
 import math
+import os
+import time
 from collections import deque
 from dataclasses import dataclass
 from fractions import Fraction
@@ -236,7 +238,6 @@ class Dataloader:
         # stream priority: the host link is the bottleneck resource, so by
         # default the gather's blocks are dispatched first when SM slots free
         # up (GIDS_PRIORITY=ctl flips it, for experiments)
-        import os
         gather_first = os.environ.get("GIDS_PRIORITY", "gather") != "ctl"
         self._ctl = torch.cuda.Stream(self.device, priority=0 if gather_first else -1)
         self._gat = torch.cuda.Stream(self.device, priority=-1 if gather_first else 0)
@@ -258,6 +259,11 @@ class Dataloader:
         self._ringed = 0
         self._rng_on_device = False
         self._edge_cap, self._unique_cap = self._h.sample_capacity()
+        # pre-warm the gather stream's allocator pool with the blocks a
+        # pipelined caller keeps live (its batch, the one being gathered,
+        # the next one, and one freed but not yet retired)
+        warm = [self._out_block() for _ in range(4)]
+        del warm
         ring = cfg.runahead_cap + 4
         self._sizes = torch.zeros((ring, len(cfg.fanouts) + 5), dtype=torch.int64,
                                   pin_memory=True)
@@ -265,12 +271,21 @@ class Dataloader:
         self._sizes_next = 0
 
         self._iteration = 0
+        # host-time trace of next_batch (diagnostics): run-ahead, output
+        # allocation, serve launch, wait for the decisions -- seconds per call
+        self._trace = [] if os.environ.get("GIDS_TRACE_HOST") == "1" else None
         self._clock_us = Fraction(0)
         self._fetch_us_total = Fraction(0)
         self._train_us_total = Fraction(0)
         self._row_frac = Fraction(row_bytes)
         self._cpu_bytes_per_s = exact(cfg.cpu_gbps) * 10**9
         self.last_counts = None
+
+    def _out_block(self):
+        import torch
+        with torch.cuda.stream(self._gat):
+            return torch.empty((self._unique_cap, self.features.dim), dtype=torch.float32,
+                               device=self._torch_dev)
 
     def _upload_graph(self, g: GraphCsc):
         """Host GraphCsc -> (indptr int64, indices int32) CUDA tensors."""
@@ -380,6 +395,9 @@ class Dataloader:
     # -- serving (dataloader.py:232-299)
     def next_batch(self):
         import torch
+        tr = self._trace
+        if tr is not None:
+            t0 = time.perf_counter()
         self.run_ahead()
         if not self._pending:
             raise StopIteration
@@ -390,16 +408,27 @@ class Dataloader:
             self.window.pop_iteration()
             self._ringed -= 1
         self.run_ahead()
+        if tr is not None:
+            t1 = time.perf_counter()
 
         batch = entry.batch
         unique = batch.unique_nodes
-        with torch.cuda.stream(self._gat):
-            rows = torch.empty((unique.numel(), self.features.dim), dtype=torch.float32,
-                               device=self._torch_dev)
+        # output rows: every batch takes a block of the workspace bound (a view
+        # of the first U rows is returned), so torch's caching allocator keeps
+        # cycling the same pre-warmed blocks; exact-size requests (U varies)
+        # made it cudaMalloc fresh segments, stalling next_batch by 10-90 ms
+        n = unique.numel()
+        rows = self._out_block()[:n]
         unique.record_stream(self._gat)
+        if tr is not None:
+            t2 = time.perf_counter()
         self._h.serve(unique, self._iteration, rows, self._ctl.cuda_stream,
                       self._gat.cuda_stream)
+        if tr is not None:
+            t3 = time.perf_counter()
         c = self._h.serve_counts()  # waits for the decisions only, not the gather
+        if tr is not None:
+            tr.append((t1 - t0, t2 - t1, t3 - t2, time.perf_counter() - t3))
         self.last_counts = c
         # hand the batch to the caller's stream without blocking the host
         cur = torch.cuda.current_stream(self.device)
