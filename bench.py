@@ -35,9 +35,11 @@ WORKLOADS = {
                fanouts=[10, 15], batch_size=1024, cache_lines=100_000, buffer_fraction=0.10,
                window_depth=8, consume_rate=0.0, seed=42),
     # configs[0]: 100K nodes, everything fits the GPU cache
+    # (one permutation epoch is only 97 batches here, so seeds are drawn uniformly)
     "c1": dict(num_nodes=100_000, avg_degree=12.0, degree_model="uniform", feature_dim=1024,
                fanouts=[10, 15], batch_size=1024, cache_lines=100_000, buffer_fraction=0.0,
-               window_depth=8, consume_rate=0.0, seed=42),
+               window_depth=8, consume_rate=0.0, seed=42, seed_mode="uniform",
+               iterations=20_000),
     # configs[3]: ogbn-papers100M shape, 1 GPU; SURVEY.md s8 C4:
     # 2,097,152 cache lines (8 GiB of 4 KiB pages), 10% constant CPU buffer
     "c4": dict(num_nodes=111_059_956, avg_degree=1_615_685_872 / 111_059_956,

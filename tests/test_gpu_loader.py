@@ -157,3 +157,35 @@ def test_gpu_device_generator_loader_matches_oracle():
             o["tiers"].tolist(), b
         assert np.array_equal(rows.cpu().numpy(), o["rows"]), b
     dl.close()
+
+
+@pytest.mark.parametrize("policy", ["exact", "setassoc"])
+def test_gpu_data_parallel_replicas_match_oracle(policy):
+    """Data-parallel replicas: rank r of 3 serves global batches
+    r, r+3, ... with sampler stream PCG64(sampler_ss).jumped(r) and its own
+    cache; each rank's run equals the oracle fed the same slice and stream."""
+    from paper_2306_16384_b200.loader import _seed_stream
+    from paper_2306_16384_b200.sampling import pcg_words
+    base = dict(num_nodes=20_000, avg_degree=10.0, degree_model="uniform", feature_dim=32,
+                fanouts=[6, 8], batch_size=128, cache_lines=2_000, buffer_fraction=0.05,
+                window_depth=4, consume_rate=0.0, seed=5, gids_policy=policy)
+    r0 = resolve(make_config(base))
+    for rank in range(3):
+        cfg = make_config({**base, "gids_dp_rank": rank, "gids_dp_world": 3})
+        ss = np.random.SeedSequence(cfg.seed).spawn(6)
+        words = pcg_words(np.random.Generator(np.random.PCG64(ss[2]).jumped(rank)))
+        batches = list(_seed_stream(cfg, cfg.num_nodes, ss[5], ss[3]))
+        ld = O.OracleLoader(r0["graph"].indptr, r0["graph"].indices, r0["table"],
+                            r0["buffer_nodes"], batches, cfg.fanouts, words, r0["evict_words"],
+                            cfg.resolved_cache_lines(), cfg.window_depth, r0["base_threshold"],
+                            policy=policy, evict_key=r0["evict_seed"])
+        dl = Dataloader(cfg)
+        for b in range(8):
+            o = ld.next_batch()
+            mb, rows, st = dl.next_batch()
+            assert np.array_equal(mb.seeds, batches[b]), (rank, b)
+            assert np.array_equal(mb.unique_nodes.cpu().numpy(), o["unique"]), (rank, b)
+            assert [st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses] == \
+                o["tiers"].tolist(), (rank, b)
+            assert np.array_equal(rows.cpu().numpy(), o["rows"]), (rank, b)
+        dl.close()
