@@ -316,7 +316,10 @@ def main() -> None:
     cfg_dict = {**WORKLOADS[args.workload], "gids_policy": args.policy}
     for kv in args.set:
         k, v = kv.split("=", 1)
-        cfg_dict[k] = json.loads(v) if v[:1] in "[{0123456789-tfn" else v
+        try:
+            cfg_dict[k] = json.loads(v)
+        except json.JSONDecodeError:
+            cfg_dict[k] = v
 
     if args.impl == "reference":
         run_reference(args, cfg_dict)
@@ -491,6 +494,7 @@ def main() -> None:
                 "note": "timed through Dataloader.next_batch (the public API): host seed "
                         "batches in, host-tier rows over the link, per-step stats read back"},
         "gpu_launches": launches, "clocks": clocks,
+        "storage_file": dl.storage_stats(),
         "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),
         "e2e_host_ms_per_call": {"min": float(np.min(call_ms)), "median": float(np.median(call_ms)),
                                  "p90": float(np.percentile(call_ms, 90)),

@@ -224,6 +224,22 @@ GIDS_API int gids_shard_counts(gids_handle* h, int64_t* local, int64_t* remote);
 GIDS_API int gids_synthesize_rows_strided(int device, uint64_t seed, int64_t row0, int64_t stride,
                                           int64_t n, int32_t dim, float* dst, void* stream);
 
+/* ---- file-backed storage tier ----
+ * The storage tier read from a file instead of pinned memory: the reference's
+ * .gfea layout (graph.py:304-327) -- `offset` header bytes, then fp32 rows --
+ * read in pages of `page_bytes` (the GIDS init parameters).
+ * Each served batch's storage rows become an ascending, de-duplicated page
+ * list (the access accumulator), read as runs of consecutive pages by
+ * `io_threads` pread() threads into pinned staging (O_DIRECT when `direct`
+ * and page_bytes % 4096 == 0), copied to HBM by one DMA, then gathered.
+ * Replaces gids_set_backing; max_pages bounds the staging (0 = automatic). */
+GIDS_API int gids_set_storage_file(gids_handle* h, const char* path, int64_t offset,
+                                   int32_t page_bytes, int64_t max_pages, int32_t io_threads,
+                                   int32_t direct);
+/* cumulative pages / bytes read, read calls (runs), host I/O time, O_DIRECT in use */
+GIDS_API int gids_storage_file_stats(gids_handle* h, int64_t* pages, int64_t* bytes, int64_t* runs,
+                                     double* io_ms, int32_t* direct);
+
 /* Per-phase device time (CUDA events on the launching stream), accumulated
  * while profiling is on: out_ms[0] sampling, [1] window + cache policy,
  * [2] hit gather (HBM), [3] host-tier gather (zero-copy), [4] batches

@@ -89,6 +89,9 @@ def lib() -> C.CDLL:
         "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
                                    vp, vp], C.c_int),
         "gids_load_graph_device": ([vp, vp, vp], C.c_int),
+        "gids_set_storage_file": ([vp, C.c_char_p, i64, i32, i64, i32, i32], C.c_int),
+        "gids_storage_file_stats": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
+                                     C.POINTER(C.c_double), C.POINTER(i32)], C.c_int),
         "gids_device_alloc": ([i32, i64, C.POINTER(vp)], C.c_int),
         "gids_device_free": ([i32, vp], C.c_int),
         "gids_ipc_handle": ([i32, vp, vp], C.c_int),
@@ -123,7 +126,7 @@ def exported_symbols() -> list[str]:
             "gids_reverse_pagerank", "gids_load_graph_device", "gids_device_alloc",
             "gids_device_free", "gids_ipc_handle",
             "gids_ipc_open", "gids_ipc_close", "gids_set_sharded_table", "gids_shard_counts",
-            "gids_synthesize_rows_strided"]
+            "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -209,6 +212,20 @@ class Handle:
         a, b = C.c_int64(), C.c_int64()
         check(lib().gids_shard_counts(self.h, C.byref(a), C.byref(b)), "shard_counts")
         return a.value, b.value
+
+    def set_storage_file(self, path: str, offset: int, page_bytes: int, max_pages: int = 0,
+                         io_threads: int = 8, direct: bool = False) -> None:
+        check(lib().gids_set_storage_file(self.h, str(path).encode(), offset, page_bytes,
+                                          max_pages, io_threads, 1 if direct else 0),
+              "set_storage_file")
+
+    def storage_file_stats(self) -> dict:
+        p, b, r, d = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        ms = C.c_double()
+        check(lib().gids_storage_file_stats(self.h, C.byref(p), C.byref(b), C.byref(r),
+                                            C.byref(ms), C.byref(d)), "storage_file_stats")
+        return {"pages": p.value, "bytes": b.value, "runs": r.value, "io_ms": ms.value,
+                "direct": bool(d.value)}
 
     def set_backing(self, table, n_rows: int) -> None:
         self._keep.append(table)

@@ -817,6 +817,10 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(h->sel_tmp, tb, items, h->flag_host, h->host_list,
                                                  h->list_cnt + 1, n, st));
         h->launches += 2;
+        if (h->ft) {  // file-backed storage tier: plan this batch's page reads
+            int rc = gids_file_plan(h, par, st);
+            if (rc) return rc;
+        }
     }
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
                                   cudaMemcpyDeviceToHost, st));

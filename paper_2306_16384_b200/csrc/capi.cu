@@ -250,6 +250,7 @@ int gids_destroy(gids_handle* h) {
     if (!h) return GIDS_OK;
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
+    gids_file_free(h);
     void* ptrs[] = {h->indptr,    h->indices,  h->pinned_off, h->cache_rows, h->slot_of,
                     h->line_node, h->safe_bits, h->evict_bits, h->blk_cnt,   h->sup_cnt,
                     h->reuse,     h->future,   h->meta,       h->last_ins,   h->bm_front,
@@ -482,7 +483,7 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
         gids_set_error("batch larger than the serving workspace");
         return GIDS_E_CAPACITY;
     }
-    if (n > 0 && !h->backing && h->n_shards == 0) {
+    if (n > 0 && !h->backing && h->n_shards == 0 && !h->ft) {
         gids_set_error("no backing store attached (gids_set_backing)");
         return GIDS_E_STATE;
     }

@@ -231,6 +231,22 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
     // rest of the GPU to the next batch's sampling and cache decisions
     const int hit_grid = gids_grid(n, WARPS, 4 * GIDS_SMS);
     const int host_grid = gids_grid(n, WARPS, h->gather_blocks);
+    if (h->ft) {  // file-backed storage tier: hits, then pages -> HBM staging -> rows
+        if ((dim & 3) == 0) {
+            k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(
+                h->hit_list, h->list_cnt, h->line, reinterpret_cast<const int4*>(h->cache_rows),
+                reinterpret_cast<int4*>(out), chunk_idx(dim >> 2));
+        } else {
+            k_gather_hits<float, 4><<<hit_grid, BLOCK, 0, st>>>(h->hit_list, h->list_cnt, h->line,
+                                                                h->cache_rows, out, chunk_idx(dim));
+        }
+        GIDS_LAUNCH_CHECK(h);
+        if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
+        int rc = gids_file_fetch_and_gather(h, h->parity, out, st);
+        if (rc) return rc;
+        if (h->profiling) cudaEventRecord(h->gev[h->parity][2], st);
+        return GIDS_OK;
+    }
     if ((dim & 3) == 0) {
         ChunkIdx ci = chunk_idx(dim >> 2);
         k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(

@@ -147,6 +147,8 @@ struct CacheMeta {  // persistent cache counters (CacheState)
     uint64_t rng[6];       // exact-policy eviction PCG64 words
 };
 
+struct FileTier;
+
 struct gids_handle {
     gids_config cfg;
     int device;
@@ -254,6 +256,9 @@ struct gids_handle {
     int32_t my_shard;
     const float** shard_ptrs;  // device array [n_shards]
 
+    // file-backed storage tier (storage_file.cu); null = pinned-host tier
+    struct FileTier* ft;
+
     // phase timing (gids_set_profiling)
     bool profiling;
     cudaEvent_t tev[8];    // 2,3 decide phase
@@ -328,6 +333,9 @@ inline void gids_mark(gids_handle* h, int i, cudaStream_t st) {
 int gids_scan_take_draw(gids_handle* h, int fanout, int layer, cudaStream_t st);
 int gids_bitmap_compact(gids_handle* h, uint32_t* bm, int32_t* out, int64_t* count_out,
                         int64_t cap, bool clear, cudaStream_t st);
+int gids_bitmap_compact_n(gids_handle* h, uint32_t* bm, int64_t nbits, int32_t* out,
+                          int64_t* count_out, int64_t cap, bool clear, int64_t* overflow,
+                          cudaStream_t st);
 int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* out,
                          cudaStream_t st);
 // sampler.cu
@@ -344,6 +352,10 @@ int gids_launch_contribution(gids_handle* h, cudaStream_t st);
 // shard.cu
 int gids_launch_shard_serve(gids_handle* h, const int64_t* uniq, int64_t n, float* out,
                             cudaStream_t st, cudaStream_t gst, int par);
+// storage_file.cu
+int gids_file_plan(gids_handle* h, int par, cudaStream_t st);
+int gids_file_fetch_and_gather(gids_handle* h, int par, float* out, cudaStream_t gst);
+void gids_file_free(gids_handle* h);
 // gather.cu
 int gids_launch_gather(gids_handle* h, const int64_t* unique, int64_t n, float* out,
                        cudaStream_t st);

@@ -234,11 +234,17 @@ int gids_scan_take_draw(gids_handle* h, int fanout, int layer, cudaStream_t st) 
 
 int gids_bitmap_compact(gids_handle* h, uint32_t* bm, int32_t* out, int64_t* count_out,
                         int64_t cap, bool clear, cudaStream_t st) {
-    int64_t nwords = ceil_div(h->N, 32);
+    return gids_bitmap_compact_n(h, bm, h->N, out, count_out, cap, clear, &h->sc->overflow, st);
+}
+
+int gids_bitmap_compact_n(gids_handle* h, uint32_t* bm, int64_t nbits, int32_t* out,
+                          int64_t* count_out, int64_t cap, bool clear, int64_t* overflow,
+                          cudaStream_t st) {
+    int64_t nwords = ceil_div(nbits, 32);
     int np = parts_for(nwords);
     k_bm_reduce<<<np, SCAN_BLOCK, 0, st>>>(bm, nwords, h->word_parts);
     GIDS_LAUNCH_CHECK(h);
-    k_bm_parts<<<1, MAX_PARTS, 0, st>>>(h->word_parts, np, count_out, cap, &h->sc->overflow);
+    k_bm_parts<<<1, MAX_PARTS, 0, st>>>(h->word_parts, np, count_out, cap, overflow);
     GIDS_LAUNCH_CHECK(h);
     k_bm_apply<<<np, SCAN_BLOCK, 0, st>>>(bm, nwords, h->word_parts, out, cap, clear ? 1 : 0);
     GIDS_LAUNCH_CHECK(h);

@@ -29,8 +29,8 @@ from fractions import Fraction
 import numpy as np
 
 from . import _native
-from .csc import (FeatureStore, GraphCsc, generate_synthetic, load_features, load_graph,
-                  pinned_feature_table)
+from .csc import (HEADER_BYTES, FeatureStore, GraphCsc, generate_synthetic, load_features,
+                  load_graph, pinned_feature_table, write_synthetic_features)
 from .feature_cache import GpuCacheView, WindowBuffer
 from .hot_buffer import build_constant_buffer, reverse_pagerank_device, top_k_nodes_device
 from .sampling import MiniBatch, Sampler, batch_iterator, check_seeds, pcg_words
@@ -160,12 +160,15 @@ class Dataloader:
             np.random.SeedSequence(cfg.seed).spawn(6)
         graph_seed = int(graph_ss.generate_state(1)[0])
         self.sharded = None
+        self._storage_file = None
         if cfg.graph_path is not None:
             self.graph = load_graph(cfg.graph_path)
             host = load_features(cfg.features_path, mmap=True)
             if host.num_nodes != self.graph.num_nodes:
                 raise ConfigError("feature table and graph disagree on node count")
-            self.features = self._pin_table(host)
+            self._storage_file = str(cfg.features_path) if cfg.gids_storage == "file" else None
+            # file tier: the rows stay in the file (memory-mapped for the host API)
+            self.features = host if self._storage_file else self._pin_table(host)
             dev_graph = self._upload_graph(self.graph)
         else:
             if cfg.gids_generator == "device":
@@ -189,6 +192,15 @@ class Dataloader:
                                             virtual=virtual)
                 self.features = FeatureStore(num_nodes=cfg.num_nodes, dim=cfg.feature_dim,
                                              table=None, seed=feat_seed)
+            elif cfg.gids_storage == "file":
+                # the synthetic table written once to a .gfea file, then served
+                # from the file (csrc/storage_file.cu)
+                write_synthetic_features(cfg.gids_storage_path, cfg.num_nodes, cfg.feature_dim,
+                                         feat_seed, self.device)
+                host = load_features(cfg.gids_storage_path, mmap=True)
+                self.features = FeatureStore(num_nodes=host.num_nodes, dim=host.dim,
+                                             table=host.table, seed=feat_seed)
+                self._storage_file = str(cfg.gids_storage_path)
             else:
                 self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim, feat_seed,
                                                      self.device)
@@ -226,6 +238,9 @@ class Dataloader:
         del dev_graph
         if self.sharded is not None:
             self._h.set_sharded_table(self.sharded.ptrs, self.sharded.rank)
+        elif self._storage_file is not None:
+            self._h.set_storage_file(self._storage_file, HEADER_BYTES, self.spec.page_bytes,
+                                     io_threads=cfg.gids_io_threads, direct=cfg.gids_io_direct)
         else:
             self._h.set_backing(self.features.pinned if self.features.pinned is not None
                                 else self.features.table, self.graph.num_nodes)
@@ -292,7 +307,8 @@ class Dataloader:
         import torch
         if g.num_nodes >= 1 << 31:
             raise ValueError("the CUDA path stores node ids as int32 (num_nodes < 2^31)")
-        ip = torch.from_numpy(np.ascontiguousarray(g.indptr).view(np.int64)).to(self._torch_dev)
+        ip = torch.from_numpy(np.array(g.indptr, dtype=np.uint64).view(np.int64)).to(
+            self._torch_dev)
         ix = torch.from_numpy(np.asarray(g.indices).astype(np.int32)).to(self._torch_dev)
         return ip, ix
 
@@ -314,7 +330,10 @@ class Dataloader:
         num_elements: N * dim fp32 elements.  Returns the resolved layout."""
         layout = {"offset": 24, "cacheline_bytes": self.spec.page_bytes,
                   "num_elements": self.graph.num_nodes * self.features.dim,
-                  "n_ssd": self.spec.n_ssd, "row_bytes": self.features.row_bytes}
+                  "n_ssd": self.spec.n_ssd, "row_bytes": self.features.row_bytes,
+                  "storage": "file" if self._storage_file else
+                             ("hbm-sharded" if self.sharded else "pinned"),
+                  "path": self._storage_file}
         for key, val in (("offset", offset), ("cacheline_bytes", cacheline_bytes),
                          ("num_elements", num_elements), ("n_ssd", n_ssd)):
             if val is not None and val != layout[key]:
@@ -483,6 +502,10 @@ class Dataloader:
 
     def __next__(self):
         return self.next_batch()
+
+    def storage_stats(self) -> dict | None:
+        """File tier: cumulative pages / bytes read, read calls, host I/O ms."""
+        return self._h.storage_file_stats() if self._storage_file is not None else None
 
     def shard_counts(self) -> tuple[int, int]:
         """Sharded-table mode: rows of the last batch read from this rank's

@@ -25,6 +25,13 @@ prefixed ``gids``) select the B200 path:
                       peer loads over NVLink (sharded_table.py); no host tiers.
 * ``gids_virtual_shards`` G > 0 keeps all G shards on this process's GPU
                       (single-GPU runs of the sharded path).
+* ``gids_storage``    "pinned" = the storage tier in page-locked host memory
+                      read zero-copy; "file" = the .gfea file itself, read in
+                      pages of ``page_bytes`` after the 24-byte header through
+                      the page-coalescing accumulator (csrc/storage_file.cu).
+                      A synthetic config writes its table to
+                      ``gids_storage_path`` first.
+* ``gids_io_threads`` / ``gids_io_direct``  pread threads / O_DIRECT for "file".
 """
 from __future__ import annotations
 
@@ -94,6 +101,10 @@ class PipelineConfig:
     gids_generator: str = "reference"
     gids_sharded_table: bool = False
     gids_virtual_shards: int = 0
+    gids_storage: str = "pinned"
+    gids_storage_path: str | None = None
+    gids_io_threads: int = 8
+    gids_io_direct: bool = False
 
     def ssd_spec(self) -> SsdSpec:
         if self.ssd_preset is None:
@@ -231,6 +242,14 @@ _RULES = [
     (lambda c: not c.gids_sharded_table or (c.buffer_fraction == 0.0 and not c.buffer_bytes),
      "gids_sharded_table keeps every row in HBM: buffer_fraction must be 0"),
     (lambda c: c.gids_virtual_shards >= 0, "gids_virtual_shards must be non-negative"),
+    (lambda c: c.gids_storage in ("pinned", "file"),
+     lambda c: f"unknown gids_storage {c.gids_storage!r}"),
+    (lambda c: c.gids_storage != "file" or c.graph_path is not None
+     or c.gids_storage_path is not None,
+     "gids_storage 'file' needs features_path or gids_storage_path"),
+    (lambda c: c.gids_storage != "file" or not c.gids_sharded_table,
+     "gids_storage 'file' and gids_sharded_table are exclusive"),
+    (lambda c: c.gids_io_threads >= 1, "gids_io_threads must be >= 1"),
     (lambda c: c.gids_virtual_shards == 0 or c.gids_dp_world == 1,
      "gids_virtual_shards is for single-process runs (gids_dp_world 1)"),
 ]
