@@ -333,15 +333,25 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.workload == "c5" and world < 3:
-        # 409.6 GB of rows need the HBM of at least three B200s
-        if rank == 0:
-            print(json.dumps({"metric": METRIC, "workload": WORKLOAD_NAMES["c5"],
-                              "n_gpus": world, "unavailable": "C5 shards a 409.6 GB table over "
-                              "the ranks' HBM; it needs >= 3 GPUs"}), flush=True)
-        return
+    if cfg_dict.get("gids_sharded_table"):
+        shard_gb = cfg_dict["num_nodes"] * cfg_dict["feature_dim"] * 4 / world / 1e9
+        if shard_gb > 150:  # HBM left for the graph and workspaces on a 180 GB B200
+            if rank == 0:
+                print(json.dumps({"metric": METRIC, "workload": WORKLOAD_NAMES[args.workload],
+                                  "n_gpus": world, "unavailable": f"the sharded table needs "
+                                  f"{shard_gb:.0f} GB of HBM per GPU at {world} GPU(s); C5's "
+                                  f"409.6 GB needs >= 3 GPUs"}), flush=True)
+            return
+    # BENCH_DIST_BACKEND=gloo lets several ranks share one GPU (a plumbing test
+    # of the multi-rank path on a single-GPU box; NCCL refuses duplicate GPUs)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if backend == "gloo":
+        local = local % torch.cuda.device_count()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     cfg = make_config({**cfg_dict, "gids_device": local, "gids_dp_rank": rank,
                        "gids_dp_world": world})
@@ -400,7 +410,8 @@ def main() -> None:
     torch.cuda.synchronize(local)
     phases = h.phase_times()
     h.set_profiling(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=local)
+    red_dev = local if backend == "nccl" else "cpu"
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
@@ -415,7 +426,7 @@ def main() -> None:
     ctl_ms = (phases["sample_ms"] + phases["cache_ms"]) / nb
     gat_ms = (phases["gather_hits_ms"] + phases["gather_host_ms"]) / nb
     dev_ms = max(ctl_ms, gat_ms)
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=local)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     value = world / (float(t.item()) / 1e3)
