@@ -461,7 +461,7 @@ def main() -> None:
                                    "peak": hbm_peak, "unit": "GB/s"}}
     else:
         # C5: rows come from the owners' HBM; the remote share crosses NVLink
-        nvl_peak = peaks.get("nvlink_gbs") or 900.0
+        nvl_peak = peaks.get("nvlink_gbs") or 770.0
         remote_bytes = shard_rows[1] * row_bytes / args.steps
         gat_s = gat_ms / 1e3
         t_roof = max(remote_bytes / (nvl_peak * 1e9),
@@ -473,7 +473,8 @@ def main() -> None:
                     "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
                     "algorithmic_bytes_per_launch": remote_bytes,
                     "peak_source": "MEASURED_PEAKS.json nvlink_gbs" if peaks.get("nvlink_gbs")
-                                   else "NVLink 5 nominal 900 GB/s per direction (not measured)",
+                                   else "B200_PROFILING.md: measured peer copy 770 GB/s per "
+                                        "direction on this pool (900 nominal)",
                     "rows_local_per_step": float(shard_rows[0]) / args.steps,
                     "rows_remote_per_step": float(shard_rows[1]) / args.steps}
     line = {
