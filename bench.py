@@ -40,6 +40,15 @@ WORKLOADS = {
                fanouts=[10, 15], batch_size=1024, cache_lines=100_000, buffer_fraction=0.0,
                window_depth=8, consume_rate=0.0, seed=42, seed_mode="uniform",
                iterations=20_000),
+    # configs[2]: IGB-medium shape; 2,097,152 lines (8 GiB of
+    # 4 KiB pages), 10% buffer = 1M rows, misses served by the storage tier
+    "c3": dict(num_nodes=10_000_000, avg_degree=12.0, degree_model="uniform", feature_dim=1024,
+               fanouts=[10, 15], batch_size=1024, cache_lines=2_097_152, buffer_fraction=0.10,
+               window_depth=8, consume_rate=0.0, seed=42, gids_generator="device"),
+    # C2 with the reference's powerlaw degree model (the locality variant)
+    "c2p": dict(num_nodes=1_000_000, avg_degree=12.0, degree_model="powerlaw",
+                feature_dim=1024, fanouts=[10, 15], batch_size=1024, cache_lines=100_000,
+                buffer_fraction=0.10, window_depth=8, consume_rate=0.0, seed=42),
     # configs[3]: ogbn-papers100M shape, 1 GPU; SURVEY.md s8 C4:
     # 2,097,152 cache lines (8 GiB of 4 KiB pages), 10% constant CPU buffer
     "c4": dict(num_nodes=111_059_956, avg_degree=1_615_685_872 / 111_059_956,
@@ -53,12 +62,17 @@ WORKLOADS = {
                cache_lines=0, buffer_fraction=0.0, window_depth=8, consume_rate=0.0, seed=42,
                gids_generator="device", gids_sharded_table=True),
 }
-DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c4": "setassoc", "c5": "exact"}
+DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c2p": "exact", "c3": "setassoc",
+                  "c4": "setassoc", "c5": "exact"}
 WORKLOAD_NAMES = {
     "c2": "IGB-small-shaped 1M nodes / 12M edges (uniform), 1024-d fp32, fanout [10,15], "
           "batch 1024, cache 100K lines (10%) + 10% constant CPU buffer, W=8",
     "c1": "synthetic 100K nodes / 1.2M edges (uniform), 1024-d fp32, fanout [10,15], "
           "batch 1024, all rows fit the GPU cache, W=8",
+    "c3": "IGB-medium-shaped 10M nodes / 120M edges (uniform), 1024-d fp32, fanout [10,15], "
+          "batch 1024, cache 2,097,152 lines + 10% constant CPU buffer, W=8",
+    "c2p": "IGB-small-shaped 1M nodes / 12M edges (powerlaw), 1024-d fp32, fanout [10,15], "
+           "batch 1024, cache 100K lines (10%) + 10% constant CPU buffer, W=8",
     "c4": "ogbn-papers100M-shaped 111,059,956 nodes / 1,615,685,872 edges (uniform), 128-d "
           "fp32, fanout [15,10,5], batch 4096, cache 2,097,152 lines + 10% constant CPU "
           "buffer, W=8, 1 GPU",
@@ -68,6 +82,8 @@ WORKLOAD_NAMES = {
 }
 L2_NOTE = {"c1": "inputs larger than L2 (410 MB HBM cache, 282 MB gathered per step)",
            "c2": "inputs larger than L2 (4.1 GB host table, 410 MB HBM cache)",
+           "c3": "inputs larger than L2 (41 GB host table, 8.6 GB HBM cache)",
+           "c2p": "inputs larger than L2 (4.1 GB host table, 410 MB HBM cache)",
            "c4": "inputs larger than L2 (56.9 GB host table, 1.07 GB HBM cache, 7.4 GB graph)",
            "c5": "inputs larger than L2 (409.6 GB table in HBM shards, 5.7 GB graph)"}
 
