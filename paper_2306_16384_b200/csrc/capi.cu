@@ -220,7 +220,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     // B200 (profiles/r01_bench_wps_b7_*.json) 1/2/4 warps per SM give the same
     // link rate, while 4 slows the overlapped exact-policy decisions by 30%
     {
-        int wps = 2;  // with gather_unroll 2: ~300 KB of loads in flight (tools/run12.sh)
+        int wps = 2;  // with gather_unroll 2: ~300 KB of loads in flight (profiles/r01_gather_wps_unroll_sweep_c2.txt)
         if (const char* e = getenv("GIDS_GATHER_WPS")) wps = atoi(e);
         if (wps < 1) wps = 1;
         int blocks = (wps * GIDS_SMS + 7) / 8;

@@ -1,0 +1,22 @@
+#!/usr/bin/env bash
+# One GPU pass over everything a round is judged on (run under gpurun):
+#   tools/gpu_round.sh [quick]
+# GPU tests + smoke, the default bench line (C2) and C4, the reference arm,
+# steady-state ncu launch lists and a full capture of the dominant kernel.
+# Outputs land in gpurun_out/ (copy what is kept into profiles/).
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+set -x
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -5
+timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' 2>&1 | tail -2
+timeout 600 python bench.py > gpurun_out/bench_c2.json 2>&1; tail -c 600 gpurun_out/bench_c2.json
+[ "$1" = quick ] && exit 0
+timeout 1500 python bench.py --workload c4 --steps 30 --warmup 10 > gpurun_out/bench_c4.json 2>&1
+timeout 900 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref_c2.json 2>&1
+export BENCH_PROFILE_STEADY=1
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
+    --csv --log-file gpurun_out/c2_launches_steady.csv python bench.py --steps 20 --warmup 30 \
+    --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gather_host -s 20 -c 1 \
+    -o gpurun_out/prof_c2_gather_host python bench.py --steps 10 --warmup 10 --no-cpu-baseline \
+    > /dev/null 2>&1
+ls gpurun_out
