@@ -152,6 +152,22 @@ GIDS_API int gids_serve_counts(gids_handle* h, gids_tier_counts* out);
  * line int64[U] (-1 on bypass).  Device pointers. */
 GIDS_API int gids_serve_decisions(gids_handle* h, int8_t* kind_dev, int64_t* line_dev, void* stream);
 
+/* The cache driven directly (the reference exports CacheState and
+ * window_update besides the loader).  gids_cache_window_update: window_update
+ * (cache.py:190-218) of `nodes` against the handle's window (gids_window_push
+ * / pop); counts_dev int32[n] (optional) receives each node's lookahead count.
+ * gids_cache_access: CacheState.access (cache.py:144-180) for n distinct
+ * nodes in list order, exact policy; kind_dev int8[n] (GIDS_KIND_*), line_dev
+ * int32[n] (-1 on bypass), victim_dev int64[n] (optional: the evicted line's
+ * occupant at the call's start, -1 when none).  Device pointers. */
+GIDS_API int gids_cache_window_update(gids_handle* h, const int64_t* nodes_dev, int64_t n,
+                                      int32_t* counts_dev, void* stream);
+GIDS_API int gids_cache_access(gids_handle* h, const int64_t* nodes_dev, int64_t n,
+                               int8_t* kind_dev, int32_t* line_dev, int64_t* victim_dev,
+                               void* stream);
+/* reuse_counter (cache.py:104-113) of every node: uint32[num_nodes], host */
+GIDS_API int gids_cache_reuse(gids_handle* h, uint32_t* reuse_host);
+
 GIDS_API int gids_cache_stats(gids_handle* h, gids_cache_counters* out);       /* synchronises */
 GIDS_API int gids_cache_rng(gids_handle* h, uint64_t words_out[6]);          /* exact-policy RNG */
 /* line table snapshot: node int64[L] (-1 empty), state int8[L] (0 empty,

@@ -10,8 +10,8 @@ from .csc import (BadMagicError, FeatureStore, FileFormatError, GraphCsc, Trunca
                   VersionMismatchError, build_csc, generate_synthetic, load_features, load_graph,
                   neighbors, pinned_feature_table, save_features, save_graph,
                   synthetic_feature_rows)
-from .feature_cache import (AccessKind, AccessResult, CacheProtocolError, CacheStats,
-                            GpuCacheView, LineState, WindowBuffer)
+from .feature_cache import (AccessKind, AccessResult, CacheProtocolError, CacheState,
+                            CacheStats, GpuCacheView, LineState, WindowBuffer, window_update)
 from .hot_buffer import (ConstantBuffer, PageRankResult, build_constant_buffer,
                          reverse_pagerank, top_k_nodes)
 from .loader import CSV_HEADER, Dataloader, IterationStats, RunSummary, run, stats_csv

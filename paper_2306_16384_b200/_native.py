@@ -89,6 +89,9 @@ def lib() -> C.CDLL:
         "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
                                    vp, vp], C.c_int),
         "gids_load_graph_device": ([vp, vp, vp], C.c_int),
+        "gids_cache_window_update": ([vp, vp, i64, vp, vp], C.c_int),
+        "gids_cache_access": ([vp, vp, i64, vp, vp, vp, vp], C.c_int),
+        "gids_cache_reuse": ([vp, vp], C.c_int),
         "gids_set_storage_file": ([vp, C.c_char_p, i64, i32, i64, i32, i32], C.c_int),
         "gids_storage_file_stats": ([vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64),
                                      C.POINTER(C.c_double), C.POINTER(i32)], C.c_int),
@@ -126,7 +129,8 @@ def exported_symbols() -> list[str]:
             "gids_reverse_pagerank", "gids_load_graph_device", "gids_device_alloc",
             "gids_device_free", "gids_ipc_handle",
             "gids_ipc_open", "gids_ipc_close", "gids_set_sharded_table", "gids_shard_counts",
-            "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats"]
+            "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats",
+            "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -292,6 +296,21 @@ class Handle:
 
     def serve_decisions(self, kind, line, stream: int) -> None:
         check(lib().gids_serve_decisions(self.h, _p(kind), _p(line), stream), "serve_decisions")
+
+    def cache_window_update(self, nodes, counts, stream: int) -> None:
+        check(lib().gids_cache_window_update(self.h, _p(nodes), nodes.numel(),
+                                             _p(counts) if counts is not None else None, stream),
+              "cache_window_update")
+
+    def cache_access(self, nodes, kind, line, victim, stream: int) -> None:
+        check(lib().gids_cache_access(self.h, _p(nodes), nodes.numel(), _p(kind), _p(line),
+                                      _p(victim) if victim is not None else None, stream),
+              "cache_access")
+
+    def cache_reuse(self, num_nodes: int) -> np.ndarray:
+        out = np.zeros(num_nodes, np.uint32)
+        check(lib().gids_cache_reuse(self.h, out.ctypes.data), "cache_reuse")
+        return out
 
     def cache_stats(self) -> CacheCounters:
         c = CacheCounters()

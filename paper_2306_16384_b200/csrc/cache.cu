@@ -60,16 +60,23 @@ __global__ void k_contribution(const int32_t* __restrict__ uniq, SampleCounters*
 }
 
 // window_update + reuse consumption; ev[p] = (line_at_start+1)<<1 | (count_after>0)
+// mode bit 1: window_update (raise by the lookahead counts, Safe->InUse flip);
+// mode bit 2: the accesses' reuse consumption (writes ev).  The serving path
+// runs both fused (every node of a batch is accessed right after the update);
+// the standalone CacheState API runs them separately.  counts (optional)
+// receives each node's lookahead count.
 __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                                  const uint8_t* __restrict__ future, uint32_t* reuse,
                                  const int32_t* __restrict__ slot_of, uint32_t* safe_bits,
                                  uint32_t* blk_cnt, uint32_t* sup_cnt, int exact,
-                                 CacheMeta* meta, uint32_t* ev) {
+                                 CacheMeta* meta, uint32_t* ev, int mode = 3,
+                                 int32_t* counts = nullptr) {
     int64_t inc = 0, dec = 0, unsafe = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = (int32_t)uniq[p];
-        uint32_t c = future[x];
+        uint32_t c = (mode & 1) ? future[x] : 0u;
+        if (counts) counts[p] = (int32_t)c;
         uint32_t old = reuse[x];
         uint32_t now = old + c;
         int32_t s = slot_of[x];
@@ -87,12 +94,12 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                 }
             }
         }
-        if (now > 0) {
+        if ((mode & 2) && now > 0) {
             now--;
             dec++;
         }
         reuse[x] = now;
-        ev[p] = ((uint32_t)(s + 1) << 1) | (now > 0 ? 1u : 0u);
+        if (mode & 2) ev[p] = ((uint32_t)(s + 1) << 1) | (now > 0 ? 1u : 0u);
     }
     inc = warp_sum64(inc);
     dec = warp_sum64(dec);
@@ -479,12 +486,13 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
 __global__ void k_post_a(const int64_t* __restrict__ uniq, const ServeCounters* svc,
                          const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
                          const int32_t* __restrict__ line_node, int32_t* slot_of, int32_t* last_ins,
-                         uint32_t* g_evict, int clear_evict) {
+                         uint32_t* g_evict, int clear_evict, int64_t* victim = nullptr) {
     int64_t n = svc->n_log;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t t = log_line[i];
         int32_t o = line_node[t];
+        if (victim) victim[log_pos[i]] = o;  // the line's occupant at the batch start
         if (o >= 0) slot_of[o] = -1;
         slot_of[uniq[log_pos[i]]] = -1;
         atomicMax(&last_ins[t], (int32_t)i);
@@ -839,5 +847,92 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         h->gather_pending[par] = h->profiling;
         h->serve_timed = h->profiling;
     }
+    return GIDS_OK;
+}
+
+// ------------------------------------------------ standalone CacheState API
+// window_update (cache.py:190-218) and CacheState.access (cache.py:144-180)
+// as separate calls, for callers that drive the cache directly (the reference
+// exports both); the serving path fuses them in gids_launch_serve.
+extern "C" int gids_cache_window_update(gids_handle* h, const int64_t* nodes, int64_t n,
+                                        int32_t* counts, void* stream) {
+    if (!h || n < 0 || (n > 0 && !nodes)) {
+        gids_set_error("cache_window_update: bad arguments");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaSetDevice(h->device));
+    if (n == 0) return GIDS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    h->last_stream = st;
+    const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
+    k_window_consume<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
+        nodes, n, h->future, h->reuse, h->slot_of, h->safe_bits, h->blk_cnt, h->sup_cnt,
+        exact ? 1 : 0, h->meta, h->ev, 1, counts);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
+}
+
+extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n,
+                                 int8_t* kind_out, int32_t* line_out, int64_t* victim_out,
+                                 void* stream) {
+    if (!h || n < 0 || (n > 0 && (!nodes || !kind_out || !line_out))) {
+        gids_set_error("cache_access: bad arguments");
+        return GIDS_E_INVALID;
+    }
+    if (h->cfg.policy != GIDS_POLICY_EXACT) {
+        gids_set_error("cache_access drives the reference (exact) policy");
+        return GIDS_E_INVALID;
+    }
+    if (n > h->serve_cap) {
+        gids_set_error("cache_access: more nodes than the handle's serving workspace");
+        return GIDS_E_CAPACITY;
+    }
+    GIDS_CUDA_TRY(cudaSetDevice(h->device));
+    if (n == 0) return GIDS_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    h->last_stream = st;
+    for (int b = 0; b < 2; b++)  // a served batch's gather may still read the lines
+        if (h->gathered_valid[b]) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->gathered[b], 0));
+    GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
+    GIDS_CUDA_TRY(cudaMemsetAsync(h->ins, 0xff, sizeof(int32_t) * n, st));
+    if (victim_out) GIDS_CUDA_TRY(cudaMemsetAsync(victim_out, 0xff, sizeof(int64_t) * n, st));
+    const int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
+    k_window_consume<<<g, BLOCK, 0, st>>>(nodes, n, h->future, h->reuse, h->slot_of,
+                                          h->safe_bits, h->blk_cnt, h->sup_cnt, 1, h->meta, h->ev,
+                                          2, nullptr);
+    GIDS_LAUNCH_CHECK(h);
+    size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
+    if (smem > 48 * 1024)
+        GIDS_CUDA_TRY(cudaFuncSetAttribute(k_exact_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+    k_exact_seq<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits, h->evict_bits,
+                                     h->blk_cnt, h->sup_cnt, h->exact_smem ? 1 : 0, h->kind,
+                                     h->line, h->log_line, h->log_pos, h->svc);
+    GIDS_LAUNCH_CHECK(h);
+    k_post_a<<<g, BLOCK, 0, st>>>(nodes, h->svc, h->log_line, h->log_pos, h->line_node,
+                                  h->slot_of, h->last_ins, h->evict_bits, h->exact_smem ? 0 : 1,
+                                  victim_out);
+    GIDS_LAUNCH_CHECK(h);
+    k_post_b<<<g, BLOCK, 0, st>>>(nodes, h->svc, h->log_line, h->log_pos, h->line_node,
+                                  h->slot_of, h->last_ins, h->ins);
+    GIDS_LAUNCH_CHECK(h);
+    k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
+    GIDS_LAUNCH_CHECK(h);
+    GIDS_CUDA_TRY(cudaMemcpyAsync(kind_out, h->kind, n, cudaMemcpyDeviceToDevice, st));
+    GIDS_CUDA_TRY(cudaMemcpyAsync(line_out, h->line, sizeof(int32_t) * n,
+                                  cudaMemcpyDeviceToDevice, st));
+    return GIDS_OK;
+}
+
+// per-node predicted-reuse counters (reuse_counter, cache.py:104-113), host copy
+extern "C" int gids_cache_reuse(gids_handle* h, uint32_t* reuse_host) {
+    if (!h || !reuse_host) {
+        gids_set_error("cache_reuse: bad arguments");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaSetDevice(h->device));
+    GIDS_CUDA_TRY(cudaDeviceSynchronize());
+    GIDS_CUDA_TRY(cudaMemcpy(reuse_host, h->reuse, sizeof(uint32_t) * h->N,
+                             cudaMemcpyDeviceToHost));
     return GIDS_OK;
 }

@@ -10,12 +10,17 @@ module keeps the reference's vocabulary around it:
   the GPU ``window_update`` reads (cache.py:190-218)
 * ``GpuCacheView``  read-only CacheState-like counters of a handle
   (cache.py:104-113,182-187)
+* ``CacheState`` / ``window_update``  cache.py:94-218 driven directly: the
+  reference's exact policy on a libgids handle of its own (HBM), for callers
+  that use the cache without the loader
 """
 from __future__ import annotations
 
 from collections import deque
 from dataclasses import dataclass
 from enum import Enum, IntEnum
+
+import numpy as np
 
 from . import _native
 
@@ -75,9 +80,18 @@ class WindowBuffer:
         return len(self.lists)
 
     def push_iteration(self, nodes, trusted: bool = False) -> None:
-        """Append one future iteration's ascending unique list (a CUDA int64 tensor)."""
+        """Append one future iteration's ascending unique list (a CUDA int64
+        tensor; an unbound window also takes array-likes, as the reference's)."""
         if len(self.lists) >= self.depth:
             raise CacheProtocolError(f"window already holds {self.depth} iterations")
+        if not hasattr(nodes, "numel"):
+            if self._h is not None:
+                raise TypeError("a handle-bound window takes CUDA int64 tensors")
+            nodes = np.asarray(nodes, dtype=np.int64)
+            if len(nodes) > 1 and np.any(np.diff(nodes) <= 0):
+                raise CacheProtocolError("iteration list must be ascending and unique")
+            self.lists.append(nodes)
+            return
         if not trusted and nodes.numel() > 1 and not bool((nodes[1:] > nodes[:-1]).all()):
             raise CacheProtocolError("iteration list must be ascending and unique")
         self.lists.append(nodes)
@@ -128,3 +142,110 @@ class GpuCacheView:
 
     def eviction_rng_words(self):
         return self._h.cache_rng()
+
+
+NodeId = int
+
+
+class CacheState(GpuCacheView):
+    """CacheState (cache.py:94-187) in HBM, driven by libgids.
+
+    The reference's policy exactly (fully associative, lowest empty line
+    first, uniform eviction among SafeToEvict lines from the numpy stream of
+    ``eviction_seed``, bypass when every line is InUse).  Same constructor
+    plus ``num_nodes`` (per-node state is dense on the GPU) and ``device``.
+    ``access(node)`` serves one node like the reference; ``access_batch``
+    serves distinct nodes in order in one call (the loader's path)."""
+
+    def __init__(self, capacity_lines: int, line_bytes: int, eviction_seed: int = 0, *,
+                 num_nodes: int, device: int = 0):
+        if capacity_lines < 0:
+            raise ValueError("capacity_lines must be non-negative")
+        if line_bytes < 1:
+            raise ValueError("line_bytes must be positive")
+        if num_nodes < 1:
+            raise ValueError("num_nodes must be positive")
+        import torch
+
+        from .sampling import pcg_words
+        self.num_nodes = num_nodes
+        self._dev = torch.device("cuda", device)
+        h = _native.Handle(num_nodes=num_nodes, num_edges=0, feature_dim=1, device=device,
+                           cache_lines=capacity_lines, policy="exact", ways=32, evict_key=0,
+                           window_depth=255, fanouts=[1], max_seeds=num_nodes,
+                           eviction_words=pcg_words(np.random.default_rng(eviction_seed)))
+        super().__init__(h, line_bytes)
+        self._owned = h
+
+    def _nodes(self, nodes):
+        import torch
+        arr = np.asarray(nodes, dtype=np.int64).reshape(-1)
+        if len(arr) and (arr.min() < 0 or arr.max() >= self.num_nodes):
+            bad = int(arr[(arr < 0) | (arr >= self.num_nodes)][0])
+            raise ValueError(f"node {bad} out of range (num_nodes={self.num_nodes})")
+        return torch.as_tensor(arr).to(self._dev)
+
+    def access_batch(self, nodes):
+        """Serve distinct nodes in order: (kind int8[n] of _native.KIND_*,
+        line int32[n], -1 on bypass)."""
+        import torch
+        t = self._nodes(nodes)
+        n = t.numel()
+        if n > 1 and int(torch.unique(t).numel()) != n:
+            raise ValueError("access_batch takes distinct nodes (use access() per repeat)")
+        kind = torch.empty(n, dtype=torch.int8, device=self._dev)
+        line = torch.empty(n, dtype=torch.int32, device=self._dev)
+        st = _native.stream_ptr(self._dev.index)
+        self._h.cache_access(t, kind, line, None, st)
+        return kind.cpu().numpy(), line.cpu().numpy()
+
+    def access(self, node: NodeId) -> AccessResult:
+        """Serve one node; classify as hit, miss (inserted), or bypass."""
+        import torch
+        t = self._nodes([node])
+        kind = torch.empty(1, dtype=torch.int8, device=self._dev)
+        line = torch.empty(1, dtype=torch.int32, device=self._dev)
+        victim = torch.empty(1, dtype=torch.int64, device=self._dev)
+        self._h.cache_access(t, kind, line, victim, _native.stream_ptr(self._dev.index))
+        k = KIND_OF_CODE[int(kind.item())]
+        if k is AccessKind.BYPASS:
+            return AccessResult(k)
+        v = int(victim.item())
+        return AccessResult(k, slot=int(line.item()),
+                            evicted=v if (k is AccessKind.MISS and v >= 0) else None)
+
+    @property
+    def slot_node(self) -> np.ndarray:
+        return self._h.cache_lines()[0]
+
+    @property
+    def line_state(self) -> np.ndarray:
+        return self._h.cache_lines()[1]
+
+    @property
+    def reuse_counter(self) -> dict:
+        r = self._h.cache_reuse(self.num_nodes)
+        nz = np.flatnonzero(r)
+        return dict(zip(nz.tolist(), r[nz].astype(np.int64).tolist()))
+
+    def close(self) -> None:
+        self._owned.close()
+
+
+def window_update(cache: CacheState, window: WindowBuffer, current_batch) -> dict:
+    """Fold the current batch's future occurrences into the cache metadata
+    (cache.py:190-218): each node's count of window lists containing it
+    raises its reuse counter and flips its resident SafeToEvict line to
+    InUse, on the GPU.  Returns {node: count} for the whole batch."""
+    import torch
+    h = cache._h
+    st = _native.stream_ptr(cache._dev.index)
+    cur = cache._nodes(current_batch)
+    lists = [l if hasattr(l, "numel") else cache._nodes(l) for l in window.lists]
+    for l in lists:
+        h.window_push(l, st)
+    counts = torch.zeros(cur.numel(), dtype=torch.int32, device=cache._dev)
+    h.cache_window_update(cur, counts, st)
+    for l in lists:
+        h.window_pop(l, st)
+    return dict(zip(cur.cpu().tolist(), counts.cpu().tolist()))
