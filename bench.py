@@ -95,6 +95,29 @@ def load_peaks() -> dict:
         return {}
 
 
+def bind_to_gpu_numa(dev: int) -> dict:
+    """Pin this rank's threads to the CPUs of its GPU's NUMA node before any
+    host allocation, so the pinned tiers (first-touched by the allocating
+    thread) sit on the socket whose root complex the GPU hangs off and the
+    host-link reads do not cross the inter-socket link.  Best effort."""
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        bdf = f"{p.pci_domain_id:04x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+        base = Path("/sys/bus/pci/devices") / bdf
+        node = int((base / "numa_node").read_text())
+        cpus = set()
+        for part in (base / "local_cpulist").read_text().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0) or cpus
+        if cpus and len(cpus) < os.cpu_count():
+            os.sched_setaffinity(0, cpus)
+        return {"pci": bdf, "numa_node": node, "cpus": len(os.sched_getaffinity(0))}
+    except Exception as e:  # no sysfs / single-socket box: nothing to do
+        return {"skipped": repr(e)[:80]}
+
+
 def load_traffic() -> dict:
     """dram read+write bytes per launch of each workload's dominant kernel,
     from one committed `ncu --set full` capture (profiles/ncu_traffic.json)."""
@@ -369,6 +392,7 @@ def main() -> None:
         else:
             dist.init_process_group(backend)
     torch.cuda.set_device(local)
+    numa = bind_to_gpu_numa(local) if os.environ.get("BENCH_NUMA_BIND", "1") == "1" else None
     cfg = make_config({**cfg_dict, "gids_device": local, "gids_dp_rank": rank,
                        "gids_dp_world": world})
     t_setup = time.perf_counter()
@@ -523,6 +547,7 @@ def main() -> None:
                         "batches in, host-tier rows over the link, per-step stats read back"},
         "gpu_launches": launches, "clocks": clocks,
         "storage_file": dl.storage_stats(),
+        "numa": numa,
         "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),
         "e2e_host_ms_per_call": {"min": float(np.min(call_ms)), "median": float(np.median(call_ms)),
                                  "p90": float(np.percentile(call_ms, 90)),
