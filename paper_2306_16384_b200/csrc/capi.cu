@@ -148,7 +148,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->draw_off, h->front_cap + 1);
     A(h->edges, 2 * h->edge_cap);
     A(h->unique32, h->unique_cap);
-    A(h->jump_tab, 128);
+    A(h->jump_tab, GIDS_JUMP_TAB);
     A(h->rng_dev, 2);
     A(h->sc, 1);
     h->scan_parts_cap = 1024;
@@ -179,7 +179,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     }
     GIDS_CUDA_TRY(cudaMallocHost((void**)&h->sc_host, sizeof(SampleCounters)));
     GIDS_CUDA_TRY(cudaMallocHost((void**)&h->svc_host, sizeof(ServeCounters)));
-    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->jump_host, sizeof(u128) * 128));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->jump_host, sizeof(u128) * GIDS_JUMP_TAB));
     GIDS_CUDA_TRY(cudaMallocHost((void**)&h->rng_host, sizeof(u128) * 2));
     GIDS_CUDA_TRY(cudaMemset(h->pinned_off, 0xff, sizeof(int32_t) * N));
     GIDS_CUDA_TRY(cudaMemset(h->slot_of, 0xff, sizeof(int32_t) * N));
@@ -226,6 +226,8 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         int blocks = (wps * GIDS_SMS + 7) / 8;
         h->gather_blocks = blocks;
         h->gather_unroll = 2;
+        const char* ng = getenv("GIDS_NO_GRAPHS");
+        h->use_graphs = !(ng && ng[0] == '1');
         if (const char* e = getenv("GIDS_GATHER_UNROLL")) {
             int u = atoi(e);
             h->gather_unroll = u >= 8 ? 8 : u >= 4 ? 4 : u >= 2 ? 2 : 1;
@@ -251,6 +253,8 @@ int gids_destroy(gids_handle* h) {
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     gids_file_free(h);
+    for (int i = 0; i < h->n_sgraphs; i++)
+        if (h->sgraphs[i].exec) cudaGraphExecDestroy(h->sgraphs[i].exec);
     void* ptrs[] = {h->indptr,    h->indices,  h->pinned_off, h->cache_rows, h->slot_of,
                     h->line_node, h->safe_bits, h->evict_bits, h->blk_cnt,   h->sup_cnt,
                     h->reuse,     h->future,   h->meta,       h->last_ins,   h->bm_front,

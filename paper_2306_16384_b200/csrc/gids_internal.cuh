@@ -149,6 +149,14 @@ struct CacheMeta {  // persistent cache counters (CacheState)
 
 struct FileTier;
 
+// one instantiated sampling graph per distinct seed count (sampler.cu)
+struct SampleGraph {
+    int64_t n_seeds;
+    int64_t kernels;  // kernel nodes, for the launch counter
+    cudaGraphExec_t exec;
+};
+constexpr int GIDS_MAX_SGRAPHS = 4;
+
 struct gids_handle {
     gids_config cfg;
     int device;
@@ -196,7 +204,7 @@ struct gids_handle {
     int64_t* edges;        // [2*edge_cap]
     int32_t* unique32;     // [front_cap_all]
     int64_t unique_cap;
-    u128* jump_tab;        // [64][2] {A_i, H_i} for the sampler stream's inc
+    u128* jump_tab;        // [GIDS_JUMP_TAB] jumps {A_i, H_i} of 2^i, then steps of k <= 1024
     u128* jump_host;       // pinned staging of the table
     u128* rng_dev;         // [2] device-resident sampler stream: state, inc
     u128* rng_host;        // pinned staging
@@ -255,6 +263,11 @@ struct gids_handle {
     int32_t n_shards;      // 0 = tiered mode (cache + host tiers)
     int32_t my_shard;
     const float** shard_ptrs;  // device array [n_shards]
+
+    // CUDA graphs of the sampling sequence (GIDS_NO_GRAPHS=1 disables)
+    bool use_graphs;
+    int n_sgraphs;
+    SampleGraph sgraphs[GIDS_MAX_SGRAPHS];
 
     // file-backed storage tier (storage_file.cu); null = pinned-host tier
     struct FileTier* ft;
@@ -368,3 +381,4 @@ static inline int gids_grid(int64_t work, int block, int max_blocks) {
     return (int)g;
 }
 constexpr int GIDS_SMS = 148;
+constexpr int GIDS_JUMP_TAB = 128 + 2 * 1025;  // sampler LCG tables (sampler.cu)

@@ -45,7 +45,13 @@ __global__ void k_seed_mark(const int64_t* __restrict__ seeds, int64_t n, uint32
     }
 }
 
-// one warp per frontier node; fanout <= 32 keeps the swap targets in registers
+// Each warp takes a contiguous run of frontier nodes (ascending ids, so the
+// indptr reads are near each other) and walks the draw stream along it: one
+// full jump to the run's first offset, then per node every lane t reaches its
+// draw with ONE LCG step of t+1 (x -> A_{t+1} x + H_{t+1}, step table) and the
+// run's state moves on by the node's draw count -- instead of a full
+// O(log offset) jump per draw.  fanout <= 32 keeps the swap targets in
+// registers; larger fanouts stage them in shared memory.
 __global__ void __launch_bounds__(SAMPLE_BLOCK)
 k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ indices,
                const int32_t* __restrict__ front, const int64_t* __restrict__ take_off,
@@ -61,10 +67,19 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
     for (int l = 0; l < layer; l++) ebase += sc->layer_len[l];
     const uint64_t dbase = (uint64_t)sc->layer_draw_base[layer];
     const u128 s0 = rng_state[0];  // stream state at the start of this batch
+    const u128* step = tab + 128;  // step[2k], step[2k+1] = A_k, H_k
     int64_t* jw = j_smem + (int64_t)wib * fanout;
 
-    for (int64_t i = (int64_t)blockIdx.x * SAMPLE_WARPS + wib; i < nf;
-         i += (int64_t)gridDim.x * SAMPLE_WARPS) {
+    const int64_t nwarps = (int64_t)gridDim.x * SAMPLE_WARPS;
+    const int64_t per = (nf + nwarps - 1) / nwarps;
+    const int64_t i0 = ((int64_t)blockIdx.x * SAMPLE_WARPS + wib) * per;
+    const int64_t i1 = i0 + per < nf ? i0 + per : nf;
+    if (i0 >= i1) return;
+    // stream state before this run's first draw
+    u128 s = jump(s0, dbase + (uint64_t)draw_off[i0], tab);
+    const u128 Af = step[2 * fanout], Hf = step[2 * fanout + 1];
+
+    for (int64_t i = i0; i < i1; i++) {
         const int32_t v = front[i];
         const int64_t lo = indptr[v];
         const int64_t deg = indptr[v + 1] - lo;
@@ -80,19 +95,18 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
             }
             continue;
         }
-        const uint64_t r0 = dbase + (uint64_t)draw_off[i];
         if (fanout <= 32) {
             int64_t j = 0;
             if (lane < fanout) {
-                // draw r0+lane is the output of the state r0+lane+1 steps on
-                double u = (double)(pcg_output(jump(s0, r0 + lane + 1, tab)) >> 11) *
-                           (1.0 / 9007199254740992.0);
+                // draw t is the output of the state t+1 steps past s
+                const u128 st = add128(mul128(step[2 * (lane + 1)], s), step[2 * (lane + 1) + 1]);
+                double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
                 j = lane + (int64_t)__dmul_rn(u, (double)(deg - lane));
             }
             int64_t p = j;
-            for (int s = 30; s >= 0; s--) {
-                int64_t js = __shfl_sync(0xffffffffu, j, s);
-                if (s < lane && js == p) p = s;
+            for (int q = 30; q >= 0; q--) {
+                int64_t jq = __shfl_sync(0xffffffffu, j, q);
+                if (q < lane && jq == p) p = q;
             }
             if (lane < fanout) {
                 int32_t src = indices[lo + p];
@@ -103,15 +117,15 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
             }
         } else {
             for (int t = lane; t < fanout; t += 32) {
-                double u = (double)(pcg_output(jump(s0, r0 + t + 1, tab)) >> 11) *
-                           (1.0 / 9007199254740992.0);
+                const u128 st = add128(mul128(step[2 * (t + 1)], s), step[2 * (t + 1) + 1]);
+                double u = (double)(pcg_output(st) >> 11) * (1.0 / 9007199254740992.0);
                 jw[t] = t + (int64_t)__dmul_rn(u, (double)(deg - t));
             }
             __syncwarp();
             for (int t = lane; t < fanout; t += 32) {
                 int64_t p = jw[t];
-                for (int s = t - 1; s >= 0; s--)
-                    if (jw[s] == p) p = s;
+                for (int q = t - 1; q >= 0; q--)
+                    if (jw[q] == p) p = q;
                 int32_t src = indices[lo + p];
                 out[2 * t] = src;
                 out[2 * t + 1] = v;
@@ -120,6 +134,7 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
             }
             __syncwarp();
         }
+        s = add128(mul128(Af, s), Hf);  // past this node's `fanout` draws
     }
 }
 
@@ -156,7 +171,9 @@ __global__ void k_widen(const int32_t* __restrict__ in, const SampleCounters* sc
 
 }  // namespace
 
-// LCG jump tables for one increment: A_i = M^(2^i), H_i = inc * sum_{k<2^i} M^k
+// LCG tables for one increment: jumps A_i = M^(2^i), H_i = inc * sum_{k<2^i} M^k
+// (i < 64, entries 0..127), then single steps of k = 0..MAX_FANOUT:
+// A_k = M^k, H_k = inc * sum_{j<k} M^j (entries 128 + 2k, 128 + 2k + 1)
 static void build_jump_table(uint64_t inc_hi, uint64_t inc_lo, u128* tab) {
     u128 cm{PCG_MULT_LO, PCG_MULT_HI}, cp{inc_lo, inc_hi};
     for (int i = 0; i < 64; i++) {
@@ -165,33 +182,21 @@ static void build_jump_table(uint64_t inc_hi, uint64_t inc_lo, u128* tab) {
         cp = mul128(add128(cm, u128{1, 0}), cp);
         cm = mul128(cm, cm);
     }
+    const u128 m{PCG_MULT_LO, PCG_MULT_HI}, inc{inc_lo, inc_hi};
+    u128 a{1, 0}, hh{0, 0};
+    for (int k = 0; k <= MAX_FANOUT; k++) {
+        tab[128 + 2 * k] = a;
+        tab[128 + 2 * k + 1] = hh;
+        hh = add128(mul128(m, hh), inc);  // x_{k+1} = M x_k + inc
+        a = mul128(m, a);
+    }
 }
 
-int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaStream_t st) {
+// The per-batch sampling sequence (~20 kernels and copies, all sized by
+// n_seeds and the handle's bounds, every count staying on the device):
+// capturable as one CUDA graph.
+static int sample_body(gids_handle* h, int64_t n_seeds, cudaStream_t st) {
     const gids_config& c = h->cfg;
-    for (int l = 0; l < c.n_layers; l++)
-        if (c.fanouts[l] > MAX_FANOUT) {
-            gids_set_error("fanout above 1024 is not supported by the CUDA sampler");
-            return GIDS_E_INVALID;
-        }
-    gids_sample_begin(h, st);
-    if (w) {  // (re)seed the device-resident stream from the host Generator
-        if (!h->jump_valid || h->jump_inc_hi != w[2] || h->jump_inc_lo != w[3]) {
-            build_jump_table(w[2], w[3], h->jump_host);
-            GIDS_CUDA_TRY(cudaMemcpyAsync(h->jump_tab, h->jump_host, sizeof(u128) * 128,
-                                          cudaMemcpyHostToDevice, st));
-            GIDS_CUDA_TRY(cudaStreamSynchronize(st));  // staging buffer is reused
-            h->jump_valid = true;
-            h->jump_inc_hi = w[2];
-            h->jump_inc_lo = w[3];
-        }
-        k_rng_set<<<1, 1, 0, st>>>(h->rng_dev, u128{w[1], w[0]}, u128{w[3], w[2]});
-        GIDS_LAUNCH_CHECK(h);
-    } else if (!h->jump_valid) {
-        gids_set_error("sampler stream not seeded (pass the Generator state once)");
-        return GIDS_E_STATE;
-    }
-
     GIDS_CUDA_TRY(cudaMemsetAsync(h->sc, 0, sizeof(SampleCounters), st));
     k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
                                                                      h->bm_front, h->bm_all);
@@ -204,10 +209,6 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
         rc = gids_scan_take_draw(h, f, l, st);
         if (rc) return rc;
         size_t smem = f > 32 ? (size_t)SAMPLE_WARPS * f * sizeof(int64_t) : 0;
-        if (smem > 48 * 1024)
-            GIDS_CUDA_TRY(cudaFuncSetAttribute(k_sample_layer,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)smem));
         int64_t bound = l == 0 ? n_seeds : h->front_cap;
         int grid = gids_grid(bound, SAMPLE_WARPS, 16 * GIDS_SMS);
         k_sample_layer<<<grid, SAMPLE_BLOCK, smem, st>>>(
@@ -224,9 +225,84 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
     if (rc) return rc;
     k_rng_advance<<<1, 1, 0, st>>>(h->rng_dev, h->sc, c.n_layers, h->jump_tab);
     GIDS_LAUNCH_CHECK(h);
-    gids_sample_end(h, st);
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
                                   cudaMemcpyDeviceToHost, st));
+    return GIDS_OK;
+}
+
+int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaStream_t st) {
+    const gids_config& c = h->cfg;
+    for (int l = 0; l < c.n_layers; l++) {
+        if (c.fanouts[l] > MAX_FANOUT) {
+            gids_set_error("fanout above 1024 is not supported by the CUDA sampler");
+            return GIDS_E_INVALID;
+        }
+        size_t smem = c.fanouts[l] > 32 ? (size_t)SAMPLE_WARPS * c.fanouts[l] * sizeof(int64_t) : 0;
+        if (smem > 48 * 1024)  // set before any capture
+            GIDS_CUDA_TRY(cudaFuncSetAttribute(k_sample_layer,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem));
+    }
+    gids_sample_begin(h, st);
+    if (w) {  // (re)seed the device-resident stream from the host Generator
+        if (!h->jump_valid || h->jump_inc_hi != w[2] || h->jump_inc_lo != w[3]) {
+            build_jump_table(w[2], w[3], h->jump_host);
+            GIDS_CUDA_TRY(cudaMemcpyAsync(h->jump_tab, h->jump_host, sizeof(u128) * GIDS_JUMP_TAB,
+                                          cudaMemcpyHostToDevice, st));
+            GIDS_CUDA_TRY(cudaStreamSynchronize(st));  // staging buffer is reused
+            h->jump_valid = true;
+            h->jump_inc_hi = w[2];
+            h->jump_inc_lo = w[3];
+        }
+        k_rng_set<<<1, 1, 0, st>>>(h->rng_dev, u128{w[1], w[0]}, u128{w[3], w[2]});
+        GIDS_LAUNCH_CHECK(h);
+    } else if (!h->jump_valid) {
+        gids_set_error("sampler stream not seeded (pass the Generator state once)");
+        return GIDS_E_STATE;
+    }
+    // replay the batch's launch sequence as one CUDA graph (one per distinct
+    // seed count; not on the legacy default stream, which cannot capture)
+    int rc;
+    if (h->use_graphs && st != 0 && st != cudaStreamLegacy) {
+        SampleGraph* g = nullptr;
+        for (int i = 0; i < h->n_sgraphs; i++)
+            if (h->sgraphs[i].n_seeds == n_seeds) g = &h->sgraphs[i];
+        if (!g && h->n_sgraphs < GIDS_MAX_SGRAPHS) {
+            const int64_t l0 = h->launches;
+            GIDS_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            rc = sample_body(h, n_seeds, st);
+            cudaGraph_t graph = nullptr;
+            cudaError_t e = cudaStreamEndCapture(st, &graph);
+            if (rc) {
+                if (graph) cudaGraphDestroy(graph);
+                return rc;
+            }
+            if (e != cudaSuccess) {
+                gids_set_error(std::string("sampler graph capture: ") + cudaGetErrorString(e));
+                return GIDS_E_CUDA;
+            }
+            g = &h->sgraphs[h->n_sgraphs];
+            e = cudaGraphInstantiate(&g->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) {
+                gids_set_error(std::string("sampler graph instantiate: ") + cudaGetErrorString(e));
+                return GIDS_E_CUDA;
+            }
+            g->n_seeds = n_seeds;
+            g->kernels = h->launches - l0;
+            h->launches = l0;
+            h->n_sgraphs++;
+        }
+        if (g) {
+            GIDS_CUDA_TRY(cudaGraphLaunch(g->exec, st));
+            h->launches += g->kernels;
+            gids_sample_end(h, st);
+            return GIDS_OK;
+        }
+    }
+    rc = sample_body(h, n_seeds, st);
+    if (rc) return rc;
+    gids_sample_end(h, st);
     return GIDS_OK;
 }
 
