@@ -191,6 +191,7 @@ __device__ __forceinline__ void tab_clear_safe(const ExactTables& t, int64_t s) 
 constexpr int32_t NO_LINE = 0x7fffffff;
 constexpr int EV_AHEAD = 16;  // chunks of the event stream in flight
 constexpr int EV_RING = 32;
+constexpr int EV_FAST = 4;    // all-hit chunks decided together (fast path)
 
 __device__ __forceinline__ void list_insert(int32_t& sl, int32_t s) {
     const int lane = threadIdx.x & 31;
@@ -299,7 +300,64 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
         }
         asm volatile("cp.async.commit_group;");
     }
+    int fast_skip = 0;
     for (int64_t base = 0, chunk = 0; base < n; base += 32, chunk++) {
+        // fast path: EV_FAST consecutive full chunks in which every event is a
+        // hit change nothing order-dependent (no fill, eviction or bypass; the
+        // hits' InUse->Safe flips touch distinct lines and commute), so they
+        // are decided together -- the common case of a warm, large cache
+        if (fast_skip > 0) {
+            fast_skip--;
+        } else if (base + EV_FAST * 32 <= n) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(EV_AHEAD - EV_FAST));
+            __syncwarp();
+            uint32_t fe[EV_FAST];
+            bool all = true;
+#pragma unroll
+            for (int k = 0; k < EV_FAST; k++) {
+                fe[k] = ev_ring[(chunk + k) % EV_RING][lane];
+                const int32_t fs = (int32_t)(fe[k] >> 1) - 1;
+                all &= fs >= 0 && !((t.evict[fs >> 5] >> (fs & 31)) & 1u);
+            }
+            if (__all_sync(0xffffffffu, all)) {
+#pragma unroll
+                for (int k = 0; k < EV_FAST; k++) {
+                    const int32_t fs = (int32_t)(fe[k] >> 1) - 1;
+                    const bool fadd = !(fe[k] & 1u) && !((t.safe[fs >> 5] >> (fs & 31)) & 1u);
+                    if (fadd) tab_set_safe_atomic(t, fs);
+                    unsigned added = __ballot_sync(0xffffffffu, fadd);
+                    safe_count += __popc(added);
+                    if (list_ok) {
+                        if (safe_count > 32) {
+                            list_ok = false;
+                        } else {
+                            while (added) {
+                                const int l = __ffs(added) - 1;
+                                added &= added - 1;
+                                list_insert(sl, __shfl_sync(0xffffffffu, fs, l));
+                            }
+                        }
+                    }
+                    kind[base + k * 32 + lane] = (int8_t)GIDS_KIND_HIT;
+                    line[base + k * 32 + lane] = fs;
+                    // refill, one commit group per consumed chunk as below
+                    const int64_t nc = chunk + k + EV_AHEAD;
+                    const int64_t i = nc * 32 + lane;
+                    if (nc < nchunks && i < n) {
+                        const uint32_t sa =
+                            (uint32_t)__cvta_generic_to_shared(&ev_ring[nc % EV_RING][lane]);
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa),
+                                     "l"(ev + i));
+                    }
+                    asm volatile("cp.async.commit_group;");
+                }
+                hits += 32 * EV_FAST;
+                base += 32 * (EV_FAST - 1);
+                chunk += EV_FAST - 1;
+                continue;
+            }
+            fast_skip = 8;  // misses around: back off before probing again
+        }
         const int cnt = n - base < 32 ? (int)(n - base) : 32;
         const unsigned valid = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
         asm volatile("cp.async.wait_group %0;" ::"n"(EV_AHEAD - 1));
