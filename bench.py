@@ -485,7 +485,7 @@ def main() -> None:
                  hbm_bytes_step / (hbm_peak * 1e9) if hbm_peak else 0.0)
     step_s = ms_max / 1e3 / args.steps
     traffic = load_traffic().get(args.workload)
-    if dl.sharded is None:
+    if dl.sharded is None and host_ms >= hit_ms:
         roofline = {"bound": "host_link", "kernel": "k_gather_host",
                     "achieved": achieved_link, "peak": link_peak, "unit": "GB/s",
                     "frac": achieved_link / link_peak if achieved_link else None,
@@ -499,6 +499,15 @@ def main() -> None:
                     "hbm_kernel": {"kernel": "k_gather_hits",
                                    "achieved": hit_bytes / (hit_ms / 1e3) / 1e9 if hit_ms else None,
                                    "peak": hbm_peak, "unit": "GB/s"}}
+    elif dl.sharded is None:
+        # everything (or nearly) is a cache hit: the dominant gather is HBM -> HBM
+        hit_gbs = hit_bytes / (hit_ms / 1e3) / 1e9 if hit_ms else None
+        roofline = {"bound": "hbm", "kernel": "k_gather_hits", "achieved": hit_gbs,
+                    "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hit_gbs / hbm_peak if hit_gbs and hbm_peak else None,
+                    "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                    "algorithmic_bytes_per_launch": hit_bytes,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write bytes)"}
     else:
         # C5: rows come from the owners' HBM; the remote share crosses NVLink
         nvl_peak = peaks.get("nvlink_gbs") or 770.0
@@ -536,6 +545,8 @@ def main() -> None:
         "tier_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / step_s,
                           "host_link_peak_gbs": link_peak, "hbm_peak_gbs": hbm_peak},
         "roofline": roofline,
+        "step_bound": ("control stream (sampling + cache policy)" if ctl_ms > gat_ms else
+                       "gather stream (" + roofline["bound"] + ")"),
         "value_definition": "device pipeline: 1 / max(per-step sampling+decision time on the "
                             "control stream, per-step gather time on the gather stream), CUDA "
                             "events on each launching stream (a second pass of K steps after "
