@@ -23,6 +23,8 @@
 //   set-associative   32-way sets, one warp per set, lanes = ways; the same
 //                     contract per set with a counter-based eviction draw.
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "gids_internal.cuh"
 
@@ -167,23 +169,12 @@ __device__ __forceinline__ int64_t select_safe(const ExactTables& t, int64_t nw,
     return (w0 + f) * 32 + bit;
 }
 
-__device__ __forceinline__ void tab_set_safe(const ExactTables& t, int64_t s) {
-    t.safe[s >> 5] |= 1u << (s & 31);
-    t.blk[s >> 10]++;
-    t.sup[s >> 15]++;
-}
 // several lanes may mark different lines of one word / block at once
 __device__ __forceinline__ void tab_set_safe_atomic(const ExactTables& t, int64_t s) {
     atomicOr(&t.safe[s >> 5], 1u << (s & 31));
     atomicAdd(&t.blk[s >> 10], 1u);
     atomicAdd(&t.sup[s >> 15], 1u);
 }
-__device__ __forceinline__ void tab_clear_safe(const ExactTables& t, int64_t s) {
-    t.safe[s >> 5] &= ~(1u << (s & 31));
-    t.blk[s >> 10]--;
-    t.sup[s >> 15]--;
-}
-
 // ascending list of SafeToEvict lines held one per lane (lane i = i-th
 // smallest), valid while there are at most 32 of them: in the steady state of
 // a window-protected cache almost every eviction sees 1-3 safe lines, and
@@ -862,8 +853,8 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                                           h->flag_host);
         GIDS_LAUNCH_CHECK(h);
         // ordered compaction of the gather's work lists (CUB, stable)
-        cub::CountingInputIterator<int32_t> pos(0);
-        cub::TransformInputIterator<int2, HostItem, cub::CountingInputIterator<int32_t>> items(
+        thrust::counting_iterator<int32_t> pos(0);
+        thrust::transform_iterator<HostItem, thrust::counting_iterator<int32_t>, int2> items(
             pos, HostItem{uniq, h->pinned_off});
         if (!h->sel_tmp) {
             size_t b1 = 0, b2 = 0;

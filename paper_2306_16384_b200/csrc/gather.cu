@@ -29,43 +29,6 @@ __device__ __forceinline__ void st_stream(int4* p, int4 v) {
                  : "memory");
 }
 
-// copy one row with the warp; dst2 (may be null) receives a second copy
-__device__ __forceinline__ void copy_row(const float* __restrict__ src, float* __restrict__ dst,
-                                         float* __restrict__ dst2, int64_t dim, int lane) {
-    if ((dim & 3) == 0) {
-        const int4* s = reinterpret_cast<const int4*>(src);
-        int4* d = reinterpret_cast<int4*>(dst);
-        int4* d2 = reinterpret_cast<int4*>(dst2);
-        const int64_t nv = dim >> 2;
-        int64_t c = lane;
-        for (; c + 96 < nv; c += 128) {  // four 16-B loads in flight per lane
-            int4 a = ld_stream(s + c), b = ld_stream(s + c + 32), e = ld_stream(s + c + 64),
-                 f = ld_stream(s + c + 96);
-            st_stream(d + c, a);
-            st_stream(d + c + 32, b);
-            st_stream(d + c + 64, e);
-            st_stream(d + c + 96, f);
-            if (d2) {
-                d2[c] = a;
-                d2[c + 32] = b;
-                d2[c + 64] = e;
-                d2[c + 96] = f;
-            }
-        }
-        for (; c < nv; c += 32) {
-            int4 a = ld_stream(s + c);
-            st_stream(d + c, a);
-            if (d2) d2[c] = a;
-        }
-    } else {
-        for (int64_t c = lane; c < dim; c += 32) {
-            float v = src[c];
-            dst[c] = v;
-            if (dst2) dst2[c] = v;
-        }
-    }
-}
-
 // Work is a flat range of 16-byte chunks over the compacted row list: chunk
 // i is chunk (i % cpr) of list row (i / cpr), cpr = chunks per row.  Every
 // lane keeps UNROLL loads in flight before it stores, so a warp has

@@ -26,6 +26,7 @@
 //                         to a multiple of 8), evaluated level by level
 //      nxt *= d; nxt += c  -> two separately rounded operations (no FMA)
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
 
 #include <vector>
 
@@ -448,7 +449,7 @@ extern "C" int gids_reverse_pagerank(int device, int64_t N, int64_t E, const int
     GIDS_CUDA_TRY(cudaGetLastError());
     {
         size_t tb = 0;
-        cub::CountingInputIterator<int32_t> ids(0);
+        thrust::counting_iterator<int32_t> ids(0);
         GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, tb, ids, sink, sinks, nsink_d, N, st));
         void* tmp = nullptr;
         GIDS_CUDA_TRY(cudaMallocAsync(&tmp, tb, st));

@@ -120,9 +120,9 @@ k_gather_file(const int2* __restrict__ host_list, const int64_t* __restrict__ li
                                                      b0 % page);
                 }
                 v[k] = src[c];
-                d[k] = (int64_t)it.x * cpr + c;
+                d[k] = (int64_t)it.x * cpr + (int64_t)c;
                 const int32_t t = ins[it.x];
-                d2[k] = t >= 0 ? (int64_t)t * cpr + c : -1;
+                d2[k] = t >= 0 ? (int64_t)t * cpr + (int64_t)c : (int64_t)-1;
             }
         }
 #pragma unroll
