@@ -126,6 +126,13 @@ GIDS_API int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* uni
 GIDS_API int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev,
                                       int64_t* sizes_host, void* stream);
 GIDS_API int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* unique_cap);
+/* Run-ahead contribution (dataloader.py:188-192) of an exported batch --
+ * its unpinned, non-resident nodes -- against the cache as `stream` reaches
+ * the call: n is read through n_ptr (device-visible, e.g. the pinned sizes
+ * row of gids_sample_export_async), the count lands in out_host (pinned).
+ * Lets a caller sample ahead of the point where the reference samples. */
+GIDS_API int gids_contribution_async(gids_handle* h, const int64_t* unique_dev,
+                                     const int64_t* n_ptr, int64_t* out_host, void* stream);
 /* Device-resident sampler stream state (synchronises; for tests). */
 GIDS_API int gids_sampler_rng(gids_handle* h, uint64_t words_out[6]);
 

@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
                                    vp, vp], C.c_int),
         "gids_load_graph_device": ([vp, vp, vp], C.c_int),
+        "gids_contribution_async": ([vp, vp, vp, vp, vp], C.c_int),
         "gids_cache_window_update": ([vp, vp, i64, vp, vp], C.c_int),
         "gids_cache_access": ([vp, vp, i64, vp, vp, vp, vp], C.c_int),
         "gids_cache_reuse": ([vp, vp], C.c_int),
@@ -130,7 +131,8 @@ def exported_symbols() -> list[str]:
             "gids_device_free", "gids_ipc_handle",
             "gids_ipc_open", "gids_ipc_close", "gids_set_sharded_table", "gids_shard_counts",
             "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats",
-            "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse"]
+            "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse",
+            "gids_contribution_async"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -255,6 +257,10 @@ class Handle:
     def sample_export_async(self, edges, unique, sizes_host, stream: int) -> None:
         check(lib().gids_sample_export_async(self.h, _p(edges), _p(unique), _p(sizes_host),
                                              stream), "sample_export_async")
+
+    def contribution_async(self, unique, n_ptr: int, out_ptr: int, stream: int) -> None:
+        check(lib().gids_contribution_async(self.h, _p(unique), n_ptr, out_ptr, stream),
+              "contribution_async")
 
     def sample_capacity(self) -> tuple[int, int]:
         e, u = C.c_int64(), C.c_int64()

@@ -61,6 +61,22 @@ __global__ void k_contribution(const int32_t* __restrict__ uniq, SampleCounters*
                                                 (unsigned long long)c);
 }
 
+// the same count for an exported batch, at the moment it joins the run-ahead
+// queue: n read through a device-visible pointer (pinned host is fine)
+__global__ void k_contribution64(const int64_t* __restrict__ uniq, const int64_t* n_ptr,
+                                 const int32_t* __restrict__ pinned_off,
+                                 const int32_t* __restrict__ slot_of, unsigned long long* out) {
+    const int64_t n = *n_ptr;
+    int64_t c = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = uniq[i];
+        c += (pinned_off[x] < 0 && slot_of[x] < 0) ? 1 : 0;
+    }
+    c = warp_sum64(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
 // window_update + reuse consumption; ev[p] = (line_at_start+1)<<1 | (count_after>0)
 // mode bit 1: window_update (raise by the lookahead counts, Safe->InUse flip);
 // mode bit 2: the accesses' reuse consumption (writes ev).  The serving path
@@ -983,5 +999,28 @@ extern "C" int gids_cache_reuse(gids_handle* h, uint32_t* reuse_host) {
     GIDS_CUDA_TRY(cudaDeviceSynchronize());
     GIDS_CUDA_TRY(cudaMemcpy(reuse_host, h->reuse, sizeof(uint32_t) * h->N,
                              cudaMemcpyDeviceToHost));
+    return GIDS_OK;
+}
+
+// run-ahead contribution of an already exported batch (dataloader.py:188-192)
+// against the cache as the stream reaches this call: lets the loader sample
+// batches ahead of the moment the reference would, and still count them
+// against the reference's cache state
+extern "C" int gids_contribution_async(gids_handle* h, const int64_t* unique_dev,
+                                       const int64_t* n_ptr, int64_t* out_host, void* stream) {
+    if (!h || !unique_dev || !n_ptr || !out_host) {
+        gids_set_error("contribution_async: bad arguments");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaSetDevice(h->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long* scratch = reinterpret_cast<unsigned long long*>(h->contrib_dev);
+    GIDS_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(int64_t), st));
+    if (h->n_shards == 0) {  // a sharded table keeps every row resident: 0
+        k_contribution64<<<gids_grid(h->unique_cap, BLOCK, 4 * GIDS_SMS), BLOCK, 0, st>>>(
+            unique_dev, n_ptr, h->pinned_off, h->slot_of, scratch);
+        GIDS_LAUNCH_CHECK(h);
+    }
+    GIDS_CUDA_TRY(cudaMemcpyAsync(out_host, scratch, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     return GIDS_OK;
 }

@@ -151,6 +151,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->jump_tab, GIDS_JUMP_TAB);
     A(h->rng_dev, 2);
     A(h->sc, 1);
+    A(h->contrib_dev, 1);
     h->scan_parts_cap = 1024;
     A(h->scan_parts, 2 * h->scan_parts_cap);
     A(h->word_parts, h->scan_parts_cap);
@@ -266,7 +267,7 @@ int gids_destroy(gids_handle* h) {
                     h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
                     h->svc,       h->hit_list_buf[0], h->hit_list_buf[1], h->host_list_buf[0],
                     h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
-                    h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs};
+                    h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)

@@ -211,6 +211,7 @@ struct gids_handle {
     uint64_t jump_inc_hi, jump_inc_lo;
     bool jump_valid;
     SampleCounters* sc;    // device
+    int64_t* contrib_dev;  // device scratch of gids_contribution_async
     SampleCounters* sc_host;  // pinned mirror
     int64_t scan_parts_cap;
     int64_t* scan_parts;   // [scan_parts_cap * 2]

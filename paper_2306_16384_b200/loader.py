@@ -88,13 +88,15 @@ class _Queued:
     stream; ``resolve()`` waits for them (normally long finished) and fixes
     the sizes, the run-ahead contribution and the host Generator's offset."""
 
-    __slots__ = ("seeds", "edges", "unique", "sizes", "event", "batch", "storage_accesses")
+    __slots__ = ("seeds", "edges", "unique", "sizes", "event", "batch", "storage_accesses",
+                 "error")
 
     def __init__(self, seeds, edges, unique, sizes, event):
         self.seeds, self.edges, self.unique, self.sizes, self.event = \
             seeds, edges, unique, sizes, event
         self.batch = None
         self.storage_accesses = None
+        self.error = None
 
     def resolve(self, n_layers: int, rng) -> None:
         if self.batch is not None:
@@ -269,7 +271,10 @@ class Dataloader:
             self._sampler_rng = np.random.default_rng(sampler_ss)
         self._batches = _seed_stream(cfg, self.graph.num_nodes, work_ss, shuffle_ss)
         self._exhausted = False
+        self._seeds_done = False
         self._pending: deque[_Queued] = deque()
+        self._spec: deque[_Queued] = deque()  # sampled ahead, not yet admitted
+        self._spec_depth = cfg.gids_speculate
         self._resolved_storage = 0  # sum of resolved contributions of pending batches
         self._ringed = 0
         self._rng_on_device = False
@@ -279,7 +284,7 @@ class Dataloader:
         # the next one, and one freed but not yet retired)
         warm = [self._out_block() for _ in range(4)]
         del warm
-        ring = cfg.runahead_cap + 4
+        ring = cfg.runahead_cap + cfg.gids_speculate + 4
         self._sizes = torch.zeros((ring, len(cfg.fanouts) + 5), dtype=torch.int64,
                                   pin_memory=True)
         self._sizes_np = self._sizes.numpy()
@@ -368,15 +373,23 @@ class Dataloader:
                     return True
         return False
 
-    def _sample_one(self) -> bool:
-        """Launch one batch on the control stream; sizes are read lazily."""
+    def _launch_sample(self):
+        """Sample the next seed batch on the control stream (outputs exported
+        asynchronously); None when the seeds are exhausted.  A seed error is
+        carried in the entry and raised when the batch is admitted, where the
+        reference would raise it."""
         import torch
         try:
             seeds = next(self._batches)
         except StopIteration:
-            self._exhausted = True
-            return False
-        seeds = check_seeds(seeds, self.graph.num_nodes)
+            self._seeds_done = True
+            return None
+        try:
+            seeds = check_seeds(seeds, self.graph.num_nodes)
+        except ValueError as e:
+            q = _Queued(seeds, None, None, None, None)
+            q.error = e
+            return q
         st = self._ctl.cuda_stream
         words = None if self._rng_on_device else pcg_words(self._sampler_rng)
         self._h.sample(seeds, words, st)
@@ -387,10 +400,40 @@ class Dataloader:
         sizes = self._sizes[self._sizes_next]
         self._sizes_next = (self._sizes_next + 1) % len(self._sizes)
         self._h.sample_export_async(edges, unique, sizes, st)
-        ev = torch.cuda.Event()
-        ev.record(self._ctl)
-        self._pending.append(_Queued(seeds, edges, unique, sizes, ev))
+        return _Queued(seeds, edges, unique, sizes, None)
+
+    def _sample_one(self) -> bool:
+        """One batch joins the run-ahead queue (dataloader.py:194-205): the next
+        speculatively sampled batch, else a fresh one.  Its contribution is
+        counted now, against the cache as the reference would see it."""
+        import torch
+        q = self._spec.popleft() if self._spec else self._launch_sample()
+        if q is None:
+            self._exhausted = True
+            return False
+        if q.error is not None:
+            raise q.error
+        L = len(self.cfg.fanouts)
+        row = q.sizes.data_ptr()
+        self._h.contribution_async(q.unique, row + 8 * L, row + 8 * (L + 2),
+                                   self._ctl.cuda_stream)
+        q.event = torch.cuda.Event()
+        q.event.record(self._ctl)
+        self._pending.append(q)
         return True
+
+    def _speculate(self) -> None:
+        """Sample up to gids_speculate batches beyond the run-ahead queue, so
+        the sampling of the batch the next call admits runs while this batch
+        is gathered (the sampled content is fixed by the seed order and the
+        sampler stream, so it does not depend on when it is drawn)."""
+        while len(self._spec) < self._spec_depth and not self._seeds_done:
+            q = self._launch_sample()
+            if q is None:
+                break
+            self._spec.append(q)
+            if q.error is not None:
+                break
 
     def run_ahead(self) -> None:
         want = self.cfg.window_depth + 1
@@ -460,6 +503,7 @@ class Dataloader:
         stats = self._account(c.sampled, c.cache_hits, c.cpu_buffer_hits, c.storage,
                               c.bypasses, inflight)
         self._iteration += 1
+        self._speculate()
         return batch, rows, stats
 
     def _verify(self, unique, rows) -> None:

@@ -32,6 +32,9 @@ prefixed ``gids``) select the B200 path:
                       A synthetic config writes its table to
                       ``gids_storage_path`` first.
 * ``gids_io_threads`` / ``gids_io_direct``  pread threads / O_DIRECT for "file".
+* ``gids_speculate``  batches sampled ahead of the run-ahead queue (their
+                      contributions are still counted when they join it, so
+                      results are unchanged; 0 disables).
 """
 from __future__ import annotations
 
@@ -105,6 +108,7 @@ class PipelineConfig:
     gids_storage_path: str | None = None
     gids_io_threads: int = 8
     gids_io_direct: bool = False
+    gids_speculate: int = 2
 
     def ssd_spec(self) -> SsdSpec:
         if self.ssd_preset is None:
@@ -250,6 +254,7 @@ _RULES = [
     (lambda c: c.gids_storage != "file" or not c.gids_sharded_table,
      "gids_storage 'file' and gids_sharded_table are exclusive"),
     (lambda c: c.gids_io_threads >= 1, "gids_io_threads must be >= 1"),
+    (lambda c: c.gids_speculate >= 0, "gids_speculate must be non-negative"),
     (lambda c: c.gids_virtual_shards == 0 or c.gids_dp_world == 1,
      "gids_virtual_shards is for single-process runs (gids_dp_world 1)"),
 ]
