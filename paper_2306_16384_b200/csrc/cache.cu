@@ -162,13 +162,9 @@ __device__ __forceinline__ int64_t warp_find(const uint32_t* cnt, int64_t m, uin
     return -1;  // unreachable when r < total safe lines
 }
 
-// r-th SafeToEvict line in ascending line order (np.flatnonzero(mask)[r])
-__device__ __forceinline__ int64_t select_safe(const ExactTables& t, int64_t nw, int64_t nb,
-                                               int64_t ns, uint32_t r) {
-    int64_t sb = warp_find(t.sup, ns, r);
-    int64_t b0 = sb * 32;
-    int64_t bsel = b0 + warp_find(t.blk + b0, (nb - b0) < 32 ? (nb - b0) : 32, r);
-    int64_t w0 = bsel * 32;
+// r-th set bit among the 32 safe words starting at word w0 (warp-cooperative)
+__device__ __forceinline__ int64_t select_in_words(const ExactTables& t, int64_t nw, int64_t w0,
+                                                   uint32_t r) {
     const int lane = threadIdx.x & 31;
     uint32_t word = w0 + lane < nw ? t.safe[w0 + lane] : 0u;
     uint32_t c = __popc(word), inc = c;
@@ -183,6 +179,77 @@ __device__ __forceinline__ int64_t select_safe(const ExactTables& t, int64_t nw,
     uint32_t wsel = __shfl_sync(0xffffffffu, word, f);
     int bit = __fns(wsel, 0, (int)(r - excl) + 1);
     return (w0 + f) * 32 + bit;
+}
+
+// r-th SafeToEvict line in ascending line order (np.flatnonzero(mask)[r])
+__device__ __forceinline__ int64_t select_safe(const ExactTables& t, int64_t nw, int64_t nb,
+                                               int64_t ns, uint32_t r) {
+    int64_t sb = warp_find(t.sup, ns, r);
+    int64_t b0 = sb * 32;
+    int64_t bsel = b0 + warp_find(t.blk + b0, (nb - b0) < 32 ? (nb - b0) : 32, r);
+    return select_in_words(t, nw, bsel * 32, r);
+}
+
+// Caches of up to 128 blocks (131072 lines) also keep the inclusive prefix of
+// safe lines over the 1024-line blocks in registers, four blocks per lane,
+// updated in place on every change (a predicated add per lane, no
+// shuffles), so an eviction finds its block with one ballot instead of two
+// warp scans over the count tables.
+struct RegPrefix {
+    uint32_t p[4];  // safe lines in blocks [0, 4*lane + j]
+    __device__ __forceinline__ void add(int64_t b, int d) {
+        const int64_t mine = 4 * (int64_t)(threadIdx.x & 31);
+#pragma unroll
+        for (int j = 0; j < 4; j++) p[j] += (mine + j >= b) ? d : 0;
+    }
+};
+
+__device__ __forceinline__ void reg_prefix_init(RegPrefix& P, const ExactTables& t, int64_t nb) {
+    const int lane = threadIdx.x & 31;
+    uint32_t run = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int64_t b = 4 * (int64_t)lane + j;
+        run += b < nb ? t.blk[b] : 0u;
+        P.p[j] = run;
+    }
+    uint32_t inc = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += u;
+    }
+    const uint32_t before = inc - run;
+#pragma unroll
+    for (int j = 0; j < 4; j++) P.p[j] += before;
+}
+
+__device__ __forceinline__ int64_t select_reg(const ExactTables& t, int64_t nw,
+                                              const RegPrefix& P, uint32_t r) {
+    const int lane = threadIdx.x & 31;
+    const unsigned bal = __ballot_sync(0xffffffffu, P.p[3] > r);
+    const int f = __ffs(bal) - 1;
+    const uint32_t q0 = __shfl_sync(0xffffffffu, P.p[0], f);
+    const uint32_t q1 = __shfl_sync(0xffffffffu, P.p[1], f);
+    const uint32_t q2 = __shfl_sync(0xffffffffu, P.p[2], f);
+    const uint32_t up = __shfl_sync(0xffffffffu, P.p[3], f > 0 ? f - 1 : 0);
+    int j;
+    uint32_t excl;
+    if (q0 > r) {
+        j = 0;
+        excl = f > 0 ? up : 0u;
+    } else if (q1 > r) {
+        j = 1;
+        excl = q0;
+    } else if (q2 > r) {
+        j = 2;
+        excl = q1;
+    } else {
+        j = 3;
+        excl = q2;
+    }
+    (void)lane;
+    return select_in_words(t, nw, (int64_t)(4 * f + j) * 32, r - excl);
 }
 
 // several lanes may mark different lines of one word / block at once
@@ -210,6 +277,22 @@ __device__ __forceinline__ void list_remove(int32_t& sl, int r) {
     const int lane = threadIdx.x & 31;
     const int32_t down = __shfl_down_sync(0xffffffffu, sl, 1);
     sl = lane < r ? sl : (lane == 31 ? NO_LINE : down);
+}
+
+// `added` lanes just made the lines in `val` SafeToEvict: count them, keep
+// the short sorted list (while it holds <= 32 lines) and the register prefix
+__device__ __forceinline__ void note_added(unsigned added, int32_t val, int64_t& safe_count,
+                                           bool& list_ok, int32_t& sl, bool reg, RegPrefix& P) {
+    safe_count += __popc(added);
+    if (list_ok && safe_count > 32) list_ok = false;
+    if (!list_ok && !reg) return;
+    while (added) {
+        const int l = __ffs(added) - 1;
+        added &= added - 1;
+        const int32_t v = __shfl_sync(0xffffffffu, val, l);
+        if (list_ok) list_insert(sl, v);
+        if (reg) P.add(v >> 10, 1);
+    }
 }
 
 // rebuild the list from the tables (<= 32 safe lines known to exist)
@@ -294,6 +377,9 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
     int64_t hits = 0, misses = 0, byp = 0, evs = 0, nlog = 0;
     bool list_ok = safe_count <= 32;
     int32_t sl = list_ok ? list_rebuild(t, nw, nb) : NO_LINE;
+    const bool reg = nb <= 128;
+    RegPrefix P;
+    if (reg) reg_prefix_init(P, t, nb);
 
     // the event stream is staged through a shared-memory ring by cp.async,
     // EV_AHEAD chunks ahead, so the sequential loop never waits on HBM
@@ -332,19 +418,8 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                     const int32_t fs = (int32_t)(fe[k] >> 1) - 1;
                     const bool fadd = !(fe[k] & 1u) && !((t.safe[fs >> 5] >> (fs & 31)) & 1u);
                     if (fadd) tab_set_safe_atomic(t, fs);
-                    unsigned added = __ballot_sync(0xffffffffu, fadd);
-                    safe_count += __popc(added);
-                    if (list_ok) {
-                        if (safe_count > 32) {
-                            list_ok = false;
-                        } else {
-                            while (added) {
-                                const int l = __ffs(added) - 1;
-                                added &= added - 1;
-                                list_insert(sl, __shfl_sync(0xffffffffu, fs, l));
-                            }
-                        }
-                    }
+                    note_added(__ballot_sync(0xffffffffu, fadd), fs, safe_count, list_ok, sl, reg,
+                               P);
                     kind[base + k * 32 + lane] = (int8_t)GIDS_KIND_HIT;
                     line[base + k * 32 + lane] = fs;
                     // refill, one commit group per consumed chunk as below
@@ -408,19 +483,8 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                 }
                 const bool mk = mine && (hit ? adds : !my_inuse);
                 if (mk) tab_set_safe_atomic(t, my_line);
-                unsigned added = __ballot_sync(0xffffffffu, mk);
-                safe_count += __popc(added);
-                if (list_ok) {
-                    if (safe_count > 32) {
-                        list_ok = false;
-                    } else {
-                        while (added) {
-                            const int l = __ffs(added) - 1;
-                            added &= added - 1;
-                            list_insert(sl, __shfl_sync(0xffffffffu, my_line, l));
-                        }
-                    }
-                }
+                note_added(__ballot_sync(0xffffffffu, mk), my_line, safe_count, list_ok, sl, reg,
+                           P);
                 hits += __popc(H & span);
                 misses += __popc(fm);
                 fill += __popc(fm);
@@ -443,21 +507,9 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                 }
                 const bool mk = mine && adds;
                 if (mk) tab_set_safe_atomic(t, my_s);
-                unsigned added = __ballot_sync(0xffffffffu, mk);
                 byp += __popc(M & span);
                 hits += __popc(H & span);
-                safe_count += __popc(added);
-                if (list_ok) {
-                    if (safe_count > 32) {
-                        list_ok = false;
-                    } else {
-                        while (added) {
-                            const int l = __ffs(added) - 1;
-                            added &= added - 1;
-                            list_insert(sl, __shfl_sync(0xffffffffu, my_s, l));
-                        }
-                    }
-                }
+                note_added(__ballot_sync(0xffffffffu, mk), my_s, safe_count, list_ok, sl, reg, P);
                 pos = stop;
                 if (safe_count > 0 && pos < cnt && ((M >> pos) & 1u)) {
                     // the evicting miss at lane m = pos
@@ -470,7 +522,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                         if (inuse_m) list_remove(sl, (int)r);
                     } else {
                         __syncwarp();
-                        v = (int32_t)select_safe(t, nw, nb, ns, r);
+                        v = (int32_t)(reg ? select_reg(t, nw, P, r) : select_safe(t, nw, nb, ns, r));
                     }
                     if (lane == 0) {
                         atomicOr(&t.evict[v >> 5], 1u << (v & 31));
@@ -489,6 +541,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                         my_line = v;
                     }
                     if (inuse_m) {
+                        if (reg) P.add(v >> 10, -1);
                         safe_count--;
                         if (!list_ok && safe_count <= 16) {
                             __syncwarp();
