@@ -7,12 +7,15 @@ CPU implementation.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
 LIB_PATH = PKG / "libgids.so"
+if os.environ.get("GIDS_LIB"):  # an alternative build of the same ABI (experiments)
+    LIB_PATH = Path(os.environ["GIDS_LIB"]).resolve()
 ABI_VERSION = 1
 MAX_LAYERS = 8
 

@@ -177,7 +177,9 @@ __device__ __forceinline__ int64_t select_in_words(const ExactTables& t, int64_t
     int f = __ffs(m) - 1;
     uint32_t excl = __shfl_sync(0xffffffffu, inc - c, f);
     uint32_t wsel = __shfl_sync(0xffffffffu, word, f);
-    int bit = __fns(wsel, 0, (int)(r - excl) + 1);
+    // the (r - excl)-th set bit of wsel: lane b holds bit b and its rank
+    const bool at = ((wsel >> lane) & 1u) && __popc(wsel & ((1u << lane) - 1u)) == (int)(r - excl);
+    int bit = __ffs(__ballot_sync(0xffffffffu, at)) - 1;
     return (w0 + f) * 32 + bit;
 }
 
@@ -281,17 +283,23 @@ __device__ __forceinline__ void list_remove(int32_t& sl, int r) {
 
 // `added` lanes just made the lines in `val` SafeToEvict: count them, keep
 // the short sorted list (while it holds <= 32 lines) and the register prefix
+// (a few lines update the prefix in place; more mark it stale, and it is
+// rebuilt from the block counts when an eviction next needs it)
 __device__ __forceinline__ void note_added(unsigned added, int32_t val, int64_t& safe_count,
-                                           bool& list_ok, int32_t& sl, bool reg, RegPrefix& P) {
-    safe_count += __popc(added);
+                                           bool& list_ok, int32_t& sl, bool reg, RegPrefix& P,
+                                           bool& stale) {
+    const int na = __popc(added);
+    safe_count += na;
     if (list_ok && safe_count > 32) list_ok = false;
-    if (!list_ok && !reg) return;
+    const bool upd = reg && !stale && na <= 2;
+    if (reg && !upd && na) stale = true;
+    if (!list_ok && !upd) return;
     while (added) {
         const int l = __ffs(added) - 1;
         added &= added - 1;
         const int32_t v = __shfl_sync(0xffffffffu, val, l);
         if (list_ok) list_insert(sl, v);
-        if (reg) P.add(v >> 10, 1);
+        if (upd) P.add(v >> 10, 1);
     }
 }
 
@@ -339,6 +347,9 @@ __device__ __forceinline__ int32_t list_rebuild(const ExactTables& t, int64_t nw
 //     are BYPASSes; that hit restores one safe line.
 // A lane's hit status only changes when its line is evicted, so the shared
 // tables are read once per chunk.
+// smem_bits: the safe / evicted bitmaps fit in shared memory.  (Specialising
+// the kernel on it -- shared-space loads and aggregated ATOMS -- measured 20%
+// slower on all-hit batches: the generic accesses stay.)
 __global__ void __launch_bounds__(32, 1)
 k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* meta,
             uint32_t* g_safe, uint32_t* g_evict, uint32_t* g_blk, uint32_t* g_sup, int smem_bits,
@@ -379,7 +390,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
     int32_t sl = list_ok ? list_rebuild(t, nw, nb) : NO_LINE;
     const bool reg = nb <= 128;
     RegPrefix P;
-    if (reg) reg_prefix_init(P, t, nb);
+    bool stale = true;  // built on the first eviction that needs it
 
     // the event stream is staged through a shared-memory ring by cp.async,
     // EV_AHEAD chunks ahead, so the sequential loop never waits on HBM
@@ -418,8 +429,23 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                     const int32_t fs = (int32_t)(fe[k] >> 1) - 1;
                     const bool fadd = !(fe[k] & 1u) && !((t.safe[fs >> 5] >> (fs & 31)) & 1u);
                     if (fadd) tab_set_safe_atomic(t, fs);
-                    note_added(__ballot_sync(0xffffffffu, fadd), fs, safe_count, list_ok, sl, reg,
-                               P);
+                    {  // note_added without the in-place prefix update: a run of
+                       // hits adds many lines, so the prefix goes stale instead
+                        unsigned added = __ballot_sync(0xffffffffu, fadd);
+                        safe_count += __popc(added);
+                        if (added) stale = true;
+                        if (list_ok) {
+                            if (safe_count > 32) {
+                                list_ok = false;
+                            } else {
+                                while (added) {
+                                    const int l = __ffs(added) - 1;
+                                    added &= added - 1;
+                                    list_insert(sl, __shfl_sync(0xffffffffu, fs, l));
+                                }
+                            }
+                        }
+                    }
                     kind[base + k * 32 + lane] = (int8_t)GIDS_KIND_HIT;
                     line[base + k * 32 + lane] = fs;
                     // refill, one commit group per consumed chunk as below
@@ -484,7 +510,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                 const bool mk = mine && (hit ? adds : !my_inuse);
                 if (mk) tab_set_safe_atomic(t, my_line);
                 note_added(__ballot_sync(0xffffffffu, mk), my_line, safe_count, list_ok, sl, reg,
-                           P);
+                           P, stale);
                 hits += __popc(H & span);
                 misses += __popc(fm);
                 fill += __popc(fm);
@@ -509,7 +535,8 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                 if (mk) tab_set_safe_atomic(t, my_s);
                 byp += __popc(M & span);
                 hits += __popc(H & span);
-                note_added(__ballot_sync(0xffffffffu, mk), my_s, safe_count, list_ok, sl, reg, P);
+                note_added(__ballot_sync(0xffffffffu, mk), my_s, safe_count, list_ok, sl, reg, P,
+                           stale);
                 pos = stop;
                 if (safe_count > 0 && pos < cnt && ((M >> pos) & 1u)) {
                     // the evicting miss at lane m = pos
@@ -522,6 +549,10 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                         if (inuse_m) list_remove(sl, (int)r);
                     } else {
                         __syncwarp();
+                        if (reg && stale) {
+                            reg_prefix_init(P, t, nb);
+                            stale = false;
+                        }
                         v = (int32_t)(reg ? select_reg(t, nw, P, r) : select_safe(t, nw, nb, ns, r));
                     }
                     if (lane == 0) {
@@ -541,7 +572,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                         my_line = v;
                     }
                     if (inuse_m) {
-                        if (reg) P.add(v >> 10, -1);
+                        if (reg && !stale) P.add(v >> 10, -1);
                         safe_count--;
                         if (!list_ok && safe_count <= 16) {
                             __syncwarp();
@@ -839,6 +870,18 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
 
 }  // namespace
 
+static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t st) {
+    auto k = k_exact_seq;
+    if (smem > 48 * 1024)
+        GIDS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+    k<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits, h->evict_bits, h->blk_cnt,
+                           h->sup_cnt, h->exact_smem ? 1 : 0, h->kind, h->line, h->log_line,
+                           h->log_pos, h->svc);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
+}
+
 int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delta,
                        cudaStream_t st) {
     if (n == 0) return GIDS_OK;
@@ -886,15 +929,8 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         GIDS_LAUNCH_CHECK(h);
         if (exact) {
             size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
-            if (smem > 48 * 1024)
-                GIDS_CUDA_TRY(cudaFuncSetAttribute(k_exact_seq,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)smem));
-            k_exact_seq<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits,
-                                             h->evict_bits, h->blk_cnt, h->sup_cnt,
-                                             h->exact_smem ? 1 : 0, h->kind, h->line,
-                                             h->log_line, h->log_pos, h->svc);
-            GIDS_LAUNCH_CHECK(h);
+            int rc = launch_exact_seq(h, n, smem, st);
+            if (rc) return rc;
             k_post_a<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
                                           h->slot_of, h->last_ins, h->evict_bits,
                                           h->exact_smem ? 0 : 1);
@@ -1020,13 +1056,10 @@ extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n
                                           2, nullptr);
     GIDS_LAUNCH_CHECK(h);
     size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
-    if (smem > 48 * 1024)
-        GIDS_CUDA_TRY(cudaFuncSetAttribute(k_exact_seq, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-    k_exact_seq<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits, h->evict_bits,
-                                     h->blk_cnt, h->sup_cnt, h->exact_smem ? 1 : 0, h->kind,
-                                     h->line, h->log_line, h->log_pos, h->svc);
-    GIDS_LAUNCH_CHECK(h);
+    {
+        int rc = launch_exact_seq(h, n, smem, st);
+        if (rc) return rc;
+    }
     k_post_a<<<g, BLOCK, 0, st>>>(nodes, h->svc, h->log_line, h->log_pos, h->line_node,
                                   h->slot_of, h->last_ins, h->evict_bits, h->exact_smem ? 0 : 1,
                                   victim_out);
