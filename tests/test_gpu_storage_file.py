@@ -94,3 +94,23 @@ def test_gpu_file_tier_from_graph_and_feature_files(tmp_path):
         assert s1.csv_row() == s2.csv_row()
     dl.close()
     ref.close()
+
+
+def test_gpu_file_tier_direct_io_matches_pinned_tier(tmp_path):
+    """4 KiB pages with O_DIRECT (when the filesystem allows it): the same
+    rows and tier counts as the pinned-host tier."""
+    base = dict(num_nodes=20_000, avg_degree=10.0, degree_model="uniform", feature_dim=256,
+                fanouts=[8, 8], batch_size=256, cache_lines=1_000, buffer_fraction=0.05,
+                window_depth=4, consume_rate=0.0, seed=13, page_bytes=4096)
+    ref = Dataloader(make_config(base))
+    dl = Dataloader(make_config({**base, "gids_storage": "file", "gids_io_direct": True,
+                                 "gids_storage_path": str(tmp_path / "d.gfea")}))
+    for b in range(8):
+        _, r1, s1 = ref.next_batch()
+        _, r2, s2 = dl.next_batch()
+        assert np.array_equal(r1.cpu().numpy(), r2.cpu().numpy()), b
+        assert s1.csv_row() == s2.csv_row(), b
+    st = dl.storage_stats()
+    assert st["pages"] > 0 and st["bytes"] == st["pages"] * 4096
+    dl.close()
+    ref.close()
