@@ -8,7 +8,6 @@ single process with virtual shards, and two processes on one device whose
 shards are opened from real CUDA IPC handles."""
 from __future__ import annotations
 
-import os
 import socket
 
 import numpy as np
