@@ -353,6 +353,7 @@ def main() -> None:
     # the GPU cache must be warm before timing (the paper warms 10 iterations,
     # PAPER.md:621): the first batches fill and churn the
     # exact policy's cache one eviction at a time (~100 ms per batch at C2)
+    args.warmup_requested = args.warmup
     args.warmup = max(args.warmup, 3 if args.impl == "reference" else 10)
     args.policy = args.policy or DEFAULT_POLICY[args.workload]
     cfg_dict = {**WORKLOADS[args.workload], "gids_policy": args.policy}
@@ -531,7 +532,8 @@ def main() -> None:
                     "rows_remote_per_step": float(shard_rows[1]) / args.steps}
     line = {
         "metric": METRIC, "value": value, "unit": "minibatches/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms,
+        "steps": args.steps, "warmup": args.warmup, "warmup_requested": args.warmup_requested,
+        "ms_per_step": dev_ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic (reference generate_synthetic graph + synthetic_feature_rows table)",
         "config": {"workload": WORKLOAD_NAMES[args.workload], "policy": args.policy,
