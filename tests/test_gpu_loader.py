@@ -121,6 +121,37 @@ def test_gpu_c2_shape_properties():
         assert st.cache_hits + st.cpu_buffer_hits + st.ssd_accesses == st.sampled_nodes
         assert rows.shape == (u.numel(), 1024)
     assert dl.cache.evictions > 0 or dl.cache.bypasses > 0
+    dl.close()
+
+
+def test_gpu_c2_fullsize_matches_oracle():
+    """The default bench workload (BASELINE configs[1], exact policy) at full size,
+    bit for bit against the oracle for 12 batches: unique nodes, every layer,
+    tier counts, the CSV-relevant inflight, gathered rows, and the cache's
+    line table and eviction RNG at the end."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    cfg = make_config(bench.WORKLOADS["c2"])
+    dl = Dataloader(cfg)
+    r = bench.oracle_inputs(cfg, dl.graph, dl.features.table, dl.buffer.node_ids)
+    ld = bench.oracle_loader(cfg, r, buffer_rows=dl.buffer.rows)
+    ld.keep_rows = True
+    for b in range(12):
+        o = ld.next_batch()
+        mb, rows, st = dl.next_batch()
+        assert np.array_equal(mb.unique_nodes.cpu().numpy(), o["unique"]), b
+        for l, ol in zip(mb.layers, o["layers"]):
+            assert np.array_equal(l.cpu().numpy(), ol), b
+        assert [st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses] == \
+            o["tiers"].tolist(), b
+        assert np.array_equal(rows.cpu().numpy(), o["rows"]), b
+    node, state = dl.cache.lines()
+    onode, ostate = ld.cache.lines_snapshot()
+    assert np.array_equal(node, onode) and np.array_equal(state, ostate)
+    assert dl.cache.eviction_rng_words().tolist() == ld.cache.rng_words().tolist()
+    dl.close()
 
 
 def test_gpu_device_generator_loader_matches_oracle():
