@@ -299,6 +299,10 @@ class Dataloader:
         self._train_us_total = Fraction(0)
         self._row_frac = Fraction(row_bytes)
         self._cpu_bytes_per_s = exact(cfg.cpu_gbps) * 10**9
+        self._cpu_us_per_row = self._row_frac * 1_000_000 / self._cpu_bytes_per_s
+        self._row_us_bytes = self._row_frac * 1_000_000
+        self._train_us_per_node = (Fraction(1_000_000) / exact(cfg.consume_rate)
+                                   if cfg.consume_rate > 0 else 0)
         self.last_counts = None
 
     def _out_block(self):
@@ -517,22 +521,28 @@ class Dataloader:
             raise AssertionError("gathered rows diverge from the feature table")
 
     def _account(self, sampled, hits, buf_hits, ssd, bypasses, inflight) -> IterationStats:
-        ssd_us = Fraction(0)
+        # exact rationals as the reference (dataloader.py:301-337); the per-row
+        # and per-node constants are folded once (rational arithmetic is exact,
+        # so the values are unchanged) and zero terms skip the Fraction work
+        fetch_us = 0
         if ssd > 0:
             joint = max(inflight, ssd)
-            ssd_us = fetch_total_us(self.spec, joint) * Fraction(ssd, joint)
-        cpu_us = Fraction(buf_hits) * self._row_frac * 1_000_000 / self._cpu_bytes_per_s
-        fetch_us = ssd_us + cpu_us
-        train_us = (Fraction(sampled) * 1_000_000 / exact(self.cfg.consume_rate)
-                    if self.cfg.consume_rate > 0 else Fraction(0))
-        self._clock_us += max(fetch_us, train_us)
-        self._fetch_us_total += fetch_us
-        self._train_us_total += train_us
+            fetch_us = fetch_total_us(self.spec, joint) * Fraction(ssd, joint)
+        if buf_hits:
+            fetch_us = fetch_us + buf_hits * self._cpu_us_per_row
+        train_us = sampled * self._train_us_per_node if self._train_us_per_node else 0
+        step = fetch_us if fetch_us >= train_us else train_us
+        if step:
+            self._clock_us += step
+        if fetch_us:
+            self._fetch_us_total += fetch_us
+        if train_us:
+            self._train_us_total += train_us
         redirect = (hits + buf_hits) / sampled if sampled else 0.0
         a = self.cfg.redirect_ema_alpha
         self.redirect_ema = a * redirect + (1.0 - a) * self.redirect_ema
         if fetch_us > 0:
-            bw = float(Fraction(sampled) * self._row_frac * 1_000_000 / fetch_us)
+            bw = float(sampled * self._row_us_bytes / fetch_us)
         else:
             bw = float("inf") if sampled else 0.0
         return IterationStats(iteration=self._iteration, sampled_nodes=sampled, cache_hits=hits,
