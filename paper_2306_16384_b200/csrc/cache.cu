@@ -88,8 +88,8 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                                  const int32_t* __restrict__ slot_of, uint32_t* safe_bits,
                                  uint32_t* blk_cnt, uint32_t* sup_cnt, int exact,
                                  CacheMeta* meta, uint32_t* ev, int mode = 3,
-                                 int32_t* counts = nullptr) {
-    int64_t inc = 0, dec = 0, unsafe = 0;
+                                 int32_t* counts = nullptr, int64_t* nmiss0 = nullptr) {
+    int64_t inc = 0, dec = 0, unsafe = 0, miss0 = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = (int32_t)uniq[p];
@@ -118,10 +118,16 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
         }
         reuse[x] = now;
         if (mode & 2) ev[p] = ((uint32_t)(s + 1) << 1) | (now > 0 ? 1u : 0u);
+        miss0 += s < 0;
     }
     inc = warp_sum64(inc);
     dec = warp_sum64(dec);
     unsafe = warp_sum64(unsafe);
+    if (nmiss0) {
+        miss0 = warp_sum64(miss0);
+        if ((threadIdx.x & 31) == 0 && miss0)
+            atomicAdd((unsigned long long*)nmiss0, (unsigned long long)miss0);
+    }
     if ((threadIdx.x & 31) == 0) {
         if (inc) atomicAdd((unsigned long long*)&meta->inc, (unsigned long long)inc);
         if (dec) atomicAdd((unsigned long long*)&meta->dec, (unsigned long long)dec);
@@ -347,6 +353,38 @@ __device__ __forceinline__ int32_t list_rebuild(const ExactTables& t, int64_t nw
 //     are BYPASSes; that hit restores one safe line.
 // A lane's hit status only changes when its line is evicted, so the shared
 // tables are read once per chunk.
+// A batch whose nodes are all resident when its decisions start has no miss,
+// hence no fill, eviction or bypass: every access hits its line and the only
+// state change is InUse->Safe for the lines whose reuse count reached zero --
+// independent per line.  Decided by the whole GPU instead of the sequential
+// warp (k_exact_seq then returns at once); a no-op when n_miss0 > 0.
+__global__ void k_exact_allhit(const uint32_t* __restrict__ ev, int64_t n, CacheMeta* meta,
+                               uint32_t* safe_bits, uint32_t* blk, uint32_t* sup,
+                               const ServeCounters* __restrict__ svc, int8_t* __restrict__ kind,
+                               int32_t* __restrict__ line) {
+    if (svc->n_miss0 != 0) return;
+    int64_t adds = 0;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t e = ev[p];
+        const int32_t s = (int32_t)(e >> 1) - 1;
+        kind[p] = (int8_t)GIDS_KIND_HIT;
+        line[p] = s;
+        const uint32_t bit = 1u << (s & 31);
+        if (!(e & 1u) && !(safe_bits[s >> 5] & bit)) {
+            atomicOr(&safe_bits[s >> 5], bit);
+            atomicAdd(&blk[s >> 10], 1u);
+            atomicAdd(&sup[s >> 15], 1u);
+            adds++;
+        }
+    }
+    adds = warp_sum64(adds);
+    if ((threadIdx.x & 31) == 0 && adds)
+        atomicAdd((unsigned long long*)&meta->safe_count, (unsigned long long)adds);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd((unsigned long long*)&meta->hits, (unsigned long long)n);
+}
+
 // smem_bits: the safe / evicted bitmaps fit in shared memory.  (Specialising
 // the kernel on it -- shared-space loads and aggregated ATOMS -- measured 20%
 // slower on all-hit batches: the generic accesses stay.)
@@ -356,6 +394,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
             int8_t* __restrict__ kind, int32_t* __restrict__ line, int32_t* __restrict__ log_line,
             int32_t* __restrict__ log_pos, ServeCounters* svc) {
     extern __shared__ uint32_t sm[];
+    if (svc->n_miss0 == 0) return;  // all hits: decided by k_exact_allhit
     const int lane = threadIdx.x;
     const unsigned below = (1u << lane) - 1u;
     const int64_t nw = (L + 31) / 32, nb = (L + 1023) / 1024, ns = (L + 32767) / 32768;
@@ -871,6 +910,9 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
 }  // namespace
 
 static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t st) {
+    k_exact_allhit<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
+        h->ev, n, h->meta, h->safe_bits, h->blk_cnt, h->sup_cnt, h->svc, h->kind, h->line);
+    GIDS_LAUNCH_CHECK(h);
     auto k = k_exact_seq;
     if (smem > 48 * 1024)
         GIDS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -925,7 +967,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
         k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
                                               h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
-                                              h->meta, h->ev);
+                                              h->meta, h->ev, 3, nullptr, &h->svc->n_miss0);
         GIDS_LAUNCH_CHECK(h);
         if (exact) {
             size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
@@ -1053,7 +1095,7 @@ extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n
     const int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
     k_window_consume<<<g, BLOCK, 0, st>>>(nodes, n, h->future, h->reuse, h->slot_of,
                                           h->safe_bits, h->blk_cnt, h->sup_cnt, 1, h->meta, h->ev,
-                                          2, nullptr);
+                                          2, nullptr, &h->svc->n_miss0);
     GIDS_LAUNCH_CHECK(h);
     size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
     {

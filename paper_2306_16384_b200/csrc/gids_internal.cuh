@@ -138,6 +138,7 @@ struct SampleCounters {
 struct ServeCounters {
     int64_t tiers[4];      // hits, buffer, storage, bypasses (this batch)
     int64_t n_log;         // insertions logged by the exact policy this batch
+    int64_t n_miss0;       // nodes not resident when the batch's decisions start
     int64_t shard_local, shard_remote;  // sharded-table mode: rows from own / peer HBM
 };
 
