@@ -263,6 +263,11 @@ GIDS_API int gids_set_storage_file(gids_handle* h, const char* path, int64_t off
 GIDS_API int gids_storage_file_stats(gids_handle* h, int64_t* pages, int64_t* bytes, int64_t* runs,
                                      double* io_ms, int32_t* direct);
 
+/* Page-lock (and map for zero-copy reads) host memory the caller allocated,
+ * e.g. a 2 MiB-page (THP) region for a multi-GB storage tier. */
+GIDS_API int gids_host_register(void* ptr, int64_t bytes);
+GIDS_API int gids_host_unregister(void* ptr);
+
 /* Per-phase device time (CUDA events on the launching stream), accumulated
  * while profiling is on: out_ms[0] sampling, [1] window + cache policy,
  * [2] hit gather (HBM), [3] host-tier gather (zero-copy), [4] batches

@@ -93,6 +93,8 @@ def lib() -> C.CDLL:
                                    vp, vp], C.c_int),
         "gids_load_graph_device": ([vp, vp, vp], C.c_int),
         "gids_contribution_async": ([vp, vp, vp, vp, vp], C.c_int),
+        "gids_host_register": ([vp, i64], C.c_int),
+        "gids_host_unregister": ([vp], C.c_int),
         "gids_cache_window_update": ([vp, vp, i64, vp, vp], C.c_int),
         "gids_cache_access": ([vp, vp, i64, vp, vp, vp, vp], C.c_int),
         "gids_cache_reuse": ([vp, vp], C.c_int),
@@ -135,7 +137,7 @@ def exported_symbols() -> list[str]:
             "gids_ipc_open", "gids_ipc_close", "gids_set_sharded_table", "gids_shard_counts",
             "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats",
             "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse",
-            "gids_contribution_async"]
+            "gids_contribution_async", "gids_host_register", "gids_host_unregister"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -151,7 +153,9 @@ def check(rc: int, what: str = "") -> None:
 
 
 def _p(a) -> int:
-    """Raw address of a numpy array or a torch tensor."""
+    """Raw address of a numpy array, a torch tensor, or an address already."""
+    if isinstance(a, int):
+        return a
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return a.data_ptr()
@@ -428,3 +432,39 @@ def synthesize_rows_strided(device: int, seed: int, row0: int, stride: int, n: i
     check(lib().gids_synthesize_rows_strided(device, seed & ((1 << 64) - 1), row0, stride, n,
                                              dim, dst if isinstance(dst, int) else _p(dst),
                                              stream), "synthesize_rows_strided")
+
+
+class HugePageHost:
+    """Host memory on transparent 2 MiB pages, page-locked and mapped for
+    zero-copy reads (gids_host_register).  ``array(shape, dtype)`` views it."""
+
+    def __init__(self, nbytes: int):
+        import mmap
+        align = 2 << 20
+        self._map = mmap.mmap(-1, nbytes + align)
+        base = np.frombuffer(self._map, dtype=np.uint8)
+        addr = base.ctypes.data
+        self._off = (-addr) % align
+        self.nbytes = nbytes
+        try:
+            self._map.madvise(mmap.MADV_HUGEPAGE, self._off, nbytes - nbytes % align or nbytes)
+        except (AttributeError, OSError, ValueError):
+            pass  # THP unavailable: still correct, just 4 KiB pages
+        self._view = base[self._off:self._off + nbytes]
+        self._view[::4096] = 0  # fault the pages in (huge where the kernel allows)
+        self.ptr = self._view.ctypes.data
+        check(lib().gids_host_register(C.c_void_p(self.ptr), nbytes), "host_register")
+
+    def array(self, shape, dtype) -> np.ndarray:
+        return self._view.view(dtype).reshape(shape)
+
+    def close(self) -> None:
+        if getattr(self, "ptr", None):
+            lib().gids_host_unregister(C.c_void_p(self.ptr))
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -608,6 +608,20 @@ int gids_phase_times(gids_handle* h, double out_ms[5]) {
     return GIDS_OK;
 }
 
+int gids_host_register(void* ptr, int64_t bytes) {
+    if (!ptr || bytes <= 0) {
+        gids_set_error("host_register: bad arguments");
+        return GIDS_E_INVALID;
+    }
+    GIDS_CUDA_TRY(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterMapped));
+    return GIDS_OK;
+}
+
+int gids_host_unregister(void* ptr) {
+    GIDS_CUDA_TRY(cudaHostUnregister(ptr));
+    return GIDS_OK;
+}
+
 int64_t gids_cache_capacity(gids_handle* h) { return h ? h->L : -1; }
 int64_t gids_launch_count(gids_handle* h) { return h ? h->launches : -1; }
 

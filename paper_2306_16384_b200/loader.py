@@ -244,8 +244,9 @@ class Dataloader:
             self._h.set_storage_file(self._storage_file, HEADER_BYTES, self.spec.page_bytes,
                                      io_threads=cfg.gids_io_threads, direct=cfg.gids_io_direct)
         else:
-            self._h.set_backing(self.features.pinned if self.features.pinned is not None
-                                else self.features.table, self.graph.num_nodes)
+            pinned = self.features.pinned
+            self._h.set_backing(pinned if isinstance(pinned, torch.Tensor) else self.features.table,
+                                self.graph.num_nodes)
         if self.buffer.pinned is not None:
             self._h.set_constant_buffer(self.buffer.device_ids, self.buffer.pinned)
         else:
