@@ -11,6 +11,8 @@ timeout 300 python -c 'import __graft_entry__ as g; g.smoke()' 2>&1 | tail -2
 timeout 600 python bench.py > gpurun_out/bench_c2.json 2>&1; tail -c 600 gpurun_out/bench_c2.json
 [ "$1" = quick ] && exit 0
 timeout 1500 python bench.py --workload c4 --steps 30 --warmup 10 > gpurun_out/bench_c4.json 2>&1
+timeout 600 python bench.py --workload c1 --steps 100 --warmup 40 > gpurun_out/bench_c1.json 2>&1
+timeout 1500 python bench.py --workload c3 --steps 30 --warmup 10 > gpurun_out/bench_c3.json 2>&1
 timeout 900 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref_c2.json 2>&1
 export BENCH_PROFILE_STEADY=1
 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
