@@ -63,6 +63,80 @@ int map_host(const void* p, size_t bytes, bool* registered) {
 
 }  // namespace
 
+// everything after the device allocations: pinned mirrors, initial state,
+// events, launch geometry (gids_create destroys the handle if this fails)
+static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
+    const int64_t N = h->N, L = h->L;
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->sc_host, sizeof(SampleCounters)));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->svc_host, sizeof(ServeCounters)));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->jump_host, sizeof(u128) * GIDS_JUMP_TAB));
+    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->rng_host, sizeof(u128) * 2));
+    GIDS_CUDA_TRY(cudaMemset(h->pinned_off, 0xff, sizeof(int32_t) * N));
+    GIDS_CUDA_TRY(cudaMemset(h->slot_of, 0xff, sizeof(int32_t) * N));
+    GIDS_CUDA_TRY(cudaMemset(h->line_node, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
+    GIDS_CUDA_TRY(cudaMemset(h->last_ins, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
+    GIDS_CUDA_TRY(cudaMemset(h->safe_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->evict_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->blk_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 1024)));
+    GIDS_CUDA_TRY(cudaMemset(h->sup_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32768)));
+    GIDS_CUDA_TRY(cudaMemset(h->reuse, 0, sizeof(uint32_t) * N));
+    GIDS_CUDA_TRY(cudaMemset(h->future, 0, N));
+    GIDS_CUDA_TRY(cudaMemset(h->bm_front, 0, sizeof(uint32_t) * ceil_div(N, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->bm_all, 0, sizeof(uint32_t) * ceil_div(N, 32)));
+    CacheMeta m;
+    memset(&m, 0, sizeof(m));
+    if (eviction_rng)
+        for (int i = 0; i < 6; i++) m.rng[i] = eviction_rng[i];
+    GIDS_CUDA_TRY(cudaMemcpy(h->meta, &m, sizeof(m), cudaMemcpyHostToDevice));
+
+    // exact policy: keep the safe/evicted bitmaps in shared memory when they fit
+    int dev_smem = 0;
+    GIDS_CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                         h->device));
+    size_t with_bits = gids_exact_smem_bytes(L, true), without = gids_exact_smem_bytes(L, false);
+    const size_t static_smem = 4096;  // k_exact_seq's event ring
+    h->exact_smem = with_bits + static_smem <= (size_t)dev_smem;
+    if (!h->exact_smem && without + static_smem > (size_t)dev_smem) {
+        gids_set_error("cache_lines too large for the exact policy (use the set-associative one)");
+        gids_destroy(h);
+        return GIDS_E_INVALID;
+    }
+    for (int i = 0; i < 8; i++) GIDS_CUDA_TRY(cudaEventCreate(&h->tev[i]));
+    for (int i = 0; i < gids_handle::SRING; i++)
+        for (int j = 0; j < 2; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->sev[i][j]));
+    // gather residency in warps per SM (GIDS_GATHER_WPS).  2 keeps ~0.6 MB of
+    // 16-B loads in flight -- several times the host link's bandwidth-delay
+    // product -- and leaves the SMs to sampling and decisions: measured on
+    // B200 (profiles/r01_bench_wps_b7_*.json) 1/2/4 warps per SM give the same
+    // link rate, while 4 slows the overlapped exact-policy decisions by 30%
+    {
+        int wps = 2;  // with gather_unroll 2: ~300 KB of loads in flight (profiles/r01_gather_wps_unroll_sweep_c2.txt)
+        if (const char* e = getenv("GIDS_GATHER_WPS")) wps = atoi(e);
+        if (wps < 1) wps = 1;
+        int blocks = (wps * GIDS_SMS + 7) / 8;
+        h->gather_blocks = blocks;
+        h->gather_unroll = 2;
+        const char* ng = getenv("GIDS_NO_GRAPHS");
+        h->use_graphs = !(ng && ng[0] == '1');
+        if (const char* e = getenv("GIDS_GATHER_UNROLL")) {
+            int u = atoi(e);
+            h->gather_unroll = u >= 8 ? 8 : u >= 4 ? 4 : u >= 2 ? 2 : 1;
+        }
+    }
+    for (int i = 0; i < 2; i++) {
+        GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->gathered[i], cudaEventDisableTiming));
+        for (int j = 0; j < 3; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->gev[i][j]));
+    }
+    GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->decided, cudaEventDisableTiming));
+    h->kind = h->kind_buf[0];
+    h->line = h->line_buf[0];
+    h->ins = h->ins_buf[0];
+    h->hit_list = h->hit_list_buf[0];
+    h->host_list = h->host_list_buf[0];
+    h->list_cnt = h->list_cnt_buf[0];
+    return GIDS_OK;
+}
+
 extern "C" {
 
 int gids_abi_version(void) { return GIDS_ABI_VERSION; }
@@ -178,73 +252,11 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         gids_destroy(h);
         return rc;
     }
-    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->sc_host, sizeof(SampleCounters)));
-    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->svc_host, sizeof(ServeCounters)));
-    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->jump_host, sizeof(u128) * GIDS_JUMP_TAB));
-    GIDS_CUDA_TRY(cudaMallocHost((void**)&h->rng_host, sizeof(u128) * 2));
-    GIDS_CUDA_TRY(cudaMemset(h->pinned_off, 0xff, sizeof(int32_t) * N));
-    GIDS_CUDA_TRY(cudaMemset(h->slot_of, 0xff, sizeof(int32_t) * N));
-    GIDS_CUDA_TRY(cudaMemset(h->line_node, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
-    GIDS_CUDA_TRY(cudaMemset(h->last_ins, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
-    GIDS_CUDA_TRY(cudaMemset(h->safe_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
-    GIDS_CUDA_TRY(cudaMemset(h->evict_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
-    GIDS_CUDA_TRY(cudaMemset(h->blk_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 1024)));
-    GIDS_CUDA_TRY(cudaMemset(h->sup_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32768)));
-    GIDS_CUDA_TRY(cudaMemset(h->reuse, 0, sizeof(uint32_t) * N));
-    GIDS_CUDA_TRY(cudaMemset(h->future, 0, N));
-    GIDS_CUDA_TRY(cudaMemset(h->bm_front, 0, sizeof(uint32_t) * ceil_div(N, 32)));
-    GIDS_CUDA_TRY(cudaMemset(h->bm_all, 0, sizeof(uint32_t) * ceil_div(N, 32)));
-    CacheMeta m;
-    memset(&m, 0, sizeof(m));
-    if (eviction_rng)
-        for (int i = 0; i < 6; i++) m.rng[i] = eviction_rng[i];
-    GIDS_CUDA_TRY(cudaMemcpy(h->meta, &m, sizeof(m), cudaMemcpyHostToDevice));
-
-    // exact policy: keep the safe/evicted bitmaps in shared memory when they fit
-    int dev_smem = 0;
-    GIDS_CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin,
-                                         h->device));
-    size_t with_bits = gids_exact_smem_bytes(L, true), without = gids_exact_smem_bytes(L, false);
-    const size_t static_smem = 4096;  // k_exact_seq's event ring
-    h->exact_smem = with_bits + static_smem <= (size_t)dev_smem;
-    if (!h->exact_smem && without + static_smem > (size_t)dev_smem) {
-        gids_set_error("cache_lines too large for the exact policy (use the set-associative one)");
+    rc = init_handle(h, eviction_rng);
+    if (rc) {  // no partially built handle escapes
         gids_destroy(h);
-        return GIDS_E_INVALID;
+        return rc;
     }
-    for (int i = 0; i < 8; i++) GIDS_CUDA_TRY(cudaEventCreate(&h->tev[i]));
-    for (int i = 0; i < gids_handle::SRING; i++)
-        for (int j = 0; j < 2; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->sev[i][j]));
-    // gather residency in warps per SM (GIDS_GATHER_WPS).  2 keeps ~0.6 MB of
-    // 16-B loads in flight -- several times the host link's bandwidth-delay
-    // product -- and leaves the SMs to sampling and decisions: measured on
-    // B200 (profiles/r01_bench_wps_b7_*.json) 1/2/4 warps per SM give the same
-    // link rate, while 4 slows the overlapped exact-policy decisions by 30%
-    {
-        int wps = 2;  // with gather_unroll 2: ~300 KB of loads in flight (profiles/r01_gather_wps_unroll_sweep_c2.txt)
-        if (const char* e = getenv("GIDS_GATHER_WPS")) wps = atoi(e);
-        if (wps < 1) wps = 1;
-        int blocks = (wps * GIDS_SMS + 7) / 8;
-        h->gather_blocks = blocks;
-        h->gather_unroll = 2;
-        const char* ng = getenv("GIDS_NO_GRAPHS");
-        h->use_graphs = !(ng && ng[0] == '1');
-        if (const char* e = getenv("GIDS_GATHER_UNROLL")) {
-            int u = atoi(e);
-            h->gather_unroll = u >= 8 ? 8 : u >= 4 ? 4 : u >= 2 ? 2 : 1;
-        }
-    }
-    for (int i = 0; i < 2; i++) {
-        GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->gathered[i], cudaEventDisableTiming));
-        for (int j = 0; j < 3; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->gev[i][j]));
-    }
-    GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->decided, cudaEventDisableTiming));
-    h->kind = h->kind_buf[0];
-    h->line = h->line_buf[0];
-    h->ins = h->ins_buf[0];
-    h->hit_list = h->hit_list_buf[0];
-    h->host_list = h->host_list_buf[0];
-    h->list_cnt = h->list_cnt_buf[0];
     *out = h;
     return GIDS_OK;
 }
