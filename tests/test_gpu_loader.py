@@ -220,3 +220,38 @@ def test_gpu_data_parallel_replicas_match_oracle(policy):
                 o["tiers"].tolist(), (rank, b)
             assert np.array_equal(rows.cpu().numpy(), o["rows"]), (rank, b)
         dl.close()
+
+
+@pytest.mark.parametrize("lines,nodes,batch", [(200_000, 1_000_000, 2048),
+                                               (1_000_000, 3_000_000, 4096)],
+                         ids=["no-register-prefix", "global-tables"])
+def test_gpu_exact_policy_large_caches_match_oracle(lines, nodes, batch):
+    """The exact policy beyond its fast structures: more than 131072 lines (no
+    register prefix: three-level table select) and more than fit shared memory
+    (bitmaps in global memory).  Bit-exact vs the oracle once evictions run."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    cfg = make_config(dict(num_nodes=nodes, avg_degree=8.0, degree_model="uniform",
+                           feature_dim=16, fanouts=[10, 10], batch_size=batch,
+                           cache_lines=lines, buffer_fraction=0.02, window_depth=2,
+                           consume_rate=0.0, seed=21, gids_generator="device"))
+    dl = Dataloader(cfg)
+    g, buf = bench.host_device_shape(cfg)
+    r = bench.oracle_inputs(cfg, g, dl.features.table, buf)
+    ld = O.OracleLoader(g.indptr, g.indices, dl.features.table, buf, r["batches"], cfg.fanouts,
+                        r["sampler_words"], r["evict_words"], cfg.resolved_cache_lines(),
+                        cfg.window_depth, r["base_threshold"])
+    for b in range(10):
+        o = ld.next_batch()
+        mb, rows, st = dl.next_batch()
+        assert [st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses] == \
+            o["tiers"].tolist(), b
+        assert np.array_equal(rows.cpu().numpy(), o["rows"]), b
+    assert dl.cache.evictions > 0
+    node, state = dl.cache.lines()
+    onode, ostate = ld.cache.lines_snapshot()
+    assert np.array_equal(node, onode) and np.array_equal(state, ostate)
+    assert dl.cache.eviction_rng_words().tolist() == ld.cache.rng_words().tolist()
+    dl.close()
