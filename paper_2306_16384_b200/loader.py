@@ -160,72 +160,15 @@ class Dataloader:
 
         graph_ss, feat_ss, sampler_ss, shuffle_ss, evict_ss, work_ss = \
             np.random.SeedSequence(cfg.seed).spawn(6)
-        graph_seed = int(graph_ss.generate_state(1)[0])
         self.sharded = None
         self._storage_file = None
-        if cfg.graph_path is not None:
-            self.graph = load_graph(cfg.graph_path)
-            host = load_features(cfg.features_path, mmap=True)
-            if host.num_nodes != self.graph.num_nodes:
-                raise ConfigError("feature table and graph disagree on node count")
-            self._storage_file = str(cfg.features_path) if cfg.gids_storage == "file" else None
-            # file tier: the rows stay in the file (memory-mapped for the host API)
-            self.features = host if self._storage_file else self._pin_table(host)
-            dev_graph = self._upload_graph(self.graph)
-        else:
-            if cfg.gids_generator == "device":
-                # counter-based uniform generator in HBM (csrc/graph_setup.cu)
-                n, e = cfg.num_nodes, int(round(cfg.num_nodes * cfg.avg_degree))
-                dev_graph = _native.generate_uniform_graph(self.device, n, e, graph_seed)
-                self.graph = GraphCsc(num_nodes=n, num_edges=e,
-                                      indptr=dev_graph[0].cpu().numpy().view(np.uint64),
-                                      indices=dev_graph[1].cpu().numpy().astype(np.uint64))
-            else:
-                self.graph = generate_synthetic(cfg.num_nodes, cfg.avg_degree, cfg.degree_model,
-                                                seed=graph_seed, exponent=cfg.degree_exponent)
-                dev_graph = self._upload_graph(self.graph)
-            feat_seed = int(feat_ss.generate_state(1)[0])
-            if cfg.gids_sharded_table:
-                # C5: the table lives in the ranks' HBM (sharded_table.py)
-                virtual = cfg.gids_virtual_shards > 0
-                g = cfg.gids_virtual_shards if virtual else cfg.gids_dp_world
-                self.sharded = ShardedTable(cfg.num_nodes, cfg.feature_dim, feat_seed,
-                                            self.device, 0 if virtual else cfg.gids_dp_rank, g,
-                                            virtual=virtual)
-                self.features = FeatureStore(num_nodes=cfg.num_nodes, dim=cfg.feature_dim,
-                                             table=None, seed=feat_seed)
-            elif cfg.gids_storage == "file":
-                # the synthetic table written once to a .gfea file, then served
-                # from the file (csrc/storage_file.cu)
-                write_synthetic_features(cfg.gids_storage_path, cfg.num_nodes, cfg.feature_dim,
-                                         feat_seed, self.device)
-                host = load_features(cfg.gids_storage_path, mmap=True)
-                self.features = FeatureStore(num_nodes=host.num_nodes, dim=host.dim,
-                                             table=host.table, seed=feat_seed)
-                self._storage_file = str(cfg.gids_storage_path)
-            else:
-                self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim, feat_seed,
-                                                     self.device)
+        dev_graph = self._build_graph_and_features(int(graph_ss.generate_state(1)[0]),
+                                                   int(feat_ss.generate_state(1)[0]))
         row_bytes = self.features.row_bytes
         if row_bytes > self.spec.page_bytes:
             raise InfeasibleError(f"feature row ({row_bytes} B) exceeds one cache line / page "
                                   f"({self.spec.page_bytes} B)")
-
-        budget = cfg.resolved_buffer_bytes(self.graph.num_nodes, row_bytes)
-        if budget // row_bytes > 0:
-            # reverse PageRank + top-k on the GPU, float64-identical to
-            # cpu_buffer.py:26-109 (so the pinned set is the reference's)
-            self.pagerank, dev_scores = reverse_pagerank_device(self.device, *dev_graph)
-            chosen = top_k_nodes_device(dev_scores, budget // row_bytes)
-            del dev_scores
-            self.buffer = build_constant_buffer(self.pagerank.scores, self.features, budget,
-                                                pinned=chosen, pin_memory=True)
-        else:
-            self.pagerank = None
-            self.buffer = build_constant_buffer(np.empty(0), self.features, 0,
-                                                pinned=np.empty(0, dtype=np.int64))
-        self._pinned_mask = np.zeros(self.graph.num_nodes, dtype=bool)
-        self._pinned_mask[self.buffer.node_ids] = True
+        self._build_constant_buffer(dev_graph, row_bytes)
 
         evict_seed = int(evict_ss.generate_state(1)[0])
         self._h = _native.Handle(
@@ -305,6 +248,71 @@ class Dataloader:
         self._train_us_per_node = (Fraction(1_000_000) / exact(cfg.consume_rate)
                                    if cfg.consume_rate > 0 else 0)
         self.last_counts = None
+
+    def _build_graph_and_features(self, graph_seed: int, feat_seed: int):
+        """Graph (dataloader.py:105-117) and the storage tier: files, the
+        reference's generator or the GPU generator; pinned host rows, the
+        .gfea file itself, or HBM shards.  Returns the graph in HBM."""
+        cfg = self.cfg
+        if cfg.graph_path is not None:
+            self.graph = load_graph(cfg.graph_path)
+            host = load_features(cfg.features_path, mmap=True)
+            if host.num_nodes != self.graph.num_nodes:
+                raise ConfigError("feature table and graph disagree on node count")
+            self._storage_file = str(cfg.features_path) if cfg.gids_storage == "file" else None
+            # file tier: the rows stay in the file (memory-mapped for the host API)
+            self.features = host if self._storage_file else self._pin_table(host)
+            return self._upload_graph(self.graph)
+        if cfg.gids_generator == "device":
+            # counter-based uniform generator in HBM (csrc/graph_setup.cu)
+            n, e = cfg.num_nodes, int(round(cfg.num_nodes * cfg.avg_degree))
+            dev_graph = _native.generate_uniform_graph(self.device, n, e, graph_seed)
+            self.graph = GraphCsc(num_nodes=n, num_edges=e,
+                                  indptr=dev_graph[0].cpu().numpy().view(np.uint64),
+                                  indices=dev_graph[1].cpu().numpy().astype(np.uint64))
+        else:
+            self.graph = generate_synthetic(cfg.num_nodes, cfg.avg_degree, cfg.degree_model,
+                                            seed=graph_seed, exponent=cfg.degree_exponent)
+            dev_graph = self._upload_graph(self.graph)
+        if cfg.gids_sharded_table:
+            # C5: the table lives in the ranks' HBM (sharded_table.py)
+            virtual = cfg.gids_virtual_shards > 0
+            g = cfg.gids_virtual_shards if virtual else cfg.gids_dp_world
+            self.sharded = ShardedTable(cfg.num_nodes, cfg.feature_dim, feat_seed, self.device,
+                                        0 if virtual else cfg.gids_dp_rank, g, virtual=virtual)
+            self.features = FeatureStore(num_nodes=cfg.num_nodes, dim=cfg.feature_dim,
+                                         table=None, seed=feat_seed)
+        elif cfg.gids_storage == "file":
+            # the synthetic table written once to a .gfea file, then served
+            # from the file (csrc/storage_file.cu)
+            write_synthetic_features(cfg.gids_storage_path, cfg.num_nodes, cfg.feature_dim,
+                                     feat_seed, self.device)
+            host = load_features(cfg.gids_storage_path, mmap=True)
+            self.features = FeatureStore(num_nodes=host.num_nodes, dim=host.dim,
+                                         table=host.table, seed=feat_seed)
+            self._storage_file = str(cfg.gids_storage_path)
+        else:
+            self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim, feat_seed,
+                                                 self.device)
+        return dev_graph
+
+    def _build_constant_buffer(self, dev_graph, row_bytes: int) -> None:
+        """ConstantBuffer (dataloader.py:125-135): reverse PageRank + top-k on
+        the GPU, float64-identical to cpu_buffer.py:26-109, so the pinned set
+        is the reference's."""
+        budget = self.cfg.resolved_buffer_bytes(self.graph.num_nodes, row_bytes)
+        if budget // row_bytes > 0:
+            self.pagerank, dev_scores = reverse_pagerank_device(self.device, *dev_graph)
+            chosen = top_k_nodes_device(dev_scores, budget // row_bytes)
+            del dev_scores
+            self.buffer = build_constant_buffer(self.pagerank.scores, self.features, budget,
+                                                pinned=chosen, pin_memory=True)
+        else:
+            self.pagerank = None
+            self.buffer = build_constant_buffer(np.empty(0), self.features, 0,
+                                                pinned=np.empty(0, dtype=np.int64))
+        self._pinned_mask = np.zeros(self.graph.num_nodes, dtype=bool)
+        self._pinned_mask[self.buffer.node_ids] = True
 
     def _out_block(self):
         import torch
