@@ -475,12 +475,14 @@ def main() -> None:
     row_bytes = cfg.feature_dim * 4
     host_rows = int(tiers[1] + tiers[2])
     e2e_value = world * args.steps / (ms_max / 1e3)
-    # device pipeline: sampling + decisions (control stream) overlap the gather
-    # (gather stream), so a step costs the slower of the two per-phase sums
+    # device pipeline: sampling (sampling stream), decisions (control stream)
+    # and the gather (gather stream) overlap, so a step costs the slowest of
+    # the three per-phase sums
     nb = max(1.0, phases["batches"])
-    ctl_ms = (phases["sample_ms"] + phases["cache_ms"]) / nb
+    smp_ms = phases["sample_ms"] / nb
+    ctl_ms = phases["cache_ms"] / nb
     gat_ms = (phases["gather_hits_ms"] + phases["gather_host_ms"]) / nb
-    dev_ms = max(ctl_ms, gat_ms)
+    dev_ms = max(smp_ms, ctl_ms, gat_ms)
     t = torch.tensor([dev_ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -571,12 +573,13 @@ def main() -> None:
         "tier_roofline": {"t_roof_ms": t_roof * 1e3, "frac": t_roof / step_s,
                           "host_link_peak_gbs": link_peak, "hbm_peak_gbs": hbm_peak},
         "roofline": roofline,
-        "step_bound": ("control stream (sampling + cache policy)" if ctl_ms > gat_ms else
+        "step_bound": ("sampling stream" if smp_ms >= max(ctl_ms, gat_ms) else
+                       "control stream (cache policy)" if ctl_ms >= gat_ms else
                        "gather stream (" + roofline["bound"] + ")"),
-        "value_definition": "device pipeline: 1 / max(per-step sampling+decision time on the "
-                            "control stream, per-step gather time on the gather stream), CUDA "
-                            "events on each launching stream (a second pass of K steps after "
-                            "the e2e pass), max over ranks",
+        "value_definition": "device pipeline: 1 / max(per-step sampling time on the sampling "
+                            "stream, decision time on the control stream, gather time on the "
+                            "gather stream), CUDA events on each launching stream (a second "
+                            "pass of K steps after the e2e pass), max over ranks",
         "e2e": {"value": e2e_value, "unit": "minibatches/s", "ms_per_step": ms_max / args.steps,
                 "h2d_bytes_per_step": int(cfg.batch_size * 8 + host_bytes_per_launch),
                 "d2h_bytes_per_step": 256,

@@ -128,6 +128,7 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
         for (int j = 0; j < 3; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->gev[i][j]));
     }
     GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->decided, cudaEventDisableTiming));
+    GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->counted, cudaEventDisableTiming));
     h->kind = h->kind_buf[0];
     h->line = h->line_buf[0];
     h->ins = h->ins_buf[0];
@@ -293,6 +294,7 @@ int gids_destroy(gids_handle* h) {
             if (h->gev[i][j]) cudaEventDestroy(h->gev[i][j]);
     }
     if (h->decided) cudaEventDestroy(h->decided);
+    if (h->counted) cudaEventDestroy(h->counted);
     if (h->sc_host) cudaFreeHost(h->sc_host);
     if (h->jump_host) cudaFreeHost(h->jump_host);
     if (h->rng_host) cudaFreeHost(h->rng_host);
@@ -511,7 +513,12 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
 
 int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
     CHECK_H(h);
-    GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    // waits for the decisions' counts only: work queued on the control stream
+    // after the serve (the next batches' sampling) keeps running
+    if (h->counted_valid)
+        GIDS_CUDA_TRY(cudaEventSynchronize(h->counted));
+    else
+        GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
     if (h->serve_timed) {
         float a = 0.f;
         if (cudaEventElapsedTime(&a, h->tev[2], h->tev[3]) == cudaSuccess) h->phase_ms[1] += a;

@@ -166,6 +166,8 @@ struct gids_handle {
     int64_t row_floats;
     int64_t launches;
     cudaStream_t last_stream;
+    cudaEvent_t counted = nullptr;  // the last serve's tier counts are in svc_host
+    bool counted_valid = false;
 
     // graph (HBM)
     int64_t* indptr;       // [N+1]

@@ -112,6 +112,8 @@ int gids_launch_shard_serve(gids_handle* h, const int64_t* uniq, int64_t n, floa
     GIDS_LAUNCH_CHECK(h);
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
                                   cudaMemcpyDeviceToHost, st));
+    GIDS_CUDA_TRY(cudaEventRecord(h->counted, st));
+    h->counted_valid = true;
     gids_mark(h, 3, st);
     h->last_serve_n = n;
     if (n == 0) return GIDS_OK;
@@ -206,7 +208,10 @@ int gids_shard_counts(gids_handle* h, int64_t* local, int64_t* remote) {
         return GIDS_E_INVALID;
     }
     GIDS_CUDA_TRY(cudaSetDevice(h->device));
-    GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
+    if (h->counted_valid)
+        GIDS_CUDA_TRY(cudaEventSynchronize(h->counted));
+    else
+        GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
     *local = h->svc_host->shard_local;
     *remote = h->svc_host->shard_remote;
     return GIDS_OK;

@@ -19,6 +19,7 @@ the reference orders its numpy result.
 """
 from __future__ import annotations
 
+import itertools
 import math
 import os
 import time
@@ -202,6 +203,19 @@ class Dataloader:
         gather_first = os.environ.get("GIDS_PRIORITY", "gather") != "ctl"
         self._ctl = torch.cuda.Stream(self.device, priority=0 if gather_first else -1)
         self._gat = torch.cuda.Stream(self.device, priority=-1 if gather_first else 0)
+        # run-ahead contributions (a read of the cache's residency at admission)
+        # go on a third stream ordered only after the previous batch's
+        # decisions and the batch's own sampling, so the host resolving them
+        # never waits behind the speculative sampling queued on ctl; the next
+        # decisions wait for them in turn
+        self._cnt = torch.cuda.Stream(self.device)
+        # sampling has its own stream too: it reads only the graph and the
+        # sampler's stream state, so batch b+k is sampled while batch b's
+        # decisions run on ctl (the decisions need a batch only after the
+        # host resolved it, i.e. after its sampling finished)
+        self._smp = torch.cuda.Stream(self.device, priority=0 if gather_first else -1)
+        self._last_decided = None
+        self._last_contrib = None
         self.cache = GpuCacheView(self._h, self.spec.page_bytes)
         self.window = WindowBuffer(cfg.window_depth, self._h, self._ctl.cuda_stream)
         self._sampler = Sampler(self._h, self.graph.num_nodes, cfg.fanouts)
@@ -217,6 +231,8 @@ class Dataloader:
         self._exhausted = False
         self._seeds_done = False
         self._pending: deque[_Queued] = deque()
+        # resolution runs oldest first, so the resolved entries are a prefix
+        self._n_resolved = 0
         self._spec: deque[_Queued] = deque()  # sampled ahead, not yet admitted
         self._spec_depth = cfg.gids_speculate
         self._resolved_storage = 0  # sum of resolved contributions of pending batches
@@ -314,11 +330,23 @@ class Dataloader:
         self._pinned_mask = np.zeros(self.graph.num_nodes, dtype=bool)
         self._pinned_mask[self.buffer.node_ids] = True
 
+    def _empty_on(self, stream, shape, dtype):
+        """torch.empty from `stream`'s allocator pool (torch.cuda.stream()
+        costs ~20 us of device-index lookups per use on the serving path)."""
+        import torch
+        dev0 = torch.cuda.current_device()
+        prev = torch.cuda.current_stream(self.device)
+        torch.cuda.set_stream(stream)  # (also makes self.device current)
+        try:
+            return torch.empty(shape, dtype=dtype, device=self._torch_dev)
+        finally:
+            torch.cuda.set_stream(prev)
+            if dev0 != self.device:
+                torch.cuda.set_device(dev0)
+
     def _out_block(self):
         import torch
-        with torch.cuda.stream(self._gat):
-            return torch.empty((self._unique_cap, self.features.dim), dtype=torch.float32,
-                               device=self._torch_dev)
+        return self._empty_on(self._gat, (self._unique_cap, self.features.dim), torch.float32)
 
     def _upload_graph(self, g: GraphCsc):
         """Host GraphCsc -> (indptr int64, indices int32) CUDA tensors."""
@@ -366,7 +394,7 @@ class Dataloader:
     @property
     def _pending_storage(self) -> int:
         """Sum of the pending batches' contributions (resolves them all)."""
-        for q in self._pending:
+        for q in itertools.islice(self._pending, self._n_resolved, None):
             self._resolve(q)
         return self._resolved_storage
 
@@ -374,12 +402,13 @@ class Dataloader:
         if q.batch is None:
             q.resolve(len(self.cfg.fanouts), self._sampler_rng)
             self._resolved_storage += q.storage_accesses
+            self._n_resolved += 1
 
     def _storage_at_least(self, bound: int) -> bool:
         """pending_storage >= bound, resolving (oldest first) only as needed."""
         if self._resolved_storage >= bound:
             return True
-        for q in self._pending:
+        for q in itertools.islice(self._pending, self._n_resolved, None):
             if q.batch is None:
                 self._resolve(q)
                 if self._resolved_storage >= bound:
@@ -403,17 +432,18 @@ class Dataloader:
             q = _Queued(seeds, None, None, None, None)
             q.error = e
             return q
-        st = self._ctl.cuda_stream
+        st = self._smp.cuda_stream
         words = None if self._rng_on_device else pcg_words(self._sampler_rng)
         self._h.sample(seeds, words, st)
         self._rng_on_device = True
-        with torch.cuda.stream(self._ctl):
-            edges = torch.empty((self._edge_cap, 2), dtype=torch.int64, device=self._torch_dev)
-            unique = torch.empty(self._unique_cap, dtype=torch.int64, device=self._torch_dev)
+        edges = self._empty_on(self._smp, (self._edge_cap, 2), torch.int64)
+        unique = self._empty_on(self._smp, self._unique_cap, torch.int64)
         sizes = self._sizes[self._sizes_next]
         self._sizes_next = (self._sizes_next + 1) % len(self._sizes)
         self._h.sample_export_async(edges, unique, sizes, st)
-        return _Queued(seeds, edges, unique, sizes, None)
+        sampled = torch.cuda.Event()
+        sampled.record(self._smp)
+        return _Queued(seeds, edges, unique, sizes, sampled)
 
     def _sample_one(self) -> bool:
         """One batch joins the run-ahead queue (dataloader.py:194-205): the next
@@ -428,10 +458,15 @@ class Dataloader:
             raise q.error
         L = len(self.cfg.fanouts)
         row = q.sizes.data_ptr()
-        self._h.contribution_async(q.unique, row + 8 * L, row + 8 * (L + 2),
-                                   self._ctl.cuda_stream)
+        cnt = self._cnt
+        cnt.wait_event(q.event)  # the batch's sampling and size export
+        if self._last_decided is not None:
+            cnt.wait_event(self._last_decided)  # the cache as of the last serve
+        q.unique.record_stream(cnt)
+        self._h.contribution_async(q.unique, row + 8 * L, row + 8 * (L + 2), cnt.cuda_stream)
         q.event = torch.cuda.Event()
-        q.event.record(self._ctl)
+        q.event.record(cnt)
+        self._last_contrib = q.event
         self._pending.append(q)
         return True
 
@@ -478,6 +513,7 @@ class Dataloader:
             raise StopIteration
         inflight = self._pending_storage
         entry = self._pending.popleft()
+        self._n_resolved -= 1
         self._resolved_storage -= entry.storage_accesses
         if self._ringed > 0:
             self.window.pop_iteration()
@@ -495,10 +531,22 @@ class Dataloader:
         n = unique.numel()
         rows = self._out_block()[:n]
         unique.record_stream(self._gat)
+        unique.record_stream(self._ctl)
         if tr is not None:
             t2 = time.perf_counter()
+        if self._last_contrib is not None:  # admissions read the cache this serve changes
+            self._ctl.wait_event(self._last_contrib)
+            self._last_contrib = None
         self._h.serve(unique, self._iteration, rows, self._ctl.cuda_stream,
                       self._gat.cuda_stream)
+        decided = torch.cuda.Event()
+        decided.record(self._ctl)
+        self._last_decided = decided
+        # the next batches' sampling is launched before the host waits for
+        # the decisions' counts, so the sampling stream stays busy while the
+        # host accounts and returns (the sampled content is fixed by the seed
+        # order and the sampler stream, not by when it is drawn)
+        self._speculate()
         if tr is not None:
             t3 = time.perf_counter()
         c = self._h.serve_counts()  # waits for the decisions only, not the gather
@@ -508,7 +556,7 @@ class Dataloader:
         # hand the batch to the caller's stream without blocking the host
         cur = torch.cuda.current_stream(self.device)
         cur.wait_stream(self._gat)
-        cur.wait_stream(self._ctl)
+        cur.wait_event(decided)
         for t in (rows, unique, *batch.layers):
             t.record_stream(cur)
         if self.cfg.verify_gather:
@@ -516,7 +564,6 @@ class Dataloader:
         stats = self._account(c.sampled, c.cache_hits, c.cpu_buffer_hits, c.storage,
                               c.bypasses, inflight)
         self._iteration += 1
-        self._speculate()
         return batch, rows, stats
 
     def _verify(self, unique, rows) -> None:
