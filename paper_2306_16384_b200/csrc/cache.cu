@@ -521,6 +521,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
         }
         const int32_t my_s = (int32_t)(my_ev >> 1) - 1;
         const bool my_inuse = my_ev & 1u;
+        const unsigned IU = __ballot_sync(0xffffffffu, my_inuse);
         bool hit = lane < cnt && my_s >= 0 && !((t.evict[my_s >> 5] >> (my_s & 31)) & 1u);
         bool adds = hit && !my_inuse && !((t.safe[my_s >> 5] >> (my_s & 31)) & 1u);
         int my_kind = GIDS_KIND_BYPASS, my_line = -1;
@@ -577,10 +578,14 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                 note_added(__ballot_sync(0xffffffffu, mk), my_s, safe_count, list_ok, sl, reg, P,
                            stale);
                 pos = stop;
-                if (safe_count > 0 && pos < cnt && ((M >> pos) & 1u)) {
-                    // the evicting miss at lane m = pos
+                // evictions: the miss at pos and every miss directly after it
+                // (no hit span between them) while safe lines remain, without
+                // re-deriving the chunk's masks in between; an eviction that
+                // takes a later hit's line turns that lane into a miss
+                unsigned Mr = M;
+                while (safe_count > 0 && pos < cnt && ((Mr >> pos) & 1u)) {
                     const int m = pos;
-                    const bool inuse_m = __shfl_sync(0xffffffffu, my_inuse, m);
+                    const bool inuse_m = (IU >> m) & 1u;
                     const uint32_t r = pcg_bounded32(g, (uint32_t)safe_count);
                     int32_t v;
                     if (list_ok) {
@@ -602,6 +607,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                             atomicSub(&t.sup[v >> 15], 1u);
                         }
                     }
+                    Mr |= __ballot_sync(0xffffffffu, hit && my_s == v);
                     if (my_s == v) {  // a later hit of this chunk lost its line
                         hit = false;
                         adds = false;

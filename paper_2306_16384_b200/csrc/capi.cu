@@ -230,6 +230,8 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     h->scan_parts_cap = 1024;
     A(h->scan_parts, 2 * h->scan_parts_cap);
     A(h->word_parts, h->scan_parts_cap);
+    A(h->serve_parts, 2 * h->scan_parts_cap);
+    A(h->serve_word_parts, h->scan_parts_cap);
     A(h->ev, h->serve_cap);
     for (int b = 0; b < 2; b++) {
         A(h->kind_buf[b], h->serve_cap);
@@ -280,7 +282,8 @@ int gids_destroy(gids_handle* h) {
                     h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
                     h->svc,       h->hit_list_buf[0], h->hit_list_buf[1], h->host_list_buf[0],
                     h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
-                    h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev};
+                    h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev,
+                    h->serve_parts, h->serve_word_parts};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)

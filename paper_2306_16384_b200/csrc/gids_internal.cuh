@@ -219,6 +219,10 @@ struct gids_handle {
     int64_t scan_parts_cap;
     int64_t* scan_parts;   // [scan_parts_cap * 2]
     uint32_t* word_parts;  // [scan_parts_cap]
+    // the serving path's own scan partials: sampling runs on another stream,
+    // concurrently with the decisions and the file-tier page planning
+    int64_t* serve_parts;       // [scan_parts_cap * 2]
+    uint32_t* serve_word_parts;  // [scan_parts_cap]
 
     // serve workspace
     int64_t serve_cap;     // max unique per batch
@@ -352,7 +356,7 @@ int gids_bitmap_compact(gids_handle* h, uint32_t* bm, int32_t* out, int64_t* cou
                         int64_t cap, bool clear, cudaStream_t st);
 int gids_bitmap_compact_n(gids_handle* h, uint32_t* bm, int64_t nbits, int32_t* out,
                           int64_t* count_out, int64_t cap, bool clear, int64_t* overflow,
-                          cudaStream_t st);
+                          uint32_t* parts, cudaStream_t st);
 int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* out,
                          cudaStream_t st);
 // sampler.cu

@@ -234,19 +234,20 @@ int gids_scan_take_draw(gids_handle* h, int fanout, int layer, cudaStream_t st) 
 
 int gids_bitmap_compact(gids_handle* h, uint32_t* bm, int32_t* out, int64_t* count_out,
                         int64_t cap, bool clear, cudaStream_t st) {
-    return gids_bitmap_compact_n(h, bm, h->N, out, count_out, cap, clear, &h->sc->overflow, st);
+    return gids_bitmap_compact_n(h, bm, h->N, out, count_out, cap, clear, &h->sc->overflow,
+                                 h->word_parts, st);
 }
 
 int gids_bitmap_compact_n(gids_handle* h, uint32_t* bm, int64_t nbits, int32_t* out,
                           int64_t* count_out, int64_t cap, bool clear, int64_t* overflow,
-                          cudaStream_t st) {
+                          uint32_t* parts, cudaStream_t st) {
     int64_t nwords = ceil_div(nbits, 32);
     int np = parts_for(nwords);
-    k_bm_reduce<<<np, SCAN_BLOCK, 0, st>>>(bm, nwords, h->word_parts);
+    k_bm_reduce<<<np, SCAN_BLOCK, 0, st>>>(bm, nwords, parts);
     GIDS_LAUNCH_CHECK(h);
-    k_bm_parts<<<1, MAX_PARTS, 0, st>>>(h->word_parts, np, count_out, cap, overflow);
+    k_bm_parts<<<1, MAX_PARTS, 0, st>>>(parts, np, count_out, cap, overflow);
     GIDS_LAUNCH_CHECK(h);
-    k_bm_apply<<<np, SCAN_BLOCK, 0, st>>>(bm, nwords, h->word_parts, out, cap, clear ? 1 : 0);
+    k_bm_apply<<<np, SCAN_BLOCK, 0, st>>>(bm, nwords, parts, out, cap, clear ? 1 : 0);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }
@@ -254,11 +255,12 @@ int gids_bitmap_compact_n(gids_handle* h, uint32_t* bm, int64_t nbits, int32_t* 
 int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* out,
                          cudaStream_t st) {
     int np = parts_for(n);
-    k_i32_reduce<<<np, SCAN_BLOCK, 0, st>>>(in, n, h->scan_parts);
+    // serving path only (set-associative bucketing): its own partials
+    k_i32_reduce<<<np, SCAN_BLOCK, 0, st>>>(in, n, h->serve_parts);
     GIDS_LAUNCH_CHECK(h);
-    k_i64_parts<<<1, MAX_PARTS, 0, st>>>(h->scan_parts, np);
+    k_i64_parts<<<1, MAX_PARTS, 0, st>>>(h->serve_parts, np);
     GIDS_LAUNCH_CHECK(h);
-    k_i32_apply<<<np, SCAN_BLOCK, 0, st>>>(in, n, h->scan_parts, out);
+    k_i32_apply<<<np, SCAN_BLOCK, 0, st>>>(in, n, h->serve_parts, out);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }

@@ -163,7 +163,7 @@ int gids_file_plan(gids_handle* h, int par, cudaStream_t st) {
     GIDS_LAUNCH_CHECK(h);
     GIDS_CUDA_TRY(cudaMemsetAsync(f->page_cnt, 0, 2 * sizeof(int64_t), st));
     int rc = gids_bitmap_compact_n(h, f->page_bits, f->npages, f->page_list, f->page_cnt, f->cap,
-                                   true, f->page_cnt + 1, st);
+                                   true, f->page_cnt + 1, h->serve_word_parts, st);
     if (rc) return rc;
     k_page_slot<<<gids_grid(f->cap, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
         f->page_list, f->page_cnt, f->page_slot[par]);
