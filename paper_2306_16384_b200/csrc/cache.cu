@@ -1034,9 +1034,9 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     }
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
                                   cudaMemcpyDeviceToHost, st));
+    gids_mark(h, 3, st);  // (before `counted`: serve_counts reads this mark's time)
     GIDS_CUDA_TRY(cudaEventRecord(h->counted, st));
     h->counted_valid = true;
-    gids_mark(h, 3, st);
     h->last_serve_n = n;
     if (n > 0) {
         if (gst != st) {
