@@ -173,12 +173,15 @@ __device__ __forceinline__ int64_t select_in_words(const ExactTables& t, int64_t
                                                    uint32_t r) {
     const int lane = threadIdx.x & 31;
     uint32_t word = w0 + lane < nw ? t.safe[w0 + lane] : 0u;
-    uint32_t c = __popc(word), inc = c;
+    const uint32_t c = __popc(word);
+    // inclusive prefix of the per-word counts (0..32, six bits) from one
+    // ballot per bit plane: six independent votes instead of a five-step
+    // dependent shuffle scan on the eviction's critical path
+    const unsigned le = 0xffffffffu >> (31 - lane);
+    uint32_t inc = 0;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        uint32_t u = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += u;
-    }
+    for (int k = 0; k < 6; k++)
+        inc += (uint32_t)__popc(__ballot_sync(0xffffffffu, (c >> k) & 1u) & le) << k;
     unsigned m = __ballot_sync(0xffffffffu, inc > r);
     int f = __ffs(m) - 1;
     uint32_t excl = __shfl_sync(0xffffffffu, inc - c, f);
