@@ -152,7 +152,9 @@ GIDS_API int gids_window_pop(gids_handle* h, const int64_t* nodes_dev, int64_t n
 GIDS_API int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
                float* out_dev, void* stream, void* gather_stream);
 
-/* Tier counts of the last gids_serve (synchronises `stream` only). */
+/* Tier counts of the last gids_serve: waits for that call's decisions only
+ * (an event recorded on its `stream`), not for work queued after it -- the
+ * caller may launch the next batches' sampling before asking. */
 GIDS_API int gids_serve_counts(gids_handle* h, gids_tier_counts* out);
 
 /* Per-node decisions of the last gids_serve: kind int8[U] (GIDS_KIND_*) and
@@ -239,7 +241,8 @@ GIDS_API int gids_ipc_close(int device, void* dev_ptr);
  * sharded mode (gids_serve then reads rows from the shards). */
 GIDS_API int gids_set_sharded_table(gids_handle* h, const uint64_t* shard_ptrs, int32_t n_shards,
                                     int32_t my_shard);
-/* rows of the last gids_serve read from this rank's shard / from peers */
+/* rows of the last gids_serve read from this rank's shard / from peers
+ * (waits like gids_serve_counts) */
 GIDS_API int gids_shard_counts(gids_handle* h, int64_t* local, int64_t* remote);
 
 /* synthetic_feature_rows (graph.py:256-275) for rows row0 + i*stride,
