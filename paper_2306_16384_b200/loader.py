@@ -195,7 +195,8 @@ class Dataloader:
             self._h.set_constant_buffer(self.buffer.device_ids, self.buffer.pinned)
         else:
             self._h.set_constant_buffer(self.buffer.node_ids, self.buffer.rows)
-        # two streams: sampling + cache decisions (ctl) and row movement (gather);
+        # streams: cache decisions (ctl) and row movement (gather), plus sampling
+        # and run-ahead admissions below;
         # the decisions of batch b+1 overlap the host-link gather of batch b
         # stream priority: the host link is the bottleneck resource, so by
         # default the gather's blocks are dispatched first when SM slots free
