@@ -594,6 +594,8 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
                     if (list_ok) {
                         v = __shfl_sync(0xffffffffu, sl, (int)r);
                         if (inuse_m) list_remove(sl, (int)r);
+                    } else if (safe_count == L) {
+                        v = (int32_t)r;  // every line is SafeToEvict: the r-th is line r
                     } else {
                         __syncwarp();
                         if (reg && stale) {
