@@ -281,6 +281,11 @@ GIDS_API int gids_phase_times(gids_handle* h, double out_ms[5]);
 /* Kernel launches issued by this handle since creation (evidence counter). */
 GIDS_API int64_t gids_launch_count(gids_handle* h);
 
+/* Served batches whose exact-policy decisions were made by the CTA-parallel
+ * kernel for a full cache (csrc/exact_par.cu) rather than the sequential warp,
+ * counted as gids_serve_counts reads them (evidence counter). */
+GIDS_API int64_t gids_exact_par_batches(gids_handle* h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         "gids_synthesize_rows": ([i32, u64, i64, i64, i32, vp, vp], C.c_int),
         "gids_verify_rows": ([i32, u64, vp, i64, i32, vp, vp, vp], C.c_int),
         "gids_launch_count": ([vp], i64),
+        "gids_exact_par_batches": ([vp], i64),
         "gids_generate_uniform_graph": ([i32, i64, i64, u64, vp, vp, vp], C.c_int),
         "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
                                    vp, vp], C.c_int),
@@ -137,7 +138,8 @@ def exported_symbols() -> list[str]:
             "gids_ipc_open", "gids_ipc_close", "gids_set_sharded_table", "gids_shard_counts",
             "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats",
             "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse",
-            "gids_contribution_async", "gids_host_register", "gids_host_unregister"]
+            "gids_contribution_async", "gids_host_register", "gids_host_unregister",
+            "gids_exact_par_batches"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -356,6 +358,9 @@ class Handle:
 
     def launch_count(self) -> int:
         return int(lib().gids_launch_count(self.h))
+
+    def exact_par_batches(self) -> int:
+        return int(lib().gids_exact_par_batches(self.h))
 
 
 def synthesize_rows(device: int, seed: int, row0: int, n: int, dim: int, dst, stream: int) -> None:

@@ -88,7 +88,9 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                                  const int32_t* __restrict__ slot_of, uint32_t* safe_bits,
                                  uint32_t* blk_cnt, uint32_t* sup_cnt, int exact,
                                  CacheMeta* meta, uint32_t* ev, int mode = 3,
-                                 int32_t* counts = nullptr, int64_t* nmiss0 = nullptr) {
+                                 int32_t* counts = nullptr, int64_t* nmiss0 = nullptr,
+                                 uint32_t* xcls = nullptr, int32_t* cand_of_slot = nullptr,
+                                 int32_t* cand_slot = nullptr, int64_t* n_cand = nullptr) {
     int64_t inc = 0, dec = 0, unsafe = 0, miss0 = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
@@ -119,6 +121,30 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
         reuse[x] = now;
         if (mode & 2) ev[p] = ((uint32_t)(s + 1) << 1) | (now > 0 ? 1u : 0u);
         miss0 += s < 0;
+        if (xcls && (mode & 2)) {
+            // the access's class for k_exact_par: by the invariant "resident
+            // line InUse iff count > 0", the count before this access's own
+            // consumption (old + c) tells a protected line from a safe one
+            const bool cb = old + c > 0, ca = now > 0;
+            const bool cand = s >= 0 && !cb;
+            uint32_t cls = s >= 0 ? (ca ? GIDS_XC_STAY : cb ? GIDS_XC_ADD : GIDS_XC_CAND)
+                                  : (ca ? GIDS_XC_MU : GIDS_XC_M0);
+            const unsigned am = __activemask();
+            const unsigned cm = __ballot_sync(am, cand);
+            const int leader = __ffs(am) - 1, lane = threadIdx.x & 31;
+            unsigned long long b0 = 0;
+            if (lane == leader && cm) b0 = atomicAdd((unsigned long long*)n_cand, (unsigned long long)__popc(cm));
+            b0 = __shfl_sync(am, b0, leader);
+            if (cand) {
+                const int64_t idx = (int64_t)b0 + __popc(cm & ((1u << lane) - 1u));
+                if (idx < GIDS_XP_CAND_CAP) {
+                    cand_of_slot[s] = (int32_t)idx;
+                    cand_slot[idx] = s;
+                    cls |= (uint32_t)idx << 3;
+                }
+            }
+            xcls[p] = cls;
+        }
     }
     inc = warp_sum64(inc);
     dec = warp_sum64(dec);
@@ -398,6 +424,7 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
             int32_t* __restrict__ log_pos, ServeCounters* svc) {
     extern __shared__ uint32_t sm[];
     if (svc->n_miss0 == 0) return;  // all hits: decided by k_exact_allhit
+    if (svc->xp_done) return;       // full cache: decided by k_exact_par
     const int lane = threadIdx.x;
     const unsigned below = (1u << lane) - 1u;
     const int64_t nw = (L + 31) / 32, nb = (L + 1023) / 1024, ns = (L + 32767) / 32768;
@@ -921,6 +948,10 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
 }  // namespace
 
 static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t st) {
+    {
+        int rc = gids_launch_exact_par(h, n, st);
+        if (rc) return rc;
+    }
     k_exact_allhit<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
         h->ev, n, h->meta, h->safe_bits, h->blk_cnt, h->sup_cnt, h->svc, h->kind, h->line);
     GIDS_LAUNCH_CHECK(h);
@@ -978,7 +1009,9 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
         k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
                                               h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
-                                              h->meta, h->ev, 3, nullptr, &h->svc->n_miss0);
+                                              h->meta, h->ev, 3, nullptr, &h->svc->n_miss0,
+                                              exact ? h->xcls : nullptr, h->cand_of_slot,
+                                              h->cand_slot, &h->svc->n_cand);
         GIDS_LAUNCH_CHECK(h);
         if (exact) {
             size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
@@ -993,6 +1026,8 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
             GIDS_LAUNCH_CHECK(h);
             k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
             GIDS_LAUNCH_CHECK(h);
+            int rc2 = gids_launch_xp_reset(h, st);
+            if (rc2) return rc2;
         } else {
             GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cnt, 0, sizeof(int32_t) * h->sets, st));
             GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cur, 0, sizeof(int32_t) * h->sets, st));
@@ -1108,7 +1143,8 @@ extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n
     const int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
     k_window_consume<<<g, BLOCK, 0, st>>>(nodes, n, h->future, h->reuse, h->slot_of,
                                           h->safe_bits, h->blk_cnt, h->sup_cnt, 1, h->meta, h->ev,
-                                          2, nullptr, &h->svc->n_miss0);
+                                          2, nullptr, &h->svc->n_miss0, h->xcls,
+                                          h->cand_of_slot, h->cand_slot, &h->svc->n_cand);
     GIDS_LAUNCH_CHECK(h);
     size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
     {
@@ -1124,6 +1160,10 @@ extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n
     GIDS_LAUNCH_CHECK(h);
     k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
     GIDS_LAUNCH_CHECK(h);
+    {
+        int rc = gids_launch_xp_reset(h, st);
+        if (rc) return rc;
+    }
     GIDS_CUDA_TRY(cudaMemcpyAsync(kind_out, h->kind, n, cudaMemcpyDeviceToDevice, st));
     GIDS_CUDA_TRY(cudaMemcpyAsync(line_out, h->line, sizeof(int32_t) * n,
                                   cudaMemcpyDeviceToDevice, st));

@@ -75,7 +75,8 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
     GIDS_CUDA_TRY(cudaMemset(h->slot_of, 0xff, sizeof(int32_t) * N));
     GIDS_CUDA_TRY(cudaMemset(h->line_node, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
     GIDS_CUDA_TRY(cudaMemset(h->last_ins, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
-    GIDS_CUDA_TRY(cudaMemset(h->safe_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
+    GIDS_CUDA_TRY(cudaMemset(h->safe_bits, 0, sizeof(uint32_t) * 32 * ceil_div(L > 0 ? L : 1, 1024)));
+    GIDS_CUDA_TRY(cudaMemset(h->cand_of_slot, 0xff, sizeof(int32_t) * (L > 0 ? L : 1)));
     GIDS_CUDA_TRY(cudaMemset(h->evict_bits, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32)));
     GIDS_CUDA_TRY(cudaMemset(h->blk_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 1024)));
     GIDS_CUDA_TRY(cudaMemset(h->sup_cnt, 0, sizeof(uint32_t) * ceil_div(L > 0 ? L : 1, 32768)));
@@ -96,6 +97,11 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
     size_t with_bits = gids_exact_smem_bytes(L, true), without = gids_exact_smem_bytes(L, false);
     const size_t static_smem = 4096;  // k_exact_seq's event ring
     h->exact_smem = with_bits + static_smem <= (size_t)dev_smem;
+    {
+        const char* e = getenv("GIDS_EXACT_PAR");
+        h->xp_enabled = !(e && e[0] == '0') && gids_xp_smem_bytes(L) <= (size_t)dev_smem &&
+                        h->cfg.policy == GIDS_POLICY_EXACT && L > 0;
+    }
     if (!h->exact_smem && without + static_smem > (size_t)dev_smem) {
         gids_set_error("cache_lines too large for the exact policy (use the set-associative one)");
         gids_destroy(h);
@@ -207,7 +213,12 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->cache_rows, L * h->row_floats);
     A(h->slot_of, N);
     A(h->line_node, L);
-    A(h->safe_bits, ceil_div(L, 32));
+    A(h->safe_bits, 32 * ceil_div(L, 1024));  // whole 1024-line blocks (exact_par.cu)
+    A(h->cand_of_slot, L);
+    A(h->cand_slot, GIDS_XP_CAND_CAP);
+    A(h->xcls, h->serve_cap);
+    h->xp_hcap = h->serve_cap + h->serve_cap / 32 + 4096;
+    A(h->xp_halves, h->xp_hcap);
     A(h->evict_bits, ceil_div(L, 32));
     A(h->blk_cnt, ceil_div(L, 1024));
     A(h->sup_cnt, ceil_div(L, 32768));
@@ -283,7 +294,8 @@ int gids_destroy(gids_handle* h) {
                     h->svc,       h->hit_list_buf[0], h->hit_list_buf[1], h->host_list_buf[0],
                     h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
                     h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev,
-                    h->serve_parts, h->serve_word_parts};
+                    h->serve_parts, h->serve_word_parts, h->cand_of_slot, h->cand_slot,
+                    h->xcls,      h->xp_halves};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)
@@ -510,6 +522,7 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
         return GIDS_E_STATE;
     }
     h->last_stream = (cudaStream_t)stream;
+    h->counts_read = false;
     return gids_launch_serve(h, unique_dev, n, epoch, out_dev, (cudaStream_t)stream,
                              gather_stream ? (cudaStream_t)gather_stream : (cudaStream_t)stream);
 }
@@ -530,6 +543,8 @@ int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
         h->serve_timed = false;
     }
     const ServeCounters& c = *h->svc_host;
+    if (!h->counts_read && c.xp_done) h->xp_batches++;
+    h->counts_read = true;
     out->sampled = h->last_serve_n;
     out->cache_hits = c.tiers[0];
     out->cpu_buffer_hits = c.tiers[1];
@@ -646,5 +661,6 @@ int gids_host_unregister(void* ptr) {
 
 int64_t gids_cache_capacity(gids_handle* h) { return h ? h->L : -1; }
 int64_t gids_launch_count(gids_handle* h) { return h ? h->launches : -1; }
+int64_t gids_exact_par_batches(gids_handle* h) { return h ? h->xp_batches : -1; }
 
 }  // extern "C"

@@ -140,6 +140,8 @@ struct ServeCounters {
     int64_t n_log;         // insertions logged by the exact policy this batch
     int64_t n_miss0;       // nodes not resident when the batch's decisions start
     int64_t shard_local, shard_remote;  // sharded-table mode: rows from own / peer HBM
+    int64_t n_cand;        // resident SafeToEvict nodes of the batch (exact_par.cu)
+    int64_t xp_done;       // the batch was decided by k_exact_par
 };
 
 struct CacheMeta {  // persistent cache counters (CacheState)
@@ -193,6 +195,15 @@ struct gids_handle {
     uint8_t* future;       // [N] lookahead-window occurrence counts
     CacheMeta* meta;       // device
     int32_t* last_ins;     // [L] scratch: last log index per line (-1)
+    // CTA-parallel exact policy for a full cache (exact_par.cu)
+    uint32_t* xcls;        // [serve_cap] access class | candidate index << 3
+    int32_t* cand_of_slot; // [L] candidate index of the line's batch-start node, -1
+    int32_t* cand_slot;    // [GIDS_XP_CAND_CAP] line of each candidate
+    uint32_t* xp_halves;   // [xp_hcap] the batch's eviction draw halves
+    int64_t xp_hcap;
+    bool xp_enabled;       // GIDS_EXACT_PAR=0 keeps every batch on k_exact_seq
+    int64_t xp_batches;    // served batches k_exact_par decided
+    bool counts_read;      // the last serve's counts were read once already
 
     // sampler workspace (HBM)
     int64_t max_seeds;
@@ -364,6 +375,13 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_word
                        cudaStream_t st);
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
 int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st);
+// exact_par.cu
+constexpr int64_t GIDS_XP_CAND_CAP = 1 << 17;
+// access classes of a batch against a full cache (k_window_consume -> k_exact_par)
+enum { GIDS_XC_STAY = 0, GIDS_XC_ADD = 1, GIDS_XC_CAND = 2, GIDS_XC_M0 = 3, GIDS_XC_MU = 4 };
+int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st);
+int gids_launch_xp_reset(gids_handle* h, cudaStream_t st);
+size_t gids_xp_smem_bytes(int64_t L);
 // cache.cu
 int gids_launch_serve(gids_handle* h, const int64_t* unique, int64_t n, uint64_t epoch,
                       float* out, cudaStream_t st, cudaStream_t gst);

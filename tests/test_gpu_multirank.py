@@ -38,4 +38,4 @@ def test_two_rank_bench_prints_one_line(extra):
     assert len(lines) == 1, out.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
-    assert d["config"]["parallelism"] == "dp2"
+    assert d["parallelism"] == "dp2"
