@@ -609,6 +609,7 @@ def main() -> None:
                 "note": "timed through Dataloader.next_batch (the public API): host seed "
                         "batches in, host-tier rows over the link, per-step stats read back"},
         "gpu_launches": launches, "clocks": clocks,
+        "exact_par": h.exact_par_stats() if cfg.gids_policy == "exact" else None,
         "storage_file": dl.storage_stats(),
         "numa": numa,
         "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),

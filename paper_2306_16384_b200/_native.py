@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         "gids_verify_rows": ([i32, u64, vp, i64, i32, vp, vp, vp], C.c_int),
         "gids_launch_count": ([vp], i64),
         "gids_exact_par_batches": ([vp], i64),
+        "gids_exact_par_stats": ([vp, vp], C.c_int),
         "gids_generate_uniform_graph": ([i32, i64, i64, u64, vp, vp, vp], C.c_int),
         "gids_reverse_pagerank": ([i32, i64, i64, vp, vp, C.c_double, C.c_double, i32, vp, vp,
                                    vp, vp], C.c_int),
@@ -139,7 +140,7 @@ def exported_symbols() -> list[str]:
             "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats",
             "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse",
             "gids_contribution_async", "gids_host_register", "gids_host_unregister",
-            "gids_exact_par_batches"]
+            "gids_exact_par_batches", "gids_exact_par_stats"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -361,6 +362,12 @@ class Handle:
 
     def exact_par_batches(self) -> int:
         return int(lib().gids_exact_par_batches(self.h))
+
+    def exact_par_stats(self) -> dict:
+        out = np.zeros(4, np.int64)
+        check(lib().gids_exact_par_stats(self.h, out.ctypes.data), "exact_par_stats")
+        return dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line"),
+                        out.tolist()), batches=self.exact_par_batches())
 
 
 def synthesize_rows(device: int, seed: int, row0: int, n: int, dim: int, dst, stream: int) -> None:

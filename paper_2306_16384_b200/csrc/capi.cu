@@ -213,7 +213,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->cache_rows, L * h->row_floats);
     A(h->slot_of, N);
     A(h->line_node, L);
-    A(h->safe_bits, 32 * ceil_div(L, 1024));  // whole 1024-line blocks (exact_par.cu)
+    A(h->safe_bits, 32 * ceil_div(L > 0 ? L : 1, 1024));  // whole 1024-line blocks (exact_par.cu)
     A(h->cand_of_slot, L);
     A(h->cand_slot, GIDS_XP_CAND_CAP);
     A(h->xcls, h->serve_cap);
@@ -543,7 +543,10 @@ int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
         h->serve_timed = false;
     }
     const ServeCounters& c = *h->svc_host;
-    if (!h->counts_read && c.xp_done) h->xp_batches++;
+    if (!h->counts_read && c.xp_done) {
+        h->xp_batches++;
+        for (int i = 0; i < 4; i++) h->xp_stats[i] += c.xp_stats[i];
+    }
     h->counts_read = true;
     out->sampled = h->last_serve_n;
     out->cache_hits = c.tiers[0];
@@ -662,5 +665,10 @@ int gids_host_unregister(void* ptr) {
 int64_t gids_cache_capacity(gids_handle* h) { return h ? h->L : -1; }
 int64_t gids_launch_count(gids_handle* h) { return h ? h->launches : -1; }
 int64_t gids_exact_par_batches(gids_handle* h) { return h ? h->xp_batches : -1; }
+int gids_exact_par_stats(gids_handle* h, int64_t out[4]) {
+    CHECK_H(h);
+    for (int i = 0; i < 4; i++) out[i] = h->xp_stats[i];
+    return GIDS_OK;
+}
 
 }  // extern "C"

@@ -26,13 +26,18 @@
 //   A  classify, saturating prefix of the safe count, prefix of the draws
 //   B  Lemire-bounded draw per miss (numpy integers(n), buffered 32-bit
 //      halves); a rejection ends the round after that access
-//   C  every evicting access selects the r-th safe line of the round-START set
-//      (interpolated block search over shared-memory prefix counts, then the
-//      32 words of the 1024-line block from the L2-resident bitmap)
-//   D  one warp finalises the round's set changes in order: each MU answer is
-//      moved past the earlier changes (removal at or below -> next safe line,
-//      addition below -> previous safe line) on a private copy of its block
-//   E  every other evicting access applies the finalised changes the same way
+//   C  the round's ADD lines join the bitmap and the prefix counts at once:
+//      T = start set + ADDs.  An access then sees T minus its "holes" -- the
+//      ADD lines of later accesses and the lines earlier MU accesses removed
+//      -- and its eviction is the least fixed point of q = r + #holes(<= line
+//      of rank q in T), found from q = r by a few selects in T (interpolated
+//      block search over shared-memory prefix counts, then the 32 words of
+//      the 1024-line block from the L2-resident bitmap, kept in registers)
+//      and popcounts of prefix masks over the line-sorted change list
+//   D  the MU lines are themselves answers: Jacobi passes over the
+//      triangular system until none moves (pass k fixes the first k; two in
+//      practice)
+//   E  every other eviction resolves once against the final change list
 //   F  a CAND whose line was taken earlier (this or the previous round; older
 //      rounds flag it through cand_of_slot) ends the round before itself and
 //      is a miss in the next one
@@ -44,9 +49,9 @@
 
 namespace {
 
-constexpr int XT = 256;           // threads = accesses per round
+constexpr int XT = 512;           // threads = accesses per round
 constexpr int XW = XT / 32;
-constexpr int XP_MAX_CHG = 32;    // set changes per round (the round ends before the 33rd)
+constexpr int XP_MAX_CHG = 64;    // set changes per round (the round ends before the 65th)
 constexpr int RING = 4096;        // staged accesses (ev, class)
 constexpr int HRING = 4096;       // staged draw halves
 constexpr int RING_LAG = 12;      // commit groups allowed in flight when a round reads
@@ -125,130 +130,39 @@ struct XpArgs {
     int32_t* log_pos;
 };
 
-// shared-memory view of the round state
+// shared-memory view of the round state.  Within a round the tables and the
+// global bitmap describe T = (round-start safe set) + (the round's ADD lines);
+// an access sees T minus its "holes": the ADD lines of later accesses and the
+// lines removed by earlier MU accesses.
 struct Xs {
-    uint32_t* CNT;    // [nb] safe lines per block
+    uint32_t* CNT;    // [nb] lines of T per block
     uint32_t* BLKP;   // [nb] exclusive prefix within the 32-block superblock
     uint32_t* SUPP;   // [ns+1] exclusive prefix over superblocks
+    uint32_t* STOT;   // [ns] superblock totals
+    uint32_t* TOUCH;  // [(ns+31)/32] superblocks whose counts changed
     uint32_t* CONV;   // [cand_cap/32] candidates whose line was taken
-    uint32_t* ROWS;   // [XT*32] private block copies (16-B chunks swizzled)
-    int32_t* ROWBLK;  // [XT] block held by each row (-1 none)
+    uint32_t* ROWS;   // [XT*32] each access's block of T
     uint32_t* REV;    // [RING]
     uint32_t* RCL;    // [RING]
     uint32_t* RH;     // [HRING]
     int32_t* ANS;     // [XT] final line per evicting access of the round, -1
     int32_t* PANS;    // [XT] same, previous round
-    int32_t* CSLOT;   // [XP_MAX_CHG]
-    int32_t* CTYPE;   // [XP_MAX_CHG] +1 add, -1 remove
-    int32_t* CLANE;   // [XP_MAX_CHG]
+    int32_t* CSLOT;   // [XP_MAX_CHG] line of each set change, in access order
+    int32_t* CTYPE;   // [XP_MAX_CHG] +1 ADD, -1 MU
+    int32_t* SS;      // [XP_MAX_CHG] change lines, ascending
+    int32_t* SIDX;    // [XP_MAX_CHG] their change indices
+    unsigned long long* PM;  // [XP_MAX_CHG+1] change-index mask of the k lowest lines
+    int32_t* CANL;    // [XT] lanes of this round's unconverted candidates
+    int32_t* CANS;    // [XT] their lines
     int32_t* W;       // [XW * 8] warp partials
     int32_t* MISC;    // [16]
     int64_t nb, ns, L;
     const uint32_t* gbits;
 };
 
-__device__ __forceinline__ uint32_t& rw(const Xs& x, int row, int w) {
-    return x.ROWS[row * 32 + ((((w >> 2) ^ (row & 7)) << 2) | (w & 3))];
-}
-
-// block g of the round-start bitmap into `row`, then the changes [0, lim) that
-// fall into it (the finalised prefix of this round's change list)
-__device__ void load_row(const Xs& x, int row, int64_t g, int lim) {
-    const uint4* src = reinterpret_cast<const uint4*>(x.gbits + g * 32);
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-        const uint4 v = __ldcg(src + q);
-        uint32_t* d = &x.ROWS[row * 32 + ((q ^ (row & 7)) << 2)];
-        d[0] = v.x;
-        d[1] = v.y;
-        d[2] = v.z;
-        d[3] = v.w;
-    }
-    for (int i = 0; i < lim; i++) {
-        const int32_t u = x.CSLOT[i];
-        if ((u >> 10) == g) {
-            uint32_t& wd = rw(x, row, (u >> 5) & 31);
-            if (x.CTYPE[i] > 0) wd |= 1u << (u & 31);
-            else wd &= ~(1u << (u & 31));
-        }
-    }
-    x.ROWBLK[row] = (int32_t)g;
-}
-
-// smallest safe line > cur in the current set (L if none)
-__device__ int32_t next_safe(const Xs& x, int row, int32_t cur, int lim) {
-    int64_t g = cur >> 10;
-    int b = (cur & 1023) + 1;
-    for (;;) {
-        if (b < 1024) {
-            if (x.ROWBLK[row] != g) load_row(x, row, g, lim);
-            for (int w = b >> 5; w < 32; w++) {
-                uint32_t m = rw(x, row, w);
-                if (w == (b >> 5)) m &= 0xffffffffu << (b & 31);
-                if (m) return (int32_t)(g * 1024 + w * 32 + __ffs(m) - 1);
-            }
-        }
-        g++;
-        b = 0;
-        if (g >= x.nb) return (int32_t)x.L;
-    }
-}
-
-// largest safe line < cur in the current set (-1 if none); cur may be L
-__device__ int32_t prev_safe(const Xs& x, int row, int32_t cur, int lim) {
-    int64_t g = (cur - 1) >> 10;
-    if (cur <= 0) return -1;
-    int b = (cur - 1) & 1023;  // last candidate bit in block g
-    if ((int64_t)cur >= x.L) {
-        g = x.nb - 1;
-        b = 1023;
-    }
-    for (;;) {
-        if (x.ROWBLK[row] != g) load_row(x, row, g, lim);
-        for (int w = b >> 5; w >= 0; w--) {
-            uint32_t m = rw(x, row, w);
-            if (w == (b >> 5) && (b & 31) != 31) m &= (2u << (b & 31)) - 1u;
-            if (m) return (int32_t)(g * 1024 + w * 32 + 31 - __clz(m));
-        }
-        if (g == 0) return -1;
-        g--;
-        b = 1023;
-    }
-}
-
-// move an answer past one set change (u, ty) made before its access:
-// removal at or below -> next safe line; addition below -> previous safe line
-// (the new set holds u).  cur == L with excess ex: the rank is ex past the end.
-__device__ __forceinline__ void apply_change(const Xs& x, int row, int32_t u, int ty,
-                                             int32_t& cur, int32_t& ex, int lim) {
-    if (x.ROWBLK[row] == (u >> 10)) {
-        uint32_t& wd = rw(x, row, (u >> 5) & 31);
-        if (ty > 0) wd |= 1u << (u & 31);
-        else wd &= ~(1u << (u & 31));
-    }
-    if ((int64_t)cur >= x.L) {
-        if (ty < 0) {
-            ex++;
-        } else if (ex > 0) {
-            ex--;
-        } else {
-            cur = prev_safe(x, row, (int32_t)x.L, lim);
-        }
-        return;
-    }
-    if (ty < 0) {
-        if (u <= cur) {
-            cur = next_safe(x, row, cur, lim);
-            if ((int64_t)cur >= x.L) ex = 0;
-        }
-    } else if (u < cur) {
-        cur = prev_safe(x, row, cur, lim);
-    }
-}
-
 __device__ __forceinline__ uint32_t pb(const Xs& x, int64_t g) { return x.SUPP[g >> 5] + x.BLKP[g]; }
 
-// block holding the r-th safe line of the round-start set (r < total)
+// block holding the r-th line of T (r < total)
 __device__ int64_t locate(const Xs& x, uint32_t r, uint32_t total) {
     const int64_t nb = x.nb;
     const uint32_t avg = total / (uint32_t)nb > 0 ? total / (uint32_t)nb : 1u;
@@ -275,6 +189,169 @@ __device__ int64_t locate(const Xs& x, uint32_t r, uint32_t total) {
     return lo;
 }
 
+// a 1024-line block of T held by one access: its 32 words in the access's
+// shared-memory row (16-B chunks swizzled by lane), the exclusive popcount
+// prefix of its eight 4-word groups in registers
+struct Blk {
+    int64_t g;
+    uint32_t gp[8];
+    uint32_t* row;
+    int sw;  // swizzle (thread & 7)
+};
+
+__device__ __forceinline__ void load_blk(const Xs& x, Blk& B, int64_t g) {
+    const uint4* src = reinterpret_cast<const uint4*>(x.gbits + g * 32);
+    uint32_t run = 0;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+        const uint4 v = __ldcg(src + q);
+        *reinterpret_cast<uint4*>(B.row + ((q ^ B.sw) << 2)) = v;
+        B.gp[q] = run;
+        run += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    }
+    B.g = g;
+}
+
+// position of the k-th set bit of w (k < popc(w))
+__device__ __forceinline__ int bit_select(uint32_t w, uint32_t k) {
+    int pos = 0;
+    uint32_t c = __popc(w & 0xffffu);
+    if (k >= c) { k -= c; pos = 16; }
+    c = __popc((w >> pos) & 0xffu);
+    if (k >= c) { k -= c; pos += 8; }
+    c = __popc((w >> pos) & 0xfu);
+    if (k >= c) { k -= c; pos += 4; }
+    c = __popc((w >> pos) & 0x3u);
+    if (k >= c) { k -= c; pos += 2; }
+    if (k >= ((w >> pos) & 1u)) pos += 1;
+    return pos;
+}
+
+// the rr-th set bit of the held block
+__device__ __forceinline__ int32_t sel_blk(const Blk& B, uint32_t rr) {
+    int grp = 0;
+    uint32_t base = 0;
+#pragma unroll
+    for (int j = 1; j < 8; j++)
+        if (B.gp[j] <= rr) {
+            grp = j;
+            base = B.gp[j];
+        }
+    const uint4 w4 = *reinterpret_cast<const uint4*>(B.row + ((grp ^ B.sw) << 2));
+    uint32_t k = rr - base, w = w4.x;
+    int wi = 0;
+    uint32_t c = __popc(w4.x);
+    if (k >= c) {
+        k -= c;
+        wi = 1;
+        w = w4.y;
+        c = __popc(w4.y);
+        if (k >= c) {
+            k -= c;
+            wi = 2;
+            w = w4.z;
+            c = __popc(w4.z);
+            if (k >= c) {
+                k -= c;
+                wi = 3;
+                w = w4.w;
+            }
+        }
+    }
+    return grp * 128 + wi * 32 + bit_select(w, k);
+}
+
+// the q-th line of T (the held block is reused when it covers q)
+__device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total, Blk& B) {
+    uint32_t base = B.g >= 0 ? pb(x, B.g) : 0u;
+    if (B.g < 0 || q < base || q >= base + x.CNT[B.g]) {
+        load_blk(x, B, locate(x, q, total));
+        base = pb(x, B.g);
+    }
+    return (int32_t)(B.g * 1024) + sel_blk(B, q - base);
+}
+
+// lines among the round's changes <= y
+__device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
+    int lo = 0, hi = m;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (x.SS[mid] <= y) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// the r-th line of T minus `holes` (a mask over the change list): the least
+// fixed point of q = r + #holes(<= sel_T(q)), reached from q = r
+__device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned long long holes,
+                                           int m, uint32_t total, Blk& B) {
+    uint32_t q = r;
+    int32_t y = sel_T(x, q, total, B);
+    if (!holes) return y;
+    for (int it = 0; it <= XP_MAX_CHG; it++) {
+        const uint32_t q2 = r + (uint32_t)__popcll(x.PM[count_le(x, m, y)] & holes);
+        if (q2 == q) break;
+        q = q2;
+        y = sel_T(x, q, total, B);
+    }
+    return y;
+}
+
+// re-prefix the superblocks flagged in TOUCH (all threads; ends synchronised)
+__device__ void rebuild(const Xs& x, int t) {
+    const int lane = t & 31, wid = t >> 5;
+    const int nsw = (int)((x.ns + 31) >> 5);
+    int k = 0;
+    for (int w32 = 0; w32 < nsw; w32++) {
+        uint32_t bits = x.TOUCH[w32];
+        while (bits) {
+            const int sb = w32 * 32 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            if (sb >= x.ns) break;
+            if ((k % XW) == wid) {
+                const int64_t blk = (int64_t)sb * 32 + lane;
+                const uint32_t c = blk < x.nb ? x.CNT[blk] : 0u;
+                uint32_t inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += u;
+                }
+                if (blk < x.nb) x.BLKP[blk] = inc - c;
+                if (lane == 31) x.STOT[sb] = inc;
+            }
+            k++;
+        }
+    }
+    __syncthreads();
+    if (wid == 0 && k > 0) {  // SUPP = exclusive prefix of STOT
+        const int per = (int)((x.ns + 31) >> 5);
+        uint32_t loc = 0;
+        for (int i = 0; i < per; i++) {
+            const int64_t s = (int64_t)lane * per + i;
+            loc += s < x.ns ? x.STOT[s] : 0u;
+        }
+        uint32_t inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        uint32_t run = inc - loc;
+        for (int i = 0; i < per; i++) {
+            const int64_t s = (int64_t)lane * per + i;
+            if (s < x.ns) {
+                run += x.STOT[s];
+                x.SUPP[s + 1] = run;
+            }
+        }
+    }
+    if (wid == 1 || XW == 1)
+        for (int i = lane; i < nsw; i += 32) x.TOUCH[i] = 0u;
+    __syncthreads();
+}
+
 __device__ __forceinline__ uint32_t get_half(const Xs& x, const XpArgs& a, int64_t k,
                                              int64_t kfill) {
     if (k < kfill && k >= kfill - HRING) return x.RH[k % HRING];
@@ -282,11 +359,17 @@ __device__ __forceinline__ uint32_t get_half(const Xs& x, const XpArgs& a, int64
     return half_direct(a.meta, k);
 }
 
-// (d, c): x -> max(x + d, c); compose(first, then)
+// (d, c): x -> max(x + d, c); (d2, c2) becomes "(d1, c1) first, then (d2, c2)"
 __device__ __forceinline__ void sat_compose(int32_t d1, int32_t c1, int32_t& d2, int32_t& c2) {
     const int32_t c = max(c1 + d2, c2);
     d2 = d1 + d2;
     c2 = c;
+}
+
+__device__ __forceinline__ void stage(uint32_t* dst, const uint32_t* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src));
 }
 
 __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
@@ -301,6 +384,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     x.gbits = a.safe_bits;
     {
         uint32_t* p = smem;
+        x.PM = reinterpret_cast<unsigned long long*>(p);
+        p += 2 * (XP_MAX_CHG + 2);
         x.ROWS = p;
         p += XT * 32;
         x.REV = p;
@@ -315,10 +400,12 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += x.nb;
         x.SUPP = p;
         p += x.ns + 1;
+        x.STOT = p;
+        p += x.ns;
+        x.TOUCH = p;
+        p += (x.ns + 31) / 32;
         x.CONV = p;
         p += (a.cand_cap + 31) / 32;
-        x.ROWBLK = reinterpret_cast<int32_t*>(p);
-        p += XT;
         x.ANS = reinterpret_cast<int32_t*>(p);
         p += XT;
         x.PANS = reinterpret_cast<int32_t*>(p);
@@ -327,60 +414,42 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += XP_MAX_CHG;
         x.CTYPE = reinterpret_cast<int32_t*>(p);
         p += XP_MAX_CHG;
-        x.CLANE = reinterpret_cast<int32_t*>(p);
+        x.SS = reinterpret_cast<int32_t*>(p);
         p += XP_MAX_CHG;
+        x.SIDX = reinterpret_cast<int32_t*>(p);
+        p += XP_MAX_CHG;
+        x.CANL = reinterpret_cast<int32_t*>(p);
+        p += XT;
+        x.CANS = reinterpret_cast<int32_t*>(p);
+        p += XT;
         x.W = reinterpret_cast<int32_t*>(p);
         p += XW * 8;
         x.MISC = reinterpret_cast<int32_t*>(p);
     }
     const int64_t n = a.n, nb = x.nb, ns = x.ns;
-    // prefix tables from the block counts
     for (int64_t i = t; i < nb; i += XT) x.CNT[i] = a.blk_cnt[i];
     for (int64_t i = t; i < (a.cand_cap + 31) / 32; i += XT) x.CONV[i] = 0u;
-    x.ROWBLK[t] = -1;
+    for (int64_t i = t; i < (ns + 31) / 32; i += XT) x.TOUCH[i] = ~0u;  // (all: first prefix)
     x.PANS[t] = -1;
-    __syncthreads();
-    for (int64_t s = t; s < ns; s += XT) {
-        uint32_t run = 0;
-        for (int64_t b = s * 32; b < nb && b < s * 32 + 32; b++) {
-            x.BLKP[b] = run;
-            run += x.CNT[b];
-        }
-        x.SUPP[s + 1] = run;  // per-superblock totals, prefixed next
-    }
-    __syncthreads();
-    if (t == 0) {
-        uint32_t run = 0;
-        x.SUPP[0] = 0;
-        for (int64_t s = 0; s < ns; s++) {
-            run += x.SUPP[s + 1];
-            x.SUPP[s + 1] = run;
-        }
-    }
+    if (t == 0) x.SUPP[0] = 0;
     // stage the first accesses and halves
     int64_t efill = n < RING ? n : RING;
     int64_t kfill = a.hcap < HRING ? a.hcap : HRING;
     for (int64_t i = t; i < efill; i += XT) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&x.REV[i % RING])),
-                     "l"(a.ev + i));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&x.RCL[i % RING])),
-                     "l"(a.xcls + i));
+        stage(&x.REV[i % RING], a.ev + i);
+        stage(&x.RCL[i % RING], a.xcls + i);
     }
-    for (int64_t i = t; i < kfill; i += XT)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(&x.RH[i % HRING])),
-                     "l"(a.H + i));
+    for (int64_t i = t; i < kfill; i += XT) stage(&x.RH[i % HRING], a.H + i);
     asm volatile("cp.async.commit_group;");
     asm volatile("cp.async.wait_group 0;");
     __syncthreads();
+    rebuild(x, t);
 
     int64_t pos = 0, kpos = 0, nlog = 0;
     int32_t nsafe = (int32_t)a.meta->safe_count;
-    int prevE = 0;
     int32_t pend_cidx = -1;  // cand_of_slot of this thread's last committed eviction
     int64_t hits = 0, misses = 0, byp = 0;
+    int64_t st_rounds = 0, st_rej = 0, st_chg = 0, st_conv = 0;  // round ends (thread 0)
 
     while (pos < n) {
         asm volatile("cp.async.wait_group %0;" ::"n"(RING_LAG));
@@ -401,8 +470,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             d = -1;
             c = 0;
         }
-        // inclusive warp scan of the saturating map
-        int32_t di = d, ci = c;
+        int32_t di = d, ci = c;  // inclusive warp scan of the saturating map
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int32_t d2 = __shfl_up_sync(0xffffffffu, di, o);
@@ -421,15 +489,23 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         if (t == 0) {
             x.MISC[0] = XT;  // end of the round before conversions (min)
             x.MISC[1] = XT;  // first candidate that lost its line (min)
-            x.MISC[3] = 0;   // set changes at accesses before that end
+            x.MISC[3] = 0;   // set changes in the round
+            x.MISC[7] = 0;   // unconverted candidates of the round
+            x.MISC[8] = XT;  // end by a Lemire rejection
+            x.MISC[9] = XT;  // end by a full change list
         }
         __syncthreads();
         int32_t dp = 0, cp = NEG;  // earlier warps, composed
-        for (int w = 0; w < wid; w++) sat_compose(x.W[w * 8 + 0], x.W[w * 8 + 1], dp, cp);
-        sat_compose(dp, cp, de, ce);  // exclusive prefix at this thread
-        const int32_t ni = max(nsafe + de, ce);   // safe lines seen by this access
-        const bool sel = miss && ni >= 1;         // evicts (else bypass)
-        const bool dr = miss && ni >= 2;          // consumes a draw (integers(1) draws nothing)
+        for (int w = 0; w < wid; w++) {
+            int32_t wd = x.W[w * 8 + 0], wc = x.W[w * 8 + 1];
+            sat_compose(dp, cp, wd, wc);
+            dp = wd;
+            cp = wc;
+        }
+        sat_compose(dp, cp, de, ce);            // exclusive prefix at this thread
+        const int32_t ni = max(nsafe + de, ce);  // safe lines seen by this access
+        const bool sel = miss && ni >= 1;        // evicts (else bypass)
+        const bool dr = miss && ni >= 2;         // consumes a draw (integers(1) draws nothing)
         const bool chg = valid && (cls == C_ADD || (cls == C_MU && sel));
         const unsigned bdr = __ballot_sync(0xffffffffu, dr);
         const unsigned bsel = __ballot_sync(0xffffffffu, sel);
@@ -455,112 +531,146 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             uint32_t left = (uint32_t)m;
             if (left < (uint32_t)ni) {
                 const uint32_t thr = (0u - (uint32_t)ni) % (uint32_t)ni;
-                while (left < thr) {  // Lemire rejection: the round ends here
+                while (left < thr) {  // Lemire rejection: the round ends after this access
                     extra++;
                     m = (uint64_t)get_half(x, a, k + extra, kfill) * (uint32_t)ni;
                     left = (uint32_t)m;
                 }
             }
             r = (uint32_t)(m >> 32);
-            if (extra) atomicMin(&x.MISC[0], t + 1);
-        }
-        if (chg && pchg == XP_MAX_CHG) atomicMin(&x.MISC[0], t);  // change list full
-        // ---------------- C: select in the round-start set
-        const uint32_t total = x.SUPP[ns];
-        int32_t cur = -1, ex = 0;
-        if (sel) {
-            if (r < total) {
-                const int64_t g = locate(x, r, total);
-                const uint32_t rr = r - pb(x, g);
-                const uint4* src = reinterpret_cast<const uint4*>(a.safe_bits + g * 32);
-                uint32_t wv[32];
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const uint4 v = __ldcg(src + q);
-                    wv[4 * q] = v.x;
-                    wv[4 * q + 1] = v.y;
-                    wv[4 * q + 2] = v.z;
-                    wv[4 * q + 3] = v.w;
-                    uint32_t* dst = &x.ROWS[t * 32 + ((q ^ (t & 7)) << 2)];
-                    dst[0] = v.x;
-                    dst[1] = v.y;
-                    dst[2] = v.z;
-                    dst[3] = v.w;
-                }
-                x.ROWBLK[t] = (int32_t)g;
-                uint32_t acc = 0, accb = 0, wsel = 0;
-                int found = 0;
-                bool got = false;
-#pragma unroll
-                for (int q = 0; q < 32; q++) {
-                    const uint32_t cq = __popc(wv[q]);
-                    const bool h = !got && acc + cq > rr;
-                    if (h) {
-                        found = q;
-                        accb = acc;
-                        wsel = wv[q];
-                        got = true;
-                    }
-                    acc += cq;
-                }
-                cur = (int32_t)(g * 1024 + found * 32 + __fns(wsel, 0, (int)(rr - accb) + 1));
-            } else {
-                cur = (int32_t)a.L;
-                ex = (int32_t)(r - total);
+            if (extra) {
+                atomicMin(&x.MISC[0], t + 1);
+                atomicMin(&x.MISC[8], t + 1);
             }
+        }
+        if (chg && pchg == XP_MAX_CHG) {  // change list full
+            atomicMin(&x.MISC[0], t);
+            atomicMin(&x.MISC[9], t);
         }
         __syncthreads();
         const int Epre0 = x.MISC[0];
         const int Epre = (int)((n - pos) < Epre0 ? (n - pos) : Epre0);
-        // ---------------- D: the round's set changes, finalised in order
-        if (chg && t < Epre) {
-            x.CSLOT[pchg] = cls == C_ADD ? s : cur;
+        const bool in = t < Epre;
+        // ---------------- C: T = start set + the round's ADD lines; the start-of-T answers
+        if (chg && in) {
             x.CTYPE[pchg] = cls == C_ADD ? 1 : -1;
-            x.CLANE[pchg] = t;
-            if (cls == C_MU) x.ANS[pchg] = ex;  // (scratch: the MU's excess)
             atomicMax(&x.MISC[3], pchg + 1);
+            if (cls == C_ADD) {
+                x.CSLOT[pchg] = s;
+                atomicOr(&a.safe_bits[s >> 5], 1u << (s & 31));
+                atomicAdd(&x.CNT[s >> 10], 1u);
+                atomicOr(&x.TOUCH[s >> 20], 1u << ((s >> 15) & 31));
+            }
+        }
+        if (valid && in && cls == C_CAND && !conv) {
+            const int k = atomicAdd(&x.MISC[7], 1);
+            x.CANL[k] = t;
+            x.CANS[k] = s;
         }
         __syncthreads();
+        rebuild(x, t);
         const int nchg = x.MISC[3];
-        if (wid == 0) {
-            int32_t ucur = -1, uex = 0, uty = 0, urow = 0;
-            if (lane < nchg) {
-                ucur = x.CSLOT[lane];
-                uty = x.CTYPE[lane];
-                urow = x.CLANE[lane];
-                uex = uty < 0 ? x.ANS[lane] : 0;
+        const uint32_t total = x.SUPP[ns];
+        Blk B;
+        B.g = -1;
+        B.row = x.ROWS + t * 32;
+        B.sw = t & 7;
+        int32_t cur = -1;
+        if (sel && in) cur = sel_T(x, r, total, B);
+        if (chg && in && cls == C_MU) x.CSLOT[pchg] = cur;
+        // ---------------- D: the MU lines, to a fixed point (Jacobi over the
+        // triangular system: pass k makes the first k final; usually 2 passes)
+        const unsigned long long mine = pchg >= 64 ? ~0ull : ((1ull << pchg) - 1ull);
+        for (int pass = 0; pass <= XP_MAX_CHG + 1; pass++) {
+            __syncthreads();
+            // sort the change lines (rank sort), then the prefix masks
+            {  // rank of change e = t / 8 among the changes of slice t % 8
+                const int e = t >> 3, part = t & 7;
+                const int32_t v = e < nchg ? x.CSLOT[e] : 0;
+                int rk = 0;
+                if (e < nchg)
+                    for (int j = part * 8; j < part * 8 + 8 && j < nchg; j++) {
+                        const int32_t u = x.CSLOT[j];
+                        rk += (u < v || (u == v && j < e)) ? 1 : 0;
+                    }
+                rk += __shfl_xor_sync(0xffffffffu, rk, 1);
+                rk += __shfl_xor_sync(0xffffffffu, rk, 2);
+                rk += __shfl_xor_sync(0xffffffffu, rk, 4);
+                if (e < nchg && part == 0) {
+                    x.SS[rk] = v;
+                    x.SIDX[rk] = e;
+                }
             }
-            for (int i = 0; i < nchg; i++) {
-                const int32_t ui = __shfl_sync(0xffffffffu, ucur, i);
-                const int32_t ti = __shfl_sync(0xffffffffu, uty, i);
-                if (lane == i) x.CSLOT[i] = ucur;  // final
-                __syncwarp();
-                if (lane > i && lane < nchg && uty < 0)
-                    apply_change(x, urow, ui, ti, ucur, uex, i + 1);
-                __syncwarp();
+            if (t == 0) x.MISC[10] = 0;
+            __syncthreads();
+            if (wid == 0) {
+                unsigned long long b0 = 0, b1 = 0;
+                if (2 * lane < nchg) b0 = 1ull << x.SIDX[2 * lane];
+                if (2 * lane + 1 < nchg) b1 = 1ull << x.SIDX[2 * lane + 1];
+                unsigned long long inc = b0 | b1;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc |= u;
+                }
+                const unsigned long long ex = inc & ~(b0 | b1);
+                // PM[k] = lines of the k lowest: PM[2l] = ex, PM[2l+1] = ex | b0
+                if (2 * lane <= nchg) x.PM[2 * lane] = ex;
+                if (2 * lane + 1 <= nchg) x.PM[2 * lane + 1] = ex | b0;
+                if (lane == 31 && nchg == 64) x.PM[64] = inc;
+                // ADD mask
+                const unsigned a0 = __ballot_sync(0xffffffffu, lane < nchg && x.CTYPE[lane] > 0);
+                const unsigned a1 =
+                    __ballot_sync(0xffffffffu, lane + 32 < nchg && x.CTYPE[lane + 32] > 0);
+                if (lane == 0) {
+                    x.MISC[11] = (int32_t)a0;
+                    x.MISC[12] = (int32_t)a1;
+                }
+            }
+            __syncthreads();
+            const unsigned long long addm =
+                (unsigned long long)(uint32_t)x.MISC[11] |
+                ((unsigned long long)(uint32_t)x.MISC[12] << 32);
+            const unsigned long long allm = nchg >= 64 ? ~0ull : ((1ull << nchg) - 1ull);
+            const unsigned long long holes = (addm & ~mine & allm) | (~addm & mine & allm);
+            if (chg && in && cls == C_MU) {
+                const int32_t y = resolve(x, r, holes, nchg, total, B);
+                if (y != x.CSLOT[pchg]) {
+                    x.CSLOT[pchg] = y;
+                    x.MISC[10] = 1;
+                }
+                cur = y;
+            }
+            __syncthreads();
+            if (!x.MISC[10]) {
+                // ---------------- E: every other eviction, against the final changes
+                if (sel && in && cls != C_MU) cur = resolve(x, r, holes, nchg, total, B);
+                break;
             }
         }
-        __syncthreads();
-        // ---------------- E: every other eviction moves past the final changes
-        if (sel && t < Epre) {
-            if (chg) {
-                cur = x.CSLOT[pchg];
-            } else {
-                for (int i = 0; i < nchg && x.CLANE[i] < t; i++)
-                    apply_change(x, t, x.CSLOT[i], x.CTYPE[i], cur, ex, i + 1);
-            }
-        }
-        x.ANS[t] = (sel && t < Epre) ? cur : -1;
+        x.ANS[t] = (sel && in) ? cur : -1;
         __syncthreads();
         // ---------------- F: a candidate whose line an earlier eviction took
-        if (valid && t < Epre && cls == C_CAND && !conv) {
-            bool taken = false;
-            for (int j = 0; j < t && !taken; j++) taken = x.ANS[j] == s;
-            for (int j = 0; j < prevE && !taken; j++) taken = x.PANS[j] == s;
-            if (taken) atomicMin(&x.MISC[1], t);
+        // (each access checks its own answer of this and the previous round
+        // against the round's few candidates)
+        {
+            const int nc = x.MISC[7];
+            const int32_t my = x.ANS[t], mine_prev = x.PANS[t];
+            for (int k = 0; k < nc; k++) {
+                const int32_t cl = x.CANL[k], cs = x.CANS[k];
+                if ((my == cs && t < cl) || mine_prev == cs) atomicMin(&x.MISC[1], cl);
+            }
         }
         __syncthreads();
         const int E = Epre < x.MISC[1] ? Epre : x.MISC[1];
+        if (t == 0) {
+            st_rounds++;
+            if (E < n - pos && E < XT) {
+                if (E == x.MISC[1]) st_conv++;
+                else if (E == x.MISC[8]) st_rej++;
+                else if (E == x.MISC[9]) st_chg++;
+            }
+        }
         if (t == E && E < Epre) x.CONV[cidx >> 5] |= 1u << (cidx & 31);  // (only this lane writes)
         // ---------------- G: commit the accesses [pos, pos + E)
         if (pend_cidx >= 0) atomicOr(&x.CONV[pend_cidx >> 5], 1u << (pend_cidx & 31));
@@ -587,69 +697,51 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             a.kind[p] = (int8_t)kd;
             a.line[p] = ln;
         }
-        // the set changes of the committed accesses: bitmap and prefix tables
-        int ncommit = 0;
-        for (int i = 0; i < nchg; i++) {
-            if (x.CLANE[i] >= E) break;
-            ncommit++;
-        }
-        for (int i = 0; i < ncommit; i++) {
-            const int32_t u = x.CSLOT[i];
-            const int ty = x.CTYPE[i];
-            const int64_t b = u >> 10, sb = b >> 5;
-            if (t == 0) {
-                if (ty > 0) atomicOr(&a.safe_bits[u >> 5], 1u << (u & 31));
-                else atomicAnd(&a.safe_bits[u >> 5], ~(1u << (u & 31)));
-                x.CNT[b] += (uint32_t)ty;
+        // committed MU lines leave T; ADD lines of accesses past the end return
+        {
+            int32_t off = -1;
+            if (t < E && chg && cls == C_MU) off = cur;
+            if (t >= E && in && chg && cls == C_ADD) off = s;
+            if (off >= 0) {
+                atomicAnd(&a.safe_bits[off >> 5], ~(1u << (off & 31)));
+                atomicSub(&x.CNT[off >> 10], 1u);
+                atomicOr(&x.TOUCH[off >> 20], 1u << ((off >> 15) & 31));
             }
-            if (t < 32 && t > (int)(b & 31) && (sb << 5) + t < nb) x.BLKP[(sb << 5) + t] += (uint32_t)ty;
-            for (int64_t q = t; q <= ns; q += XT)
-                if (q > sb) x.SUPP[q] += (uint32_t)ty;
         }
         // state after the last committed access
         if (t == E - 1) {
-            x.MISC[4] = max(ni + d, c);           // safe count after it
+            x.MISC[4] = max(ni + d, c);              // safe count after it
             x.MISC[5] = pdr + (dr ? 1 + extra : 0);  // halves consumed through it
-            x.MISC[6] = psel + (sel ? 1 : 0);       // log entries through it
+            x.MISC[6] = psel + (sel ? 1 : 0);        // log entries through it
         }
         __syncthreads();
+        rebuild(x, t);
         if (E > 0) {
             nsafe = x.MISC[4];
             kpos += x.MISC[5];
             nlog += x.MISC[6];
         }
         x.PANS[t] = t < E ? x.ANS[t] : -1;
-        x.ROWBLK[t] = -1;  // (the bitmap moved on; private copies are stale)
-        prevE = E;
         pos += E;
         // refill the rings past the consumed prefix
         {
             const int64_t etop = (pos + RING) < n ? pos + RING : n;
             for (int64_t i = efill + t; i < etop; i += XT) {
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                 (uint32_t)__cvta_generic_to_shared(&x.REV[i % RING])),
-                             "l"(a.ev + i));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                 (uint32_t)__cvta_generic_to_shared(&x.RCL[i % RING])),
-                             "l"(a.xcls + i));
+                stage(&x.REV[i % RING], a.ev + i);
+                stage(&x.RCL[i % RING], a.xcls + i);
             }
-            efill = etop;
+            efill = etop > efill ? etop : efill;
             const int64_t ktop = (kpos + HRING) < a.hcap ? kpos + HRING : a.hcap;
-            for (int64_t i = kfill + t; i < ktop; i += XT)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                                 (uint32_t)__cvta_generic_to_shared(&x.RH[i % HRING])),
-                             "l"(a.H + i));
+            for (int64_t i = kfill + t; i < ktop; i += XT) stage(&x.RH[i % HRING], a.H + i);
             kfill = ktop > kfill ? ktop : kfill;
             asm volatile("cp.async.commit_group;");
         }
     }
     asm volatile("cp.async.wait_group 0;");
-    if (pend_cidx >= 0) atomicOr(&x.CONV[pend_cidx >> 5], 1u << (pend_cidx & 31));
     __syncthreads();
     // write back: block / superblock counts, counters, generator state
     for (int64_t i = t; i < nb; i += XT) a.blk_cnt[i] = x.CNT[i];
-    for (int64_t sb = t; sb < ns; sb += XT) a.sup_cnt[sb] = x.SUPP[sb + 1] - x.SUPP[sb];
-    // block reduction of the counters
+    for (int64_t sb = t; sb < ns; sb += XT) a.sup_cnt[sb] = x.STOT[sb];
     hits = __reduce_add_sync(0xffffffffu, (unsigned)hits);
     misses = __reduce_add_sync(0xffffffffu, (unsigned)misses);
     byp = __reduce_add_sync(0xffffffffu, (unsigned)byp);
@@ -681,6 +773,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         m->safe_count = nsafe;
         a.svc->n_log = nlog;
         a.svc->xp_done = 1;
+        a.svc->xp_stats[0] = st_rounds;
+        a.svc->xp_stats[1] = st_rej;
+        a.svc->xp_stats[2] = st_chg;
+        a.svc->xp_stats[3] = st_conv;
     }
 }
 
@@ -704,8 +800,9 @@ int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
 // shared memory of k_exact_par for a cache of L lines
 size_t gids_xp_smem_bytes(int64_t L) {
     const int64_t nb = (L + 1023) / 1024, ns = (nb + 31) / 32;
-    return sizeof(uint32_t) * (size_t)(XT * 32 + 2 * RING + HRING + 2 * nb + ns + 1 +
-                                       (GIDS_XP_CAND_CAP + 31) / 32 + 3 * XT + 3 * XP_MAX_CHG +
+    return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * RING + HRING + 2 * nb +
+                                       2 * ns + 1 + (ns + 31) / 32 + XT * 32 +
+                                       (GIDS_XP_CAND_CAP + 31) / 32 + 4 * XT + 4 * XP_MAX_CHG +
                                        XW * 8 + 16);
 }
 

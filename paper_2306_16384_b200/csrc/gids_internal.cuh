@@ -142,6 +142,7 @@ struct ServeCounters {
     int64_t shard_local, shard_remote;  // sharded-table mode: rows from own / peer HBM
     int64_t n_cand;        // resident SafeToEvict nodes of the batch (exact_par.cu)
     int64_t xp_done;       // the batch was decided by k_exact_par
+    int64_t xp_stats[4];   // its rounds; rounds ended by a rejection / full change list / lost line
 };
 
 struct CacheMeta {  // persistent cache counters (CacheState)
@@ -203,6 +204,7 @@ struct gids_handle {
     int64_t xp_hcap;
     bool xp_enabled;       // GIDS_EXACT_PAR=0 keeps every batch on k_exact_seq
     int64_t xp_batches;    // served batches k_exact_par decided
+    int64_t xp_stats[4];   // their ServeCounters.xp_stats, summed
     bool counts_read;      // the last serve's counts were read once already
 
     // sampler workspace (HBM)

@@ -1,0 +1,102 @@
+"""k_exact_par -- the reference eviction policy (cache.py:144-180) for a full
+cache, decided by a whole CTA (csrc/exact_par.cu) -- bit for bit against the
+oracle's sequential CacheState restatement: per-batch tier counts and
+gathered rows, and at the end the line table (node and LineState of every
+line) and the eviction PCG64 words.  The cases drive every path of the
+kernel: eviction-heavy C4-like batches (candidates losing their lines to
+earlier evictions, Lemire rejections over millions of draws), no window
+(every line SafeToEvict), a starved cache (bypasses, the saturating safe
+count), caches smaller than one 1024-line block or ending in a partial one.
+Each case also checks that the parallel kernel decided the batches (its
+evidence counter), and one case that the sequential warp (GIDS_EXACT_PAR=0)
+produces the same run."""
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+from oracle import oracle as O  # noqa: E402
+from paper_2306_16384_b200 import Dataloader, make_config  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    # C4's ratios at 1/280 scale: every miss evicts, U ~ 3x the cache per batch
+    "evict_heavy": dict(num_nodes=400_000, avg_degree=14.55, fanouts=[15, 10, 5],
+                        batch_size=64, cache_lines=16_384, window_depth=8, batches=8),
+    "no_window": dict(num_nodes=400_000, avg_degree=14.55, fanouts=[15, 10, 5],
+                      batch_size=64, cache_lines=16_384, window_depth=0, batches=6),
+    "starved": dict(num_nodes=50_000, avg_degree=10.0, fanouts=[10, 15], batch_size=256,
+                    cache_lines=3_000, window_depth=8, batches=10),
+    "sub_block": dict(num_nodes=60_000, avg_degree=8.0, fanouts=[8, 8], batch_size=128,
+                      cache_lines=700, window_depth=4, batches=10),
+    "partial_block": dict(num_nodes=1_000_000, avg_degree=12.0, fanouts=[10, 15],
+                          batch_size=1024, cache_lines=100_500, window_depth=8, batches=10),
+}
+
+
+def _run(case: str, env_off: bool = False):
+    c = dict(CASES[case])
+    nb = c.pop("batches")
+    import bench
+    cfg = make_config(dict(degree_model="uniform", feature_dim=16, buffer_fraction=0.10,
+                           consume_rate=0.0, seed=11, gids_generator="device", **c))
+    old = os.environ.get("GIDS_EXACT_PAR")
+    if env_off:
+        os.environ["GIDS_EXACT_PAR"] = "0"
+    try:
+        dl = Dataloader(cfg)
+    finally:
+        if env_off:
+            if old is None:
+                del os.environ["GIDS_EXACT_PAR"]
+            else:
+                os.environ["GIDS_EXACT_PAR"] = old
+    g, buf = bench.host_device_shape(cfg)
+    r = bench.oracle_inputs(cfg, g, dl.features.table, buf)
+    ld = O.OracleLoader(g.indptr, g.indices, dl.features.table, buf, r["batches"], cfg.fanouts,
+                        r["sampler_words"], r["evict_words"], cfg.resolved_cache_lines(),
+                        cfg.window_depth, r["base_threshold"])
+    tiers = []
+    for b in range(nb):
+        o = ld.next_batch()
+        mb, rows, st = dl.next_batch()
+        got = [st.cache_hits, st.cpu_buffer_hits, st.ssd_accesses, st.bypasses]
+        assert got == o["tiers"].tolist(), (case, b, got, o["tiers"].tolist())
+        assert np.array_equal(rows.cpu().numpy(), o["rows"]), (case, b)
+        tiers.append(got)
+    node, state = dl.cache.lines()
+    onode, ostate = ld.cache.lines_snapshot()
+    assert np.array_equal(node, onode), case
+    assert np.array_equal(state, ostate), case
+    assert dl.cache.eviction_rng_words().tolist() == ld.cache.rng_words().tolist(), case
+    os_ = ld.cache.stats()
+    cc = dl.cache
+    assert [cc.hits, cc.misses, cc.bypasses, cc.evictions] == \
+        [os_["hits"], os_["misses"], os_["bypasses"], os_["evictions"]], case
+    par = dl._h.exact_par_batches()
+    dl.close()
+    return tiers, par, os_
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_exact_par_matches_oracle(case):
+    tiers, par, st = _run(case)
+    assert par > 0, "the CTA-parallel kernel never decided a batch"
+    if case in ("evict_heavy", "no_window", "partial_block"):
+        assert st["evictions"] > 0
+    if case == "starved":
+        assert st["bypasses"] > 0
+
+
+def test_exact_par_equals_sequential_warp():
+    a, par_a, _ = _run("evict_heavy")
+    b, par_b, _ = _run("evict_heavy", env_off=True)
+    assert a == b
+    assert par_a > 0 and par_b == 0
