@@ -285,9 +285,11 @@ GIDS_API int64_t gids_launch_count(gids_handle* h);
  * kernel for a full cache (csrc/exact_par.cu) rather than the sequential warp,
  * counted as gids_serve_counts reads them (evidence counter). */
 GIDS_API int64_t gids_exact_par_batches(gids_handle* h);
-/* Over those batches: rounds of 256 accesses, and rounds ended early by a
- * Lemire rejection / a full change list / a candidate losing its line. */
-GIDS_API int gids_exact_par_stats(gids_handle* h, int64_t out[4]);
+/* Over those batches: rounds of accesses, rounds ended early by a Lemire
+ * rejection / a full change list / a candidate losing its line, then the
+ * kernel's SM cycles per phase (draws, T tables, selects, candidates, commit,
+ * re-prefix, staging) and its fixed-point passes (diagnostics). */
+GIDS_API int gids_exact_par_stats(gids_handle* h, int64_t out[12]);
 
 #ifdef __cplusplus
 }

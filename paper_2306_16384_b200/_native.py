@@ -364,9 +364,11 @@ class Handle:
         return int(lib().gids_exact_par_batches(self.h))
 
     def exact_par_stats(self) -> dict:
-        out = np.zeros(4, np.int64)
+        out = np.zeros(12, np.int64)
         check(lib().gids_exact_par_stats(self.h, out.ctypes.data), "exact_par_stats")
-        return dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line"),
+        return dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line",
+                         "cyc_draws", "cyc_tables", "cyc_select", "cyc_fixpoint",
+                         "cyc_resolve", "cyc_candidates", "cyc_commit", "fixpoint_passes"),
                         out.tolist()), batches=self.exact_par_batches())
 
 

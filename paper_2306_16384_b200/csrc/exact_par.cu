@@ -141,7 +141,8 @@ struct Xs {
     uint32_t* STOT;   // [ns] superblock totals
     uint32_t* TOUCH;  // [(ns+31)/32] superblocks whose counts changed
     uint32_t* CONV;   // [cand_cap/32] candidates whose line was taken
-    uint32_t* ROWS;   // [XT*32] each access's block of T
+    uint32_t* GCNT;   // [2*nb] lines of T per 128-line group, one byte each
+    int32_t* FIN;     // [XP_MAX_CHG] MU lines found by the current pass
     uint32_t* REV;    // [RING]
     uint32_t* RCL;    // [RING]
     uint32_t* RH;     // [HRING]
@@ -162,19 +163,21 @@ struct Xs {
 
 __device__ __forceinline__ uint32_t pb(const Xs& x, int64_t g) { return x.SUPP[g >> 5] + x.BLKP[g]; }
 
-// block holding the r-th line of T (r < total)
+// block holding the r-th line of T (r < total): interpolated guess, then
+// steps sized by the mean block count (float arithmetic: only a guess)
 __device__ int64_t locate(const Xs& x, uint32_t r, uint32_t total) {
     const int64_t nb = x.nb;
-    const uint32_t avg = total / (uint32_t)nb > 0 ? total / (uint32_t)nb : 1u;
-    int64_t g = (int64_t)(((uint64_t)r * (uint64_t)nb) / total);
+    const float per = __fdividef((float)nb, (float)total);  // blocks per line
+    int64_t g = (int64_t)((float)r * per);
     if (g >= nb) g = nb - 1;
+    if (g < 0) g = 0;
     for (int it = 0; it < 6; it++) {
         const uint32_t base = pb(x, g), c = x.CNT[g];
         if (r < base) {
-            int64_t st = (base - r) / avg + 1;
+            const int64_t st = (int64_t)((float)(base - r) * per) + 1;
             g = g - st < 0 ? 0 : g - st;
         } else if (r >= base + c) {
-            int64_t st = (r - base - c) / avg + 1;
+            const int64_t st = (int64_t)((float)(r - base - c) * per) + 1;
             g = g + st >= nb ? nb - 1 : g + st;
         } else {
             return g;
@@ -187,29 +190,6 @@ __device__ int64_t locate(const Xs& x, uint32_t r, uint32_t total) {
         else hi = mid - 1;
     }
     return lo;
-}
-
-// a 1024-line block of T held by one access: its 32 words in the access's
-// shared-memory row (16-B chunks swizzled by lane), the exclusive popcount
-// prefix of its eight 4-word groups in registers
-struct Blk {
-    int64_t g;
-    uint32_t gp[8];
-    uint32_t* row;
-    int sw;  // swizzle (thread & 7)
-};
-
-__device__ __forceinline__ void load_blk(const Xs& x, Blk& B, int64_t g) {
-    const uint4* src = reinterpret_cast<const uint4*>(x.gbits + g * 32);
-    uint32_t run = 0;
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-        const uint4 v = __ldcg(src + q);
-        *reinterpret_cast<uint4*>(B.row + ((q ^ B.sw) << 2)) = v;
-        B.gp[q] = run;
-        run += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-    }
-    B.g = g;
 }
 
 // position of the k-th set bit of w (k < popc(w))
@@ -227,48 +207,75 @@ __device__ __forceinline__ int bit_select(uint32_t w, uint32_t k) {
     return pos;
 }
 
-// the rr-th set bit of the held block
-__device__ __forceinline__ int32_t sel_blk(const Blk& B, uint32_t rr) {
-    int grp = 0;
-    uint32_t base = 0;
-#pragma unroll
-    for (int j = 1; j < 8; j++)
-        if (B.gp[j] <= rr) {
-            grp = j;
-            base = B.gp[j];
-        }
-    const uint4 w4 = *reinterpret_cast<const uint4*>(B.row + ((grp ^ B.sw) << 2));
-    uint32_t k = rr - base, w = w4.x;
+// the 128-line group of T an access last selected in: its four bitmap words
+// (one 16-B load from the L2-resident bitmap), rank base and count
+struct Grp {
+    int64_t g;      // block, -1 none
+    int grp;        // group within the block
+    uint32_t base, cnt;
+    uint4 w;
+};
+
+// the k-th set bit of the held group
+__device__ __forceinline__ int32_t sel_grp(const Grp& G, uint32_t k) {
+    uint32_t w = G.w.x;
     int wi = 0;
-    uint32_t c = __popc(w4.x);
+    uint32_t c = __popc(G.w.x);
     if (k >= c) {
         k -= c;
         wi = 1;
-        w = w4.y;
-        c = __popc(w4.y);
+        w = G.w.y;
+        c = __popc(G.w.y);
         if (k >= c) {
             k -= c;
             wi = 2;
-            w = w4.z;
-            c = __popc(w4.z);
+            w = G.w.z;
+            c = __popc(G.w.z);
             if (k >= c) {
                 k -= c;
                 wi = 3;
-                w = w4.w;
+                w = G.w.w;
             }
         }
     }
-    return grp * 128 + wi * 32 + bit_select(w, k);
+    return (int32_t)(G.g * 1024) + G.grp * 128 + wi * 32 + bit_select(w, k);
 }
 
-// the q-th line of T (the held block is reused when it covers q)
-__device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total, Blk& B) {
-    uint32_t base = B.g >= 0 ? pb(x, B.g) : 0u;
-    if (B.g < 0 || q < base || q >= base + x.CNT[B.g]) {
-        load_blk(x, B, locate(x, q, total));
-        base = pb(x, B.g);
+// the q-th line of T (the held group, then its block, are reused when they cover q)
+__device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
+    if (G.g >= 0 && q - G.base < G.cnt) return sel_grp(G, q - G.base);
+    int64_t g = -1;
+    uint32_t base = 0;
+    if (G.g >= 0) {
+        base = pb(x, G.g);
+        if (q >= base && q < base + x.CNT[G.g]) g = G.g;
     }
-    return (int32_t)(B.g * 1024) + sel_blk(B, q - base);
+    if (g < 0) {
+        g = locate(x, q, total);
+        base = pb(x, g);
+    }
+    const uint2 cc = *reinterpret_cast<const uint2*>(x.GCNT + 2 * g);
+    const uint32_t rr = q - base;
+    uint32_t acc = 0, accb = 0, cg = 0;
+    int grp = 0;
+    bool got = false;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+        const uint32_t cj = ((j < 4 ? cc.x : cc.y) >> ((j & 3) * 8)) & 0xffu;
+        if (!got && acc + cj > rr) {
+            grp = j;
+            accb = acc;
+            cg = cj;
+            got = true;
+        }
+        acc += cj;
+    }
+    G.g = g;
+    G.grp = grp;
+    G.base = base + accb;
+    G.cnt = cg;
+    G.w = __ldcg(reinterpret_cast<const uint4*>(x.gbits + g * 32 + grp * 4));
+    return sel_grp(G, q - G.base);
 }
 
 // lines among the round's changes <= y
@@ -285,9 +292,10 @@ __device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
 // the r-th line of T minus `holes` (a mask over the change list): the least
 // fixed point of q = r + #holes(<= sel_T(q)), reached from q = r
 __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned long long holes,
-                                           int m, uint32_t total, Blk& B) {
+                                           int m, uint32_t total, Grp& B, int32_t& ylo) {
     uint32_t q = r;
     int32_t y = sel_T(x, q, total, B);
+    ylo = y;
     if (!holes) return y;
     for (int it = 0; it <= XP_MAX_CHG; it++) {
         const uint32_t q2 = r + (uint32_t)__popcll(x.PM[count_le(x, m, y)] & holes);
@@ -302,30 +310,21 @@ __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned lon
 __device__ void rebuild(const Xs& x, int t) {
     const int lane = t & 31, wid = t >> 5;
     const int nsw = (int)((x.ns + 31) >> 5);
-    int k = 0;
-    for (int w32 = 0; w32 < nsw; w32++) {
-        uint32_t bits = x.TOUCH[w32];
-        while (bits) {
-            const int sb = w32 * 32 + __ffs(bits) - 1;
-            bits &= bits - 1;
-            if (sb >= x.ns) break;
-            if ((k % XW) == wid) {
-                const int64_t blk = (int64_t)sb * 32 + lane;
-                const uint32_t c = blk < x.nb ? x.CNT[blk] : 0u;
-                uint32_t inc = c;
+    for (int64_t sb = wid; sb < x.ns; sb += XW) {
+        if (!((x.TOUCH[sb >> 5] >> (sb & 31)) & 1u)) continue;
+        const int64_t blk = sb * 32 + lane;
+        const uint32_t c = blk < x.nb ? x.CNT[blk] : 0u;
+        uint32_t inc = c;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += u;
-                }
-                if (blk < x.nb) x.BLKP[blk] = inc - c;
-                if (lane == 31) x.STOT[sb] = inc;
-            }
-            k++;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
         }
+        if (blk < x.nb) x.BLKP[blk] = inc - c;
+        if (lane == 31) x.STOT[sb] = inc;
     }
     __syncthreads();
-    if (wid == 0 && k > 0) {  // SUPP = exclusive prefix of STOT
+    if (wid == 0) {  // SUPP = exclusive prefix of STOT
         const int per = (int)((x.ns + 31) >> 5);
         uint32_t loc = 0;
         for (int i = 0; i < per; i++) {
@@ -386,8 +385,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         uint32_t* p = smem;
         x.PM = reinterpret_cast<unsigned long long*>(p);
         p += 2 * (XP_MAX_CHG + 2);
-        x.ROWS = p;
-        p += XT * 32;
+        x.GCNT = p;
+        p += 2 * x.nb;
+        x.FIN = reinterpret_cast<int32_t*>(p);
+        p += XP_MAX_CHG;
         x.REV = p;
         p += RING;
         x.RCL = p;
@@ -428,6 +429,16 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     }
     const int64_t n = a.n, nb = x.nb, ns = x.ns;
     for (int64_t i = t; i < nb; i += XT) x.CNT[i] = a.blk_cnt[i];
+    for (int64_t i = t; i < 2 * nb; i += XT) {  // four 128-line group counts per word
+        const uint4* src = reinterpret_cast<const uint4*>(a.safe_bits + i * 16);
+        uint32_t packed = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint4 v = __ldcg(src + q);
+            packed |= (uint32_t)(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w)) << (8 * q);
+        }
+        x.GCNT[i] = packed;
+    }
     for (int64_t i = t; i < (a.cand_cap + 31) / 32; i += XT) x.CONV[i] = 0u;
     for (int64_t i = t; i < (ns + 31) / 32; i += XT) x.TOUCH[i] = ~0u;  // (all: first prefix)
     x.PANS[t] = -1;
@@ -450,10 +461,15 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     int32_t pend_cidx = -1;  // cand_of_slot of this thread's last committed eviction
     int64_t hits = 0, misses = 0, byp = 0;
     int64_t st_rounds = 0, st_rej = 0, st_chg = 0, st_conv = 0;  // round ends (thread 0)
+    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // cycles per phase, D passes (thread 0)
+    long long tc = clock64();
 
     while (pos < n) {
         asm volatile("cp.async.wait_group %0;" ::"n"(RING_LAG));
         __syncthreads();
+        long long tn = clock64();
+        prof[6] += tn - tc;  // (ring wait + refill: with G)
+        tc = tn;
         // ---------------- A: classify, saturating safe-count prefix, draw prefix
         const int64_t p = pos + t;
         const bool valid = p < n;
@@ -548,6 +564,11 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             atomicMin(&x.MISC[9], t);
         }
         __syncthreads();
+        if (t == 0) {
+            tn = clock64();
+            prof[0] += tn - tc;  // A + B
+            tc = tn;
+        }
         const int Epre0 = x.MISC[0];
         const int Epre = (int)((n - pos) < Epre0 ? (n - pos) : Epre0);
         const bool in = t < Epre;
@@ -559,6 +580,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 x.CSLOT[pchg] = s;
                 atomicOr(&a.safe_bits[s >> 5], 1u << (s & 31));
                 atomicAdd(&x.CNT[s >> 10], 1u);
+                atomicAdd(&x.GCNT[s >> 9], 1u << (((s >> 7) & 3) * 8));
                 atomicOr(&x.TOUCH[s >> 20], 1u << ((s >> 15) & 31));
             }
         }
@@ -569,17 +591,32 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         }
         __syncthreads();
         rebuild(x, t);
+        if (t == 0) {
+            tn = clock64();
+            prof[1] += tn - tc;  // C: T tables
+            tc = tn;
+        }
         const int nchg = x.MISC[3];
         const uint32_t total = x.SUPP[ns];
-        Blk B;
+        Grp B;
         B.g = -1;
-        B.row = x.ROWS + t * 32;
-        B.sw = t & 7;
-        int32_t cur = -1;
-        if (sel && in) cur = sel_T(x, r, total, B);
-        if (chg && in && cls == C_MU) x.CSLOT[pchg] = cur;
-        // ---------------- D: the MU lines, to a fixed point (Jacobi over the
-        // triangular system: pass k makes the first k final; usually 2 passes)
+        int32_t cur = -1, ylo = -1;
+        if (chg && in && cls == C_MU) {  // first approximation: the no-hole line
+            cur = sel_T(x, r, total, B);
+            x.CSLOT[pchg] = cur;
+        }
+        __syncthreads();
+        if (t == 0) {
+            tn = clock64();
+            prof[2] += tn - tc;  // C selects
+            tc = tn;
+        }
+        // ---------------- D/E: every eviction resolves against the change list.
+        // The MU lines are themselves answers, so a pass uses the previous
+        // pass's MU lines (the first pass: their no-hole lines); the result is
+        // exact unless, for some access, an earlier MU line moved across the
+        // range of lines its fixed-point iteration looked at -- checked
+        // exactly, and another pass run (rare: the moves are short)
         const unsigned long long mine = pchg >= 64 ? ~0ull : ((1ull << pchg) - 1ull);
         for (int pass = 0; pass <= XP_MAX_CHG + 1; pass++) {
             __syncthreads();
@@ -600,6 +637,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                     x.SS[rk] = v;
                     x.SIDX[rk] = e;
                 }
+                if (e < nchg && part == 1) x.FIN[e] = v;  // (ADD lines are final)
             }
             if (t == 0) x.MISC[10] = 0;
             __syncthreads();
@@ -633,20 +671,32 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 ((unsigned long long)(uint32_t)x.MISC[12] << 32);
             const unsigned long long allm = nchg >= 64 ? ~0ull : ((1ull << nchg) - 1ull);
             const unsigned long long holes = (addm & ~mine & allm) | (~addm & mine & allm);
-            if (chg && in && cls == C_MU) {
-                const int32_t y = resolve(x, r, holes, nchg, total, B);
-                if (y != x.CSLOT[pchg]) {
-                    x.CSLOT[pchg] = y;
-                    x.MISC[10] = 1;
-                }
-                cur = y;
+            if (sel && in) {
+                cur = resolve(x, r, holes, nchg, total, B, ylo);
+                if (chg && cls == C_MU) x.FIN[pchg] = cur;
             }
             __syncthreads();
-            if (!x.MISC[10]) {
-                // ---------------- E: every other eviction, against the final changes
-                if (sel && in && cls != C_MU) cur = resolve(x, r, holes, nchg, total, B);
-                break;
+            if (t == 0) prof[7]++;
+            // the earlier MU lines this access counted, used vs found
+            if (sel && in) {
+                unsigned long long mu = ~addm & mine & allm;
+                bool moved = false;
+                while (mu) {
+                    const int i = __ffsll((long long)mu) - 1;
+                    mu &= mu - 1;
+                    const int32_t u0 = x.CSLOT[i], u1 = x.FIN[i];
+                    if (u0 != u1 && max(u0, u1) >= ylo && min(u0, u1) <= cur) moved = true;
+                }
+                if (moved) x.MISC[10] = 1;
             }
+            __syncthreads();
+            if (!x.MISC[10]) break;
+            if (chg && in && cls == C_MU) x.CSLOT[pchg] = cur;  // next pass
+        }
+        if (t == 0) {
+            tn = clock64();
+            prof[3] += tn - tc;  // D/E passes
+            tc = tn;
         }
         x.ANS[t] = (sel && in) ? cur : -1;
         __syncthreads();
@@ -664,6 +714,9 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         __syncthreads();
         const int E = Epre < x.MISC[1] ? Epre : x.MISC[1];
         if (t == 0) {
+            tn = clock64();
+            prof[5] += tn - tc;  // F
+            tc = tn;
             st_rounds++;
             if (E < n - pos && E < XT) {
                 if (E == x.MISC[1]) st_conv++;
@@ -705,6 +758,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             if (off >= 0) {
                 atomicAnd(&a.safe_bits[off >> 5], ~(1u << (off & 31)));
                 atomicSub(&x.CNT[off >> 10], 1u);
+                atomicSub(&x.GCNT[off >> 9], 1u << (((off >> 7) & 3) * 8));
                 atomicOr(&x.TOUCH[off >> 20], 1u << ((off >> 15) & 31));
             }
         }
@@ -715,7 +769,11 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[6] = psel + (sel ? 1 : 0);        // log entries through it
         }
         __syncthreads();
-        rebuild(x, t);
+        if (t == 0) {
+            tn = clock64();
+            prof[6] += tn - tc;  // G commit (its re-prefix joins the next round's)
+            tc = tn;
+        }
         if (E > 0) {
             nsafe = x.MISC[4];
             kpos += x.MISC[5];
@@ -739,6 +797,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     }
     asm volatile("cp.async.wait_group 0;");
     __syncthreads();
+    rebuild(x, t);  // the last round's commit
     // write back: block / superblock counts, counters, generator state
     for (int64_t i = t; i < nb; i += XT) a.blk_cnt[i] = x.CNT[i];
     for (int64_t sb = t; sb < ns; sb += XT) a.sup_cnt[sb] = x.STOT[sb];
@@ -777,6 +836,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         a.svc->xp_stats[1] = st_rej;
         a.svc->xp_stats[2] = st_chg;
         a.svc->xp_stats[3] = st_conv;
+        for (int i = 0; i < 8; i++) a.svc->xp_prof[i] = prof[i];
     }
 }
 
@@ -801,7 +861,7 @@ int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
 size_t gids_xp_smem_bytes(int64_t L) {
     const int64_t nb = (L + 1023) / 1024, ns = (nb + 31) / 32;
     return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * RING + HRING + 2 * nb +
-                                       2 * ns + 1 + (ns + 31) / 32 + XT * 32 +
+                                       2 * ns + 1 + (ns + 31) / 32 + 2 * nb + XP_MAX_CHG +
                                        (GIDS_XP_CAND_CAP + 31) / 32 + 4 * XT + 4 * XP_MAX_CHG +
                                        XW * 8 + 16);
 }

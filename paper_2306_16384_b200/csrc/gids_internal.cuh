@@ -143,6 +143,7 @@ struct ServeCounters {
     int64_t n_cand;        // resident SafeToEvict nodes of the batch (exact_par.cu)
     int64_t xp_done;       // the batch was decided by k_exact_par
     int64_t xp_stats[4];   // its rounds; rounds ended by a rejection / full change list / lost line
+    int64_t xp_prof[8];    // SM cycles per phase (A+B, C tables, selects+D+E, F, G, G prefix, ring) and D passes
 };
 
 struct CacheMeta {  // persistent cache counters (CacheState)
@@ -204,7 +205,7 @@ struct gids_handle {
     int64_t xp_hcap;
     bool xp_enabled;       // GIDS_EXACT_PAR=0 keeps every batch on k_exact_seq
     int64_t xp_batches;    // served batches k_exact_par decided
-    int64_t xp_stats[4];   // their ServeCounters.xp_stats, summed
+    int64_t xp_stats[12];  // their ServeCounters.xp_stats, xp_prof, summed
     bool counts_read;      // the last serve's counts were read once already
 
     // sampler workspace (HBM)
