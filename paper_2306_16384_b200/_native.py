@@ -367,8 +367,8 @@ class Handle:
         out = np.zeros(12, np.int64)
         check(lib().gids_exact_par_stats(self.h, out.ctypes.data), "exact_par_stats")
         return dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line",
-                         "cyc_draws", "cyc_tables", "cyc_select", "cyc_fixpoint",
-                         "cyc_resolve", "cyc_candidates", "cyc_commit", "fixpoint_passes"),
+                         "cyc_draws", "cyc_tables", "cyc_first_select", "cyc_sort",
+                         "cyc_resolve", "cyc_verify", "cyc_commit", "fixpoint_passes"),
                         out.tolist()), batches=self.exact_par_batches())
 
 

@@ -56,6 +56,8 @@ constexpr int RING = 4096;        // staged accesses (ev, class)
 constexpr int HRING = 4096;       // staged draw halves
 constexpr int RING_LAG = 12;      // commit groups allowed in flight when a round reads
 constexpr int32_t NEG = -(1 << 29);
+constexpr int MOVW = 64;          // moved-line filter: 2048 buckets (lines >> MOVS)
+
 enum { C_STAY = GIDS_XC_STAY, C_ADD = GIDS_XC_ADD, C_CAND = GIDS_XC_CAND, C_M0 = GIDS_XC_M0,
        C_MU = GIDS_XC_MU };
 
@@ -143,6 +145,7 @@ struct Xs {
     uint32_t* CONV;   // [cand_cap/32] candidates whose line was taken
     uint32_t* GCNT;   // [2*nb] lines of T per 128-line group, one byte each
     int32_t* FIN;     // [XP_MAX_CHG] MU lines found by the current pass
+    uint32_t* MOVB;   // [MOVW] 1024-line buckets a moved MU line crossed this pass
     uint32_t* REV;    // [RING]
     uint32_t* RCL;    // [RING]
     uint32_t* RH;     // [HRING]
@@ -241,9 +244,9 @@ __device__ __forceinline__ int32_t sel_grp(const Grp& G, uint32_t k) {
     return (int32_t)(G.g * 1024) + G.grp * 128 + wi * 32 + bit_select(w, k);
 }
 
-// the q-th line of T (the held group, then its block, are reused when they cover q)
-__device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
-    if (G.g >= 0 && q - G.base < G.cnt) return sel_grp(G, q - G.base);
+// hold the 128-line group of T holding rank q (its words are loaded, not
+// waited for: the first use waits)
+__device__ __forceinline__ void find_grp(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
     int64_t g = -1;
     uint32_t base = 0;
     if (G.g >= 0) {
@@ -275,6 +278,11 @@ __device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total
     G.base = base + accb;
     G.cnt = cg;
     G.w = __ldcg(reinterpret_cast<const uint4*>(x.gbits + g * 32 + grp * 4));
+}
+
+// the q-th line of T (the held group is reused when it covers q)
+__device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
+    if (!(G.g >= 0 && q - G.base < G.cnt)) find_grp(x, q, total, G);
     return sel_grp(G, q - G.base);
 }
 
@@ -290,13 +298,24 @@ __device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
 }
 
 // the r-th line of T minus `holes` (a mask over the change list): the least
-// fixed point of q = r + #holes(<= sel_T(q)), reached from q = r
+// fixed point of q = r + #holes(<= sel_T(q)).  Every fixed point lies at or
+// above r + #holes below the block holding T's r-th line (the answer is not
+// below that block), so the iteration starts there -- usually already the
+// answer, one bitmap load.  The hole counts it used: at line lb, and at the
+// lines of [ylo, answer].
 __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned long long holes,
-                                           int m, uint32_t total, Grp& B, int32_t& ylo) {
-    uint32_t q = r;
+                                           int m, uint32_t total, Grp& B, int32_t& lb,
+                                           int32_t& ylo) {
+    if (!holes) {
+        const int32_t y = sel_T(x, r, total, B);
+        ylo = y;
+        lb = -1;
+        return y;
+    }
+    lb = (int32_t)(locate(x, r, total) * 1024) - 1;
+    uint32_t q = r + (lb >= 0 ? (uint32_t)__popcll(x.PM[count_le(x, m, lb)] & holes) : 0u);
     int32_t y = sel_T(x, q, total, B);
     ylo = y;
-    if (!holes) return y;
     for (int it = 0; it <= XP_MAX_CHG; it++) {
         const uint32_t q2 = r + (uint32_t)__popcll(x.PM[count_le(x, m, y)] & holes);
         if (q2 == q) break;
@@ -353,7 +372,7 @@ __device__ void rebuild(const Xs& x, int t) {
 
 __device__ __forceinline__ uint32_t get_half(const Xs& x, const XpArgs& a, int64_t k,
                                              int64_t kfill) {
-    if (k < kfill && k >= kfill - HRING) return x.RH[k % HRING];
+    if (k < kfill && k >= kfill - HRING) return x.RH[k & (HRING - 1)];
     if (k < a.hcap) return __ldcg(a.H + k);
     return half_direct(a.meta, k);
 }
@@ -389,6 +408,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += 2 * x.nb;
         x.FIN = reinterpret_cast<int32_t*>(p);
         p += XP_MAX_CHG;
+        x.MOVB = p;
+        p += MOVW;
         x.REV = p;
         p += RING;
         x.RCL = p;
@@ -447,10 +468,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     int64_t efill = n < RING ? n : RING;
     int64_t kfill = a.hcap < HRING ? a.hcap : HRING;
     for (int64_t i = t; i < efill; i += XT) {
-        stage(&x.REV[i % RING], a.ev + i);
-        stage(&x.RCL[i % RING], a.xcls + i);
+        stage(&x.REV[i & (RING - 1)], a.ev + i);
+        stage(&x.RCL[i & (RING - 1)], a.xcls + i);
     }
-    for (int64_t i = t; i < kfill; i += XT) stage(&x.RH[i % HRING], a.H + i);
+    for (int64_t i = t; i < kfill; i += XT) stage(&x.RH[i & (HRING - 1)], a.H + i);
     asm volatile("cp.async.commit_group;");
     asm volatile("cp.async.wait_group 0;");
     __syncthreads();
@@ -473,8 +494,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // ---------------- A: classify, saturating safe-count prefix, draw prefix
         const int64_t p = pos + t;
         const bool valid = p < n;
-        const uint32_t e = valid ? x.REV[p % RING] : 0u;
-        const uint32_t xc = valid ? x.RCL[p % RING] : 0u;
+        const uint32_t e = valid ? x.REV[p & (RING - 1)] : 0u;
+        const uint32_t xc = valid ? x.RCL[p & (RING - 1)] : 0u;
         const int32_t s = (int32_t)(e >> 1) - 1;
         const int cls = (int)(xc & 7u);
         const uint32_t cidx = xc >> 3;
@@ -511,14 +532,22 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[9] = XT;  // end by a full change list
         }
         __syncthreads();
-        int32_t dp = 0, cp = NEG;  // earlier warps, composed
-        for (int w = 0; w < wid; w++) {
-            int32_t wd = x.W[w * 8 + 0], wc = x.W[w * 8 + 1];
-            sat_compose(dp, cp, wd, wc);
-            dp = wd;
-            cp = wc;
+        {  // earlier warps, composed: lane w holds warp w's map, scanned across lanes
+            int32_t wd = lane < XW ? x.W[lane * 8 + 0] : 0, wc = lane < XW ? x.W[lane * 8 + 1] : NEG;
+#pragma unroll
+            for (int o = 1; o < XW; o <<= 1) {
+                const int32_t d2 = __shfl_up_sync(0xffffffffu, wd, o);
+                const int32_t c2 = __shfl_up_sync(0xffffffffu, wc, o);
+                if (lane >= o) sat_compose(d2, c2, wd, wc);
+            }
+            int32_t dp = __shfl_sync(0xffffffffu, wd, wid > 0 ? wid - 1 : 0);
+            int32_t cp = __shfl_sync(0xffffffffu, wc, wid > 0 ? wid - 1 : 0);
+            if (wid == 0) {
+                dp = 0;
+                cp = NEG;
+            }
+            sat_compose(dp, cp, de, ce);        // exclusive prefix at this thread
         }
-        sat_compose(dp, cp, de, ce);            // exclusive prefix at this thread
         const int32_t ni = max(nsafe + de, ce);  // safe lines seen by this access
         const bool sel = miss && ni >= 1;        // evicts (else bypass)
         const bool dr = miss && ni >= 2;         // consumes a draw (integers(1) draws nothing)
@@ -533,10 +562,28 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         }
         __syncthreads();
         int32_t pdr = __popc(bdr & below), psel = __popc(bsel & below), pchg = __popc(bchg & below);
-        for (int w = 0; w < wid; w++) {
-            pdr += x.W[w * 8 + 2];
-            psel += x.W[w * 8 + 3];
-            pchg += x.W[w * 8 + 4];
+        {  // earlier warps' counts: exclusive scan across lanes
+            int32_t v2 = lane < XW ? x.W[lane * 8 + 2] : 0, v3 = lane < XW ? x.W[lane * 8 + 3] : 0,
+                    v4 = lane < XW ? x.W[lane * 8 + 4] : 0;
+#pragma unroll
+            for (int o = 1; o < XW; o <<= 1) {
+                const int32_t u2 = __shfl_up_sync(0xffffffffu, v2, o);
+                const int32_t u3 = __shfl_up_sync(0xffffffffu, v3, o);
+                const int32_t u4 = __shfl_up_sync(0xffffffffu, v4, o);
+                if (lane >= o) {
+                    v2 += u2;
+                    v3 += u3;
+                    v4 += u4;
+                }
+            }
+            const int src = wid > 0 ? wid - 1 : 0;
+            const int32_t e2 = __shfl_sync(0xffffffffu, v2, src), e3 = __shfl_sync(0xffffffffu, v3, src),
+                          e4 = __shfl_sync(0xffffffffu, v4, src);
+            if (wid > 0) {
+                pdr += e2;
+                psel += e3;
+                pchg += e4;
+            }
         }
         // ---------------- B: draws
         uint32_t r = 0;
@@ -600,10 +647,15 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         const uint32_t total = x.SUPP[ns];
         Grp B;
         B.g = -1;
-        int32_t cur = -1, ylo = -1;
-        if (chg && in && cls == C_MU) {  // first approximation: the no-hole line
-            cur = sel_T(x, r, total, B);
-            x.CSLOT[pchg] = cur;
+        int32_t cur = -1, ylo = -1, lb = -1;
+        if (sel && in) {
+            // the group of T's r-th line: its load overlaps the change sort;
+            // an MU access's first approximation of its line is interpolated
+            // inside that group (no wait: the fixed point corrects it)
+            find_grp(x, r, total, B);
+            if (chg && cls == C_MU)
+                x.CSLOT[pchg] = (int32_t)(B.g * 1024) + B.grp * 128 +
+                                (int32_t)(((r - B.base) * 128u) / (B.cnt ? B.cnt : 1u));
         }
         __syncthreads();
         if (t == 0) {
@@ -618,6 +670,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // range of lines its fixed-point iteration looked at -- checked
         // exactly, and another pass run (rare: the moves are short)
         const unsigned long long mine = pchg >= 64 ? ~0ull : ((1ull << pchg) - 1ull);
+        int movs = 0;  // bucket shift: 2048 buckets over the lines
+        while (((x.L - 1) >> movs) >= MOVW * 32) movs++;
         for (int pass = 0; pass <= XP_MAX_CHG + 1; pass++) {
             __syncthreads();
             // sort the change lines (rank sort), then the prefix masks
@@ -640,7 +694,9 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (e < nchg && part == 1) x.FIN[e] = v;  // (ADD lines are final)
             }
             if (t == 0) x.MISC[10] = 0;
+            if (t < MOVW) x.MOVB[t] = 0u;
             __syncthreads();
+            if (t == 0) { tn = clock64(); prof[3] += tn - tc; tc = tn; }  // sort + masks
             if (wid == 0) {
                 unsigned long long b0 = 0, b1 = 0;
                 if (2 * lane < nchg) b0 = 1ull << x.SIDX[2 * lane];
@@ -666,26 +722,42 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 }
             }
             __syncthreads();
+            if (t == 0) { tn = clock64(); prof[4] += tn - tc; tc = tn; }  // resolve
             const unsigned long long addm =
                 (unsigned long long)(uint32_t)x.MISC[11] |
                 ((unsigned long long)(uint32_t)x.MISC[12] << 32);
             const unsigned long long allm = nchg >= 64 ? ~0ull : ((1ull << nchg) - 1ull);
             const unsigned long long holes = (addm & ~mine & allm) | (~addm & mine & allm);
             if (sel && in) {
-                cur = resolve(x, r, holes, nchg, total, B, ylo);
-                if (chg && cls == C_MU) x.FIN[pchg] = cur;
+                cur = resolve(x, r, holes, nchg, total, B, lb, ylo);
+                if (chg && cls == C_MU) {
+                    x.FIN[pchg] = cur;
+                    const int32_t u0 = x.CSLOT[pchg];
+                    if (u0 != cur)  // mark the buckets the move spans
+                        for (int32_t b = min(u0, cur) >> movs; b <= (max(u0, cur) >> movs); b++)
+                            atomicOr(&x.MOVB[b >> 5], 1u << (b & 31));
+                }
             }
             __syncthreads();
+            if (t == 0) { tn = clock64(); prof[5] += tn - tc; tc = tn; }  // verify
             if (t == 0) prof[7]++;
             // the earlier MU lines this access counted, used vs found
+            bool near = false;  // a moved MU line near the lines this access looked at?
             if (sel && in) {
+                for (int32_t b = ylo >> movs; b <= (cur >> movs) && !near; b++)
+                    near = (x.MOVB[b >> 5] >> (b & 31)) & 1u;
+                if (lb >= 0) near = near || ((x.MOVB[(lb >> movs) >> 5] >> ((lb >> movs) & 31)) & 1u);
+            }
+            if (near) {
                 unsigned long long mu = ~addm & mine & allm;
                 bool moved = false;
                 while (mu) {
                     const int i = __ffsll((long long)mu) - 1;
                     mu &= mu - 1;
                     const int32_t u0 = x.CSLOT[i], u1 = x.FIN[i];
-                    if (u0 != u1 && max(u0, u1) >= ylo && min(u0, u1) <= cur) moved = true;
+                    if (u0 != u1 && ((max(u0, u1) >= ylo && min(u0, u1) <= cur) ||
+                                     ((u0 <= lb) != (u1 <= lb))))
+                        moved = true;
                 }
                 if (moved) x.MISC[10] = 1;
             }
@@ -695,7 +767,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         }
         if (t == 0) {
             tn = clock64();
-            prof[3] += tn - tc;  // D/E passes
+            prof[5] += tn - tc;
             tc = tn;
         }
         x.ANS[t] = (sel && in) ? cur : -1;
@@ -715,7 +787,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         const int E = Epre < x.MISC[1] ? Epre : x.MISC[1];
         if (t == 0) {
             tn = clock64();
-            prof[5] += tn - tc;  // F
+            prof[6] += tn - tc;  // F
             tc = tn;
             st_rounds++;
             if (E < n - pos && E < XT) {
@@ -785,12 +857,12 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         {
             const int64_t etop = (pos + RING) < n ? pos + RING : n;
             for (int64_t i = efill + t; i < etop; i += XT) {
-                stage(&x.REV[i % RING], a.ev + i);
-                stage(&x.RCL[i % RING], a.xcls + i);
+                stage(&x.REV[i & (RING - 1)], a.ev + i);
+                stage(&x.RCL[i & (RING - 1)], a.xcls + i);
             }
             efill = etop > efill ? etop : efill;
             const int64_t ktop = (kpos + HRING) < a.hcap ? kpos + HRING : a.hcap;
-            for (int64_t i = kfill + t; i < ktop; i += XT) stage(&x.RH[i % HRING], a.H + i);
+            for (int64_t i = kfill + t; i < ktop; i += XT) stage(&x.RH[i & (HRING - 1)], a.H + i);
             kfill = ktop > kfill ? ktop : kfill;
             asm volatile("cp.async.commit_group;");
         }
@@ -861,7 +933,7 @@ int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
 size_t gids_xp_smem_bytes(int64_t L) {
     const int64_t nb = (L + 1023) / 1024, ns = (nb + 31) / 32;
     return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * RING + HRING + 2 * nb +
-                                       2 * ns + 1 + (ns + 31) / 32 + 2 * nb + XP_MAX_CHG +
+                                       2 * ns + 1 + (ns + 31) / 32 + 2 * nb + XP_MAX_CHG + MOVW +
                                        (GIDS_XP_CAND_CAP + 31) / 32 + 4 * XT + 4 * XP_MAX_CHG +
                                        XW * 8 + 16);
 }
