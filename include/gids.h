@@ -107,10 +107,20 @@ GIDS_API int gids_set_constant_buffer(gids_handle* h, const int64_t* node_ids, i
 GIDS_API int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds,
                 const uint64_t* rng, void* stream);
 
+/* sample_layer (sampler.py:50-84) for an explicit frontier: host int64[n]
+ * visited in the given order, repeats included (each occurrence draws its
+ * own `fanout` doubles), on a handle configured with one fanout.  Same
+ * stream semantics, sizes and export as gids_sample; layer 0's edges are
+ * grouped by frontier position.  Replaces sampler.py:59-84 for callers that
+ * pass a frontier the reference's sample_subgraph would not (unsorted,
+ * duplicated). */
+GIDS_API int gids_sample_frontier(gids_handle* h, const int64_t* frontier, int64_t n,
+                                  const uint64_t* rng, void* stream);
+
 /* Sizes of the last gids_sample (synchronises the stream):
  * layer_len[n_layers], n_unique, draws (doubles consumed), and the run-ahead
- * contribution of the batch against the current cache
- * (dataloader.py:188-192). */
+ * contribution of the batch (dataloader.py:188-192), counted by this call on
+ * the sampling stream against the cache as that stream sees it. */
 GIDS_API int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique,
                       int64_t* draws, int64_t* contribution);
 
@@ -122,7 +132,8 @@ GIDS_API int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* uni
  * a host round trip: edges_dev / unique_dev must hold the workspace bounds
  * (gids_sample_capacity); sizes_host (pinned, int64[n_layers + 5]) receives
  * [layer_len..., n_unique, draws, contribution, overflow] when the stream
- * gets there. */
+ * gets there; the contribution slot is 0 -- count it with
+ * gids_contribution_async, ordered against the serving stream. */
 GIDS_API int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev,
                                       int64_t* sizes_host, void* stream);
 GIDS_API int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* unique_cap);
@@ -137,7 +148,10 @@ GIDS_API int gids_contribution_async(gids_handle* h, const int64_t* unique_dev,
 GIDS_API int gids_sampler_rng(gids_handle* h, uint64_t words_out[6]);
 
 /* WindowBuffer.push_iteration / pop_iteration (cache.py:66-91) for an
- * ascending unique device list. */
+ * ascending unique device list.  The per-node lookahead count is 8-bit: a
+ * push beyond 255 lists in flight returns GIDS_E_CAPACITY (the reference
+ * has no bound; the configs use W <= 255), a pop of an empty window
+ * GIDS_E_STATE. */
 GIDS_API int gids_window_push(gids_handle* h, const int64_t* nodes_dev, int64_t n, void* stream);
 GIDS_API int gids_window_pop(gids_handle* h, const int64_t* nodes_dev, int64_t n, void* stream);
 
@@ -148,7 +162,9 @@ GIDS_API int gids_window_pop(gids_handle* h, const int64_t* nodes_dev, int64_t n
  * set-associative eviction draws.  The decisions run on `stream`; the row
  * movement runs on `gather_stream` (NULL = same stream) after them, so the
  * next batch's decisions can overlap this batch's gather.  out_dev is
- * complete when gather_stream reaches this point. */
+ * complete when gather_stream reaches this point.  Precondition: unique_dev
+ * strictly ascending (MiniBatch.unique_nodes is); a violation is detected on
+ * the device and reported by the next gids_serve_counts (GIDS_E_INVALID). */
 GIDS_API int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
                float* out_dev, void* stream, void* gather_stream);
 
@@ -167,8 +183,9 @@ GIDS_API int gids_serve_decisions(gids_handle* h, int8_t* kind_dev, int64_t* lin
  * / pop); counts_dev int32[n] (optional) receives each node's lookahead count.
  * gids_cache_access: CacheState.access (cache.py:144-180) for n distinct
  * nodes in list order, exact policy; kind_dev int8[n] (GIDS_KIND_*), line_dev
- * int32[n] (-1 on bypass), victim_dev int64[n] (optional: the evicted line's
- * occupant at the call's start, -1 when none).  Device pointers. */
+ * int32[n] (-1 on bypass), victim_dev int64[n] (optional: the node each
+ * miss evicted -- the previous inserter of that line within this call, else
+ * the line's occupant at the call's start; -1 when none).  Device pointers. */
 GIDS_API int gids_cache_window_update(gids_handle* h, const int64_t* nodes_dev, int64_t n,
                                       int32_t* counts_dev, void* stream);
 GIDS_API int gids_cache_access(gids_handle* h, const int64_t* nodes_dev, int64_t n,

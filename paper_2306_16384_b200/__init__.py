@@ -18,7 +18,7 @@ from .loader import CSV_HEADER, Dataloader, IterationStats, RunSummary, run, sta
 from .sampling import (Fanouts, MiniBatch, batch_iterator, check_fanouts, sample_layer,
                        sample_subgraph)
 from .settings import ConfigError, InfeasibleError, PipelineConfig, load_config, make_config
-from .storage_model import (PRESETS, SsdSpec, achieved_fraction, fetch_total_us, preset,
-                            required_accesses)
+from .storage_model import (PRESETS, FetchTiming, SsdSpec, achieved_fraction, fetch_total_us,
+                            preset, required_accesses, simulate_fetch)
 
 __version__ = "0.1.0"

@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
         "gids_set_backing": ([vp, vp, i64], C.c_int),
         "gids_set_constant_buffer": ([vp, vp, i64, vp], C.c_int),
         "gids_sample": ([vp, vp, i64, vp, vp], C.c_int),
+        "gids_sample_frontier": ([vp, vp, i64, vp, vp], C.c_int),
         "gids_sample_sizes": ([vp, vp, vp, vp, vp], C.c_int),
         "gids_sample_export": ([vp, vp, vp, vp], C.c_int),
         "gids_sample_export_async": ([vp, vp, vp, vp, vp], C.c_int),
@@ -127,7 +128,7 @@ def lib() -> C.CDLL:
 def exported_symbols() -> list[str]:
     """Every entry point include/gids.h declares (checked by the CPU tests)."""
     return ["gids_abi_version", "gids_last_error", "gids_create", "gids_destroy",
-            "gids_load_graph", "gids_set_backing", "gids_set_constant_buffer", "gids_sample",
+            "gids_load_graph", "gids_set_backing", "gids_set_constant_buffer", "gids_sample", "gids_sample_frontier",
             "gids_sample_sizes", "gids_sample_export", "gids_sample_export_async",
             "gids_sample_capacity", "gids_sampler_rng", "gids_window_push", "gids_window_pop",
             "gids_serve", "gids_serve_counts", "gids_serve_decisions", "gids_cache_stats",
@@ -263,6 +264,14 @@ class Handle:
         w = None if words is None else np.ascontiguousarray(words, dtype=np.uint64)
         check(lib().gids_sample(self.h, s.ctypes.data, len(s),
                                 None if w is None else w.ctypes.data, stream), "sample")
+
+    def sample_frontier(self, frontier: np.ndarray, words, stream: int) -> None:
+        """One layer over an explicit frontier, in order, repeats included."""
+        f = np.ascontiguousarray(frontier, dtype=np.int64)
+        w = None if words is None else np.ascontiguousarray(words, dtype=np.uint64)
+        check(lib().gids_sample_frontier(self.h, f.ctypes.data, len(f),
+                                         None if w is None else w.ctypes.data, stream),
+              "sample_frontier")
 
     def sample_export_async(self, edges, unique, sizes_host, stream: int) -> None:
         check(lib().gids_sample_export_async(self.h, _p(edges), _p(unique), _p(sizes_host),

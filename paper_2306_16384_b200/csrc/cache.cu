@@ -90,11 +90,15 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                                  CacheMeta* meta, uint32_t* ev, int mode = 3,
                                  int32_t* counts = nullptr, int64_t* nmiss0 = nullptr,
                                  uint32_t* xcls = nullptr, int32_t* cand_of_slot = nullptr,
-                                 int32_t* cand_slot = nullptr, int64_t* n_cand = nullptr) {
+                                 int32_t* cand_slot = nullptr, int64_t* n_cand = nullptr,
+                                 int64_t* bad_order = nullptr) {
     int64_t inc = 0, dec = 0, unsafe = 0, miss0 = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = (int32_t)uniq[p];
+        // the serving precondition (strictly ascending, hence distinct): the
+        // counters below are updated without atomics
+        if (bad_order && p > 0 && uniq[p - 1] >= uniq[p]) *bad_order = 1;
         uint32_t c = (mode & 1) ? future[x] : 0u;
         if (counts) counts[p] = (int32_t)c;
         uint32_t old = reuse[x];
@@ -712,18 +716,34 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
 __global__ void k_post_a(const int64_t* __restrict__ uniq, const ServeCounters* svc,
                          const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
                          const int32_t* __restrict__ line_node, int32_t* slot_of, int32_t* last_ins,
-                         uint32_t* g_evict, int clear_evict, int64_t* victim = nullptr) {
+                         uint32_t* g_evict, int clear_evict) {
     int64_t n = svc->n_log;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t t = log_line[i];
         int32_t o = line_node[t];
-        if (victim) victim[log_pos[i]] = o;  // the line's occupant at the batch start
         if (o >= 0) slot_of[o] = -1;
         slot_of[uniq[log_pos[i]]] = -1;
         atomicMax(&last_ins[t], (int32_t)i);
         if (clear_evict) g_evict[t >> 5] = 0u;
     }
+}
+// CacheState.access's `evicted` per insertion of a multi-node call, in log
+// order: the previous inserter of the same line in this call, else the
+// line's occupant at the call's start (standalone API only: one thread,
+// last_ins as per-line scratch, left as it was found, -1)
+__global__ void k_victims(const int64_t* __restrict__ uniq, const ServeCounters* svc,
+                          const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
+                          const int32_t* __restrict__ line_node, int32_t* last_ins,
+                          int64_t* victim) {
+    const int64_t n = svc->n_log;
+    for (int64_t i = 0; i < n; i++) {
+        const int32_t t = log_line[i];
+        const int32_t prev = last_ins[t];
+        victim[log_pos[i]] = prev >= 0 ? uniq[log_pos[prev]] : (int64_t)line_node[t];
+        last_ins[t] = (int32_t)i;
+    }
+    for (int64_t i = 0; i < n; i++) last_ins[log_line[i]] = -1;
 }
 // post-pass B: the final inserter owns the line
 __global__ void k_post_b(const int64_t* __restrict__ uniq, const ServeCounters* svc,
@@ -1011,7 +1031,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                                               h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
                                               h->meta, h->ev, 3, nullptr, &h->svc->n_miss0,
                                               exact ? h->xcls : nullptr, h->cand_of_slot,
-                                              h->cand_slot, &h->svc->n_cand);
+                                              h->cand_slot, &h->svc->n_cand, &h->svc->bad_order);
         GIDS_LAUNCH_CHECK(h);
         if (exact) {
             size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
@@ -1151,9 +1171,13 @@ extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n
         int rc = launch_exact_seq(h, n, smem, st);
         if (rc) return rc;
     }
+    if (victim_out) {
+        k_victims<<<1, 1, 0, st>>>(nodes, h->svc, h->log_line, h->log_pos, h->line_node,
+                                   h->last_ins, victim_out);
+        GIDS_LAUNCH_CHECK(h);
+    }
     k_post_a<<<g, BLOCK, 0, st>>>(nodes, h->svc, h->log_line, h->log_pos, h->line_node,
-                                  h->slot_of, h->last_ins, h->evict_bits, h->exact_smem ? 0 : 1,
-                                  victim_out);
+                                  h->slot_of, h->last_ins, h->evict_bits, h->exact_smem ? 0 : 1);
     GIDS_LAUNCH_CHECK(h);
     k_post_b<<<g, BLOCK, 0, st>>>(nodes, h->svc, h->log_line, h->log_pos, h->line_node,
                                   h->slot_of, h->last_ins, h->ins);

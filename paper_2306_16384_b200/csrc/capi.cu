@@ -192,7 +192,8 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
 
     // workspace bounds (sampler.py: every layer edge <= frontier * fanout)
     h->max_seeds = cfg->max_seeds;
-    int64_t front = cfg->max_seeds < N ? cfg->max_seeds : N, ecap = 0, fcap = front;
+    // (layer 0 may be an explicit frontier with repeats: gids_sample_frontier)
+    int64_t front = cfg->max_seeds, ecap = 0, fcap = front;
     for (int l = 0; l < cfg->n_layers; l++) {
         int64_t e = front * cfg->fanouts[l];
         ecap += e;
@@ -426,12 +427,32 @@ int gids_sample(gids_handle* h, const int64_t* seeds, int64_t n_seeds, const uin
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->seeds_dev, seeds, sizeof(int64_t) * n_seeds,
                                   cudaMemcpyHostToDevice, st));
     h->last_stream = st;
-    return gids_launch_sample(h, n_seeds, rng, st);
+    return gids_launch_sample(h, n_seeds, rng, false, st);
+}
+
+int gids_sample_frontier(gids_handle* h, const int64_t* frontier, int64_t n, const uint64_t* rng,
+                         void* stream) {
+    CHECK_H(h);
+    if (n < 1 || n > h->max_seeds) {
+        gids_set_error("frontier length must be in [1, max_seeds]");
+        return GIDS_E_INVALID;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    GIDS_CUDA_TRY(cudaMemcpyAsync(h->seeds_dev, frontier, sizeof(int64_t) * n,
+                                  cudaMemcpyHostToDevice, st));
+    h->last_stream = st;
+    return gids_launch_sample(h, n, rng, true, st);
 }
 
 int gids_sample_sizes(gids_handle* h, int64_t* layer_len, int64_t* n_unique, int64_t* draws,
                       int64_t* contribution) {
     CHECK_H(h);
+    // the contribution is counted here, on the sampling stream after the
+    // batch, against the cache as that stream sees it (the serving path
+    // counts its admissions with gids_contribution_async instead)
+    TRY(gids_launch_contribution(h, h->last_stream));
+    GIDS_CUDA_TRY(cudaMemcpyAsync(&h->sc_host->contribution, &h->sc->contribution, sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, h->last_stream));
     GIDS_CUDA_TRY(cudaStreamSynchronize(h->last_stream));
     gids_harvest_sample(h, false);
     const SampleCounters& c = *h->sc_host;
@@ -501,13 +522,26 @@ int gids_sampler_rng(gids_handle* h, uint64_t words_out[6]) {
     return GIDS_OK;
 }
 
+// future[] holds one byte per node: at most 255 lists may be in the window
 int gids_window_push(gids_handle* h, const int64_t* nodes, int64_t n, void* stream) {
     CHECK_H(h);
-    return gids_launch_window(h, nodes, n, +1, (cudaStream_t)stream);
+    if (h->window_lists >= 255) {
+        gids_set_error("window holds 255 lists (the per-node lookahead count is 8-bit)");
+        return GIDS_E_CAPACITY;
+    }
+    TRY(gids_launch_window(h, nodes, n, +1, (cudaStream_t)stream));
+    h->window_lists++;
+    return GIDS_OK;
 }
 int gids_window_pop(gids_handle* h, const int64_t* nodes, int64_t n, void* stream) {
     CHECK_H(h);
-    return gids_launch_window(h, nodes, n, -1, (cudaStream_t)stream);
+    if (h->window_lists <= 0) {
+        gids_set_error("window is empty");
+        return GIDS_E_STATE;
+    }
+    TRY(gids_launch_window(h, nodes, n, -1, (cudaStream_t)stream));
+    h->window_lists--;
+    return GIDS_OK;
 }
 
 int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
@@ -543,6 +577,11 @@ int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
         h->serve_timed = false;
     }
     const ServeCounters& c = *h->svc_host;
+    if (c.bad_order) {
+        gids_set_error("gids_serve: unique_dev was not strictly ascending (cache state is "
+                       "undefined from this batch on)");
+        return GIDS_E_INVALID;
+    }
     if (!h->counts_read && c.xp_done) {
         h->xp_batches++;
         for (int i = 0; i < 4; i++) h->xp_stats[i] += c.xp_stats[i];

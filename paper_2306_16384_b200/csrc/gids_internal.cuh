@@ -143,6 +143,7 @@ struct ServeCounters {
     int64_t n_cand;        // resident SafeToEvict nodes of the batch (exact_par.cu)
     int64_t xp_done;       // the batch was decided by k_exact_par
     int64_t xp_stats[4];   // its rounds; rounds ended by a rejection / full change list / lost line
+    int64_t bad_order;     // the served list was not strictly ascending (k_window_consume)
     int64_t xp_prof[8];    // SM cycles per phase (A+B, C tables, selects+D+E, F, G, G prefix, ring) and D passes
 };
 
@@ -210,6 +211,7 @@ struct gids_handle {
 
     // sampler workspace (HBM)
     int64_t max_seeds;
+    int window_lists = 0;  // lists pushed and not popped (future[] is 8-bit)
     int64_t edge_cap;      // total edges over all layers
     int64_t front_cap;     // max frontier size
     uint32_t* bm_front;    // [ceil(N/32)]
@@ -374,7 +376,7 @@ int gids_bitmap_compact_n(gids_handle* h, uint32_t* bm, int64_t nbits, int32_t* 
 int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* out,
                          cudaStream_t st);
 // sampler.cu
-int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_words,
+int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_words, bool raw,
                        cudaStream_t st);
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
 int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st);

@@ -35,6 +35,20 @@ __device__ __forceinline__ void mark(uint32_t* bm, int32_t v) {
     atomicOr(bm + (v >> 5), 1u << (v & 31));
 }
 
+// sample_layer's frontier as given (sampler.py:59-84: any order, duplicates
+// expanded again, each with its own draws): ids narrowed in place of the
+// deduplicated seed frontier
+__global__ void k_front_raw(const int64_t* __restrict__ seeds, int64_t n, int32_t* front,
+                            SampleCounters* sc, uint32_t* bm_all) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) sc->n_front = n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = (int32_t)seeds[i];
+        front[i] = v;
+        mark(bm_all, v);
+    }
+}
+
 __global__ void k_seed_mark(const int64_t* __restrict__ seeds, int64_t n, uint32_t* bm_front,
                             uint32_t* bm_all) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -195,15 +209,22 @@ static void build_jump_table(uint64_t inc_hi, uint64_t inc_lo, u128* tab) {
 // The per-batch sampling sequence (~20 kernels and copies, all sized by
 // n_seeds and the handle's bounds, every count staying on the device):
 // capturable as one CUDA graph.
-static int sample_body(gids_handle* h, int64_t n_seeds, cudaStream_t st) {
+static int sample_body(gids_handle* h, int64_t n_seeds, bool raw, cudaStream_t st) {
     const gids_config& c = h->cfg;
     GIDS_CUDA_TRY(cudaMemsetAsync(h->sc, 0, sizeof(SampleCounters), st));
-    k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
-                                                                     h->bm_front, h->bm_all);
-    GIDS_LAUNCH_CHECK(h);
-    int rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
+    int rc = GIDS_OK;
+    if (raw) {
+        k_front_raw<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(
+            h->seeds_dev, n_seeds, h->frontier, h->sc, h->bm_all);
+        GIDS_LAUNCH_CHECK(h);
+    } else {
+        k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
+                                                                         h->bm_front, h->bm_all);
+        GIDS_LAUNCH_CHECK(h);
+        rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
                                  st);
-    if (rc) return rc;
+        if (rc) return rc;
+    }
     for (int l = 0; l < c.n_layers; l++) {
         int f = c.fanouts[l];
         rc = gids_scan_take_draw(h, f, l, st);
@@ -221,8 +242,6 @@ static int sample_body(gids_handle* h, int64_t n_seeds, cudaStream_t st) {
     }
     rc = gids_bitmap_compact(h, h->bm_all, h->unique32, &h->sc->n_unique, h->unique_cap, true, st);
     if (rc) return rc;
-    rc = gids_launch_contribution(h, st);
-    if (rc) return rc;
     k_rng_advance<<<1, 1, 0, st>>>(h->rng_dev, h->sc, c.n_layers, h->jump_tab);
     GIDS_LAUNCH_CHECK(h);
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
@@ -230,7 +249,8 @@ static int sample_body(gids_handle* h, int64_t n_seeds, cudaStream_t st) {
     return GIDS_OK;
 }
 
-int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaStream_t st) {
+int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, bool raw,
+                       cudaStream_t st) {
     const gids_config& c = h->cfg;
     for (int l = 0; l < c.n_layers; l++) {
         if (c.fanouts[l] > MAX_FANOUT) {
@@ -263,14 +283,14 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
     // replay the batch's launch sequence as one CUDA graph (one per distinct
     // seed count; not on the legacy default stream, which cannot capture)
     int rc;
-    if (h->use_graphs && st != 0 && st != cudaStreamLegacy) {
+    if (h->use_graphs && !raw && st != 0 && st != cudaStreamLegacy) {
         SampleGraph* g = nullptr;
         for (int i = 0; i < h->n_sgraphs; i++)
             if (h->sgraphs[i].n_seeds == n_seeds) g = &h->sgraphs[i];
         if (!g && h->n_sgraphs < GIDS_MAX_SGRAPHS) {
             const int64_t l0 = h->launches;
             GIDS_CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-            rc = sample_body(h, n_seeds, st);
+            rc = sample_body(h, n_seeds, false, st);
             cudaGraph_t graph = nullptr;
             cudaError_t e = cudaStreamEndCapture(st, &graph);
             if (rc) {
@@ -300,7 +320,7 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, cudaS
             return GIDS_OK;
         }
     }
-    rc = sample_body(h, n_seeds, st);
+    rc = sample_body(h, n_seeds, raw, st);
     if (rc) return rc;
     gids_sample_end(h, st);
     return GIDS_OK;

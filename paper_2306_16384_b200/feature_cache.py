@@ -241,6 +241,8 @@ def window_update(cache: CacheState, window: WindowBuffer, current_batch) -> dic
     h = cache._h
     st = _native.stream_ptr(cache._dev.index)
     cur = cache._nodes(current_batch)
+    if len(window.lists) > 255:
+        raise ValueError("the GPU lookahead counts are 8-bit: at most 255 window lists")
     lists = [l if hasattr(l, "numel") else cache._nodes(l) for l in window.lists]
     for l in lists:
         h.window_push(l, st)

@@ -141,17 +141,21 @@ def sample_subgraph(g: GraphCsc, seeds, fanouts: Fanouts, rng, device: int = 0) 
 
 
 def sample_layer(g: GraphCsc, frontier, fanout: int, rng, device: int = 0):
-    """One hop (sampler.py:50-84): the first layer of a one-fanout subgraph sample.
-
-    The frontier is deduplicated and sorted first, as every frontier the
-    reference produces already is."""
+    """One hop (sampler.py:50-84) on the GPU: up to ``fanout`` distinct
+    in-neighbours per frontier entry, (E, 2) [src, dst] grouped in frontier
+    order.  The frontier is taken exactly as given -- any order, repeats
+    expanded again with draws of their own -- as the reference's loop does."""
     if fanout < 1:
         raise ValueError("fanout must be >= 1")
-    f = np.unique(np.asarray(frontier, dtype=np.int64))
+    f = np.asarray(frontier, dtype=np.int64).reshape(-1)
     if len(f) == 0:
         import torch
         return torch.empty((0, 2), dtype=torch.int64, device=torch.device("cuda", device))
-    return sample_subgraph(g, f, [fanout], rng, device).layers[0]
+    f = check_seeds(f, g.num_nodes)
+    smp = _sampler_for(g, [int(fanout)], len(f), device)
+    st = _native.stream_ptr(device)
+    smp.h.sample_frontier(f, pcg_words(rng), st)
+    return smp.collect(f, rng, st)[0].layers[0]
 
 
 def batch_iterator(seed_set, batch_size: int, shuffle: bool = False,

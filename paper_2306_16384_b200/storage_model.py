@@ -11,6 +11,13 @@ dataloader.py:301-337).  Those use the three-phase SSD envelope of
                                            base threshold; 855 for Optane @ 0.95)
 * ``achieved_fraction``                    storage.py:107-114
 * ``fetch_total_us``                       storage.py:177-188 (closed form)
+* ``FetchTiming`` / ``simulate_fetch``     storage.py:117-174 -- the phase breakdown
+                                           of one fetch.  The reference replays it
+                                           as a discrete-event loop over n_ssd
+                                           round-robin servers; with balanced dealing
+                                           the last completion is ceil(n/n_ssd)
+                                           quanta past t_init, so it is computed in
+                                           closed form (same exact rationals)
 
 All arithmetic is exact (``fractions.Fraction``), floats read at their
 shortest decimal repr, as the reference does.
@@ -101,3 +108,37 @@ def fetch_total_us(spec: SsdSpec, n_access: int) -> Fraction:
         per_device = math.ceil(Fraction(n_access, spec.n_ssd))
         total += Fraction(1_000_000) / exact(spec.iop_peak) * per_device
     return total
+
+
+@dataclass(frozen=True)
+class FetchTiming:
+    """Phase breakdown of one fetch (seconds); achieved_iops over all devices."""
+
+    n_access: int
+    t_init: float
+    t_steady: float
+    t_term: float
+    achieved_iops: float
+    achieved_fraction: float
+
+    @property
+    def total(self) -> float:
+        return self.t_init + self.t_steady + self.t_term
+
+
+def simulate_fetch(spec: SsdSpec, n_access: int) -> FetchTiming:
+    """One batched fetch of n accesses: t_init, then every device retires one
+    access per 1/iop_peak s (the fullest of the round-robin loads sets the
+    steady phase), then t_term."""
+    if n_access < 0:
+        raise ValueError("n_access must be non-negative")
+    init_us = exact(spec.t_init) * 1_000_000
+    term_us = exact(spec.t_term) * 1_000_000
+    steady_us = Fraction(1_000_000) / exact(spec.iop_peak) * math.ceil(
+        Fraction(n_access, spec.n_ssd)) if n_access > 0 else Fraction(0)
+    total_us = init_us + steady_us + term_us
+    rate = Fraction(n_access) * 1_000_000 / total_us if total_us else Fraction(0)
+    return FetchTiming(n_access=n_access, t_init=float(init_us) / 1e6,
+                       t_steady=float(steady_us) / 1e6, t_term=float(term_us) / 1e6,
+                       achieved_iops=float(rate),
+                       achieved_fraction=float(rate / (exact(spec.iop_peak) * spec.n_ssd)))

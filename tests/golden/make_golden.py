@@ -15,6 +15,9 @@ rng.npz       numpy PCG64 streams: raw next64 outputs, random() doubles,
               integers(n) sequences (buffered-uint32 Lemire), advance() and
               jumped() states.  Pins the RNG the sampler (sampler.py:75) and the
               eviction draw (cache.py:165) consume.
+sample_layer.npz  sample_layer (sampler.py:50-84) over frontiers the loader
+              never produces: repeated and unsorted entries, each expanded
+              with draws of its own, fanout above and below 32.
 sample.npz    sample_subgraph (sampler.py:87-112) on tree / star / hub /
               uniform / powerlaw / parallel-edge / edgeless graphs: every
               layer, unique_nodes and the generator state afterwards.
@@ -39,7 +42,7 @@ sys.path.insert(0, str(REF))
 from tierloader.config import make_config, load_config  # noqa: E402
 from tierloader.dataloader import Dataloader  # noqa: E402
 from tierloader.graph import build_csc, generate_synthetic  # noqa: E402
-from tierloader.sampler import sample_subgraph  # noqa: E402
+from tierloader.sampler import sample_layer, sample_subgraph  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 U64 = (1 << 64) - 1
@@ -263,8 +266,36 @@ def make_loader(name: str, spec, n_batches: int | None = None, keep_rows: bool =
           "evictions", dl.cache.evictions)
 
 
+def make_sample_layer() -> None:
+    gs = graphs()
+    r = np.random.default_rng(31)
+    cases = [
+        ("star", np.zeros(5000, np.int64), 3, 2024),          # one node, 5000 times
+        ("star", np.array([0, 7, 0, 0, 300, 0]), 40, 7),        # fanout > 32, repeats
+        ("hub", r.integers(0, 600, 3000), 5, 8),                # unsorted, repeats
+        ("uniform", r.permutation(3000)[:700].repeat(2), 10, 9),
+        ("powerlaw", r.integers(0, 4000, 5000), 17, 10),
+        ("edgeless", np.array([4, 4, 1]), 2, 11),
+    ]
+    rec: dict[str, np.ndarray] = {}  # (graphs: the same g_* arrays as sample.npz)
+    meta = []
+    for ci, (gname, front, fan, rs) in enumerate(cases):
+        rng = np.random.default_rng(rs)
+        rec[f"c{ci}_frontier"] = np.asarray(front, np.int64)
+        rec[f"c{ci}_state0"] = np.array(state_words(rng.bit_generator), dtype=np.uint64)
+        rec[f"c{ci}_edges"] = sample_layer(gs[gname], front, fan, rng).astype(np.int64)
+        rec[f"c{ci}_state1"] = np.array(state_words(rng.bit_generator), dtype=np.uint64)
+        meta.append({"case": ci, "graph": gname, "fanout": fan})
+    rec["meta"] = np.array(json.dumps(meta))
+    np.savez_compressed(OUT / "sample_layer.npz", **rec)
+
+
 def main() -> None:
+    if sys.argv[1:] == ["sample_layer"]:  # regenerate that file only
+        make_sample_layer()
+        return
     make_rng()
+    make_sample_layer()
     make_sample()
     for name, spec in LOADER_CONFIGS.items():
         keep = name in ("c09", "alltiers", "edgeless")

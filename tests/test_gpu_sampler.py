@@ -119,3 +119,36 @@ def test_gpu_sampler_large_properties():
         lo, hi = indptr[dst].astype(np.int64), indptr[dst + 1].astype(np.int64)
         assert np.all(hi > lo)
         assert np.all((src >= 0) & (src < n))
+
+
+@pytest.mark.parametrize("case", range(6))
+def test_gpu_sample_layer_matches_reference_fixture(case):
+    """sample_layer over frontiers taken as given (sampler.py:59-84): repeats
+    expanded again with their own draws, unsorted order kept, fanout above
+    and below 32 -- bit-exact edges and Generator state vs the reference."""
+    from paper_2306_16384_b200 import sample_layer
+    fx = np.load(GOLDEN / "sample_layer.npz")
+    gx = np.load(GOLDEN / "sample.npz")
+    m = json.loads(str(fx["meta"]))[case]
+    ip, ix = gx[f"g_{m['graph']}_indptr"], gx[f"g_{m['graph']}_indices"]
+    g = GraphCsc(num_nodes=len(ip) - 1, num_edges=len(ix), indptr=ip, indices=ix)
+    rng = gen_from_words(fx[f"c{case}_state0"])
+    edges = sample_layer(g, fx[f"c{case}_frontier"], m["fanout"], rng).cpu().numpy()
+    assert np.array_equal(edges, fx[f"c{case}_edges"])
+    assert np.array_equal(pcg_words(rng)[:4], fx[f"c{case}_state1"][:4])
+
+
+def test_gpu_sample_layer_inclusion_frequency():
+    """The reference's Monte-Carlo check (pkg/tests/test_sampler.py:64-75):
+    100,000 copies of a star's centre, 3 of 5 leaves each: every leaf is
+    drawn with probability 3/5."""
+    from paper_2306_16384_b200 import sample_layer
+    g = build_csc([(i, 0) for i in range(1, 6)], num_nodes=6)
+    trials = 100_000
+    edges = sample_layer(g, np.zeros(trials, np.int64), 3,
+                         np.random.default_rng(2024)).cpu().numpy()
+    assert edges.shape == (3 * trials, 2)
+    freq = np.bincount(edges[:, 0], minlength=6)[1:] / trials
+    assert np.all(np.abs(freq - 0.6) <= 0.01)
+    per = edges[:, 0].reshape(trials, 3)
+    assert np.all((per[:, 0] != per[:, 1]) & (per[:, 1] != per[:, 2]) & (per[:, 0] != per[:, 2]))

@@ -271,43 +271,8 @@ int main(int argc, char** argv) {
                 });
             }
     }
-    {
-        // copy-engine gather: one cudaMemcpyBatchAsync of nsel row copies,
-        // optionally overlapped with a zero-copy kernel taking a share of rows
-        std::vector<void*> dsts(nsel), srcs(nsel);
-        std::vector<size_t> sizes(nsel, (size_t)row_bytes);
-        for (int64_t i = 0; i < nsel; i++) {
-            dsts[i] = out + i * row_bytes;
-            srcs[i] = table + (int64_t)sel[i] * row_bytes;
-        }
-        cudaMemcpyAttributes attr;
-        memset(&attr, 0, sizeof(attr));
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.srcLocHint.type = cudaMemLocationTypeHost;
-        attr.dstLocHint.type = cudaMemLocationTypeDevice;
-        attr.dstLocHint.id = 0;
-        size_t idx0 = 0, fail = 0;
-        cudaStream_t s1, s2;  // the batch API rejects the legacy NULL stream
-        CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-        for (double share : {1.0, 0.5, 0.25}) {
-            int64_t nce = (int64_t)(nsel * share);
-            snprintf(name, sizeof name, "ce batch share=%.2f", share);
-            timeit(name, [&] {
-                cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(),
-                                                     (size_t)nce, &attr, &idx0, 1, &fail, s1);
-                if (e != cudaSuccess) {
-                    fprintf(stderr, "batch: %s (fail %zu)\n", cudaGetErrorString(e), fail);
-                    exit(1);
-                }
-                if (nce < nsel)  // the rest by SM zero-copy loads, concurrently
-                    k_ldg<2><<<37, 256, 0, s2>>>(dsel + nce, nsel - nce, cpr, (const int4*)table,
-                                                 (int4*)(out + nce * row_bytes));
-                CK(cudaStreamSynchronize(s2));
-                CK(cudaStreamSynchronize(s1));
-            });
-        }
-    }
+    // (the copy-engine per-row batch copy measured in round 1 -- 3.8 GB/s at 4 KB,
+    // profiles/r01_hostread_microbench_dma_batch.txt -- is a closed API on this pool)
     timeit("dma contiguous", [&] {
         CK(cudaMemcpyAsync(out, table, (size_t)bytes, cudaMemcpyHostToDevice));
     });
