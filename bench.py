@@ -280,6 +280,17 @@ def cpu_baseline_sample(cfg, dl, seconds: float = 12.0) -> dict:
                       f"policy={cfg.gids_policy}, same graph and rows as the GPU run"}
 
 
+def _timeline(dl):
+    """GIDS_TRACE_HOST=1: (decisions done, rows done) per batch of the last
+    timed steps, ms after the first batch's decisions (device clock)."""
+    tl = getattr(dl, "_timeline", None)
+    if not tl:
+        return None
+    tl = tl[-12:]
+    base = tl[0][0]
+    return [[round(base.elapsed_time(d), 3), round(base.elapsed_time(g), 3)] for d, g in tl]
+
+
 _SHARED: dict = {}
 
 
@@ -453,6 +464,7 @@ def main() -> None:
     torch.cuda.synchronize(local)
     wall = time.perf_counter() - t0
     trace1 = dl._trace[tr0:] if dl._trace is not None else None
+    timeline1 = _timeline(dl)  # (pass 1's last batches)
     if steady_profile:
         torch.cuda.profiler.stop()
     clocks = clk.stop()
@@ -613,6 +625,7 @@ def main() -> None:
         "storage_file": dl.storage_stats(),
         "numa": numa,
         "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),
+        "e2e_timeline_ms": timeline1,
         "e2e_host_ms_per_call": {"min": float(np.min(call_ms)), "median": float(np.median(call_ms)),
                                  "p90": float(np.percentile(call_ms, 90)),
                                  "max": float(np.max(call_ms)),

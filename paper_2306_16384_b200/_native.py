@@ -491,3 +491,57 @@ class HugePageHost:
             self.close()
         except Exception:
             pass
+
+
+class SharedHost:
+    """A POSIX shared-memory region (/dev/shm/<name>) mapped into this process
+    and page-locked + mapped for zero-copy GPU reads (gids_host_register):
+    the node's one host tier, shared by every local rank instead of one
+    private pinned copy per rank.  ``create`` makes (and sizes) it; the other
+    ranks attach.  ``unlink`` drops the name once every rank has attached
+    (the mappings stay valid until closed)."""
+
+    def __init__(self, name: str, nbytes: int, create: bool, register: bool = True):
+        import mmap
+        import os
+        self.name, self.nbytes = name, int(nbytes)
+        self.path = "/dev/shm/" + name
+        flags = os.O_RDWR | (os.O_CREAT | os.O_EXCL if create else 0)
+        fd = os.open(self.path, flags, 0o600)
+        try:
+            if create:
+                os.ftruncate(fd, self.nbytes)
+            elif os.fstat(fd).st_size != self.nbytes:
+                raise RuntimeError(f"{self.path}: size {os.fstat(fd).st_size} != {self.nbytes}")
+            self._map = mmap.mmap(fd, self.nbytes, mmap.MAP_SHARED,
+                                  mmap.PROT_READ | mmap.PROT_WRITE)
+        finally:
+            os.close(fd)
+        self._view = np.frombuffer(self._map, dtype=np.uint8)
+        self.ptr = self._view.ctypes.data
+        self._registered = False
+        if register:
+            check(lib().gids_host_register(C.c_void_p(self.ptr), self.nbytes), "host_register")
+            self._registered = True
+
+    def array(self, shape, dtype) -> np.ndarray:
+        return self._view.view(dtype).reshape(shape)
+
+    def unlink(self) -> None:
+        import os
+        try:
+            os.unlink(self.path)
+        except FileNotFoundError:
+            pass
+
+    def close(self) -> None:
+        if getattr(self, "_registered", False):
+            lib().gids_host_unregister(C.c_void_p(self.ptr))
+            self._registered = False
+        if getattr(self, "_map", None) is not None:
+            self._view = None
+            try:
+                self._map.close()
+            except BufferError:  # a numpy view is still alive; the GC unmaps it
+                pass
+            self._map = None

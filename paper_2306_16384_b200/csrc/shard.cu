@@ -35,38 +35,56 @@ __global__ void k_shard_finish(int64_t n, ServeCounters* svc) {
 
 // out[p] = row of uniq[p] from its owner's shard; flat 16-byte chunks,
 // U loads in flight per lane (peer latency over NVLink is ~2 us, so the
-// whole GPU keeps several MB outstanding)
-template <int U>
+// whole GPU keeps several MB outstanding).  Index math is 32-bit (the chunk
+// count and node ids fit: checked on the host) and, when the row's chunk
+// count / the shard count are powers of two (every config here), shifts and
+// masks -- round 1's 64-bit i / cpr, x % G, x / G per chunk held the kernel
+// at 0.61 of HBM.
+template <int U, bool POW2>
 __global__ void __launch_bounds__(BLOCK)
-k_gather_shards(const int64_t* __restrict__ uniq, int64_t n, const int4* const* __restrict__ shards,
-                int32_t G, uint32_t cpr, int4* __restrict__ out) {
-    const uint64_t total = (uint64_t)n * cpr;
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * (uint64_t)BLOCK + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * BLOCK) >> 5;
-    for (uint64_t base = warp * U * 32; base < total; base += nwarps * U * 32) {
+k_gather_shards(const int64_t* __restrict__ uniq, uint32_t n, const int4* const* __restrict__ shards,
+                uint32_t G, uint32_t g_shift, uint32_t cpr, uint32_t cpr_shift,
+                int4* __restrict__ out) {
+    const uint32_t total = n * cpr;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * (uint32_t)BLOCK + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * (uint32_t)BLOCK) >> 5;
+    for (uint32_t base = warp * U * 32; base < total; base += nwarps * U * 32) {
         int4 v[U];
-        int64_t d[U];
 #pragma unroll
         for (int k = 0; k < U; k++) {
-            const uint64_t i = base + k * 32 + lane;
-            d[k] = -1;
+            const uint32_t i = base + k * 32 + lane;
             if (i < total) {
-                const uint64_t r = i / cpr, c = i - r * cpr;
-                const int64_t x = uniq[r];
-                const int4* src = shards[x % G] + (x / G) * (int64_t)cpr + c;
+                uint32_t r, c, o, q;
+                if (POW2) {
+                    r = i >> cpr_shift;
+                    c = i & (cpr - 1);
+                } else {
+                    r = i / cpr;
+                    c = i - r * cpr;
+                }
+                const uint32_t x = (uint32_t)__ldg(uniq + r);
+                if (POW2) {
+                    o = x & (G - 1);
+                    q = x >> g_shift;
+                } else {
+                    q = x / G;
+                    o = x - q * G;
+                }
+                const int4* src = shards[o] + (size_t)q * cpr + c;
                 asm volatile("ld.global.nc.v4.s32 {%0,%1,%2,%3}, [%4];"
                              : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w)
                              : "l"(src));
-                d[k] = (int64_t)i;
             }
         }
 #pragma unroll
-        for (int k = 0; k < U; k++)
-            if (d[k] >= 0)
-                asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(out + d[k]),
+        for (int k = 0; k < U; k++) {
+            const uint32_t i = base + k * 32 + lane;
+            if (i < total)
+                asm volatile("st.global.cs.v4.s32 [%0], {%1,%2,%3,%4};" ::"l"(out + i),
                              "r"(v[k].x), "r"(v[k].y), "r"(v[k].z), "r"(v[k].w)
                              : "memory");
+        }
     }
 }
 
@@ -124,10 +142,19 @@ int gids_launch_shard_serve(gids_handle* h, const int64_t* uniq, int64_t n, floa
     if (h->profiling) cudaEventRecord(h->gev[par][0], gst);
     if (h->profiling) cudaEventRecord(h->gev[par][1], gst);  // no separate hit phase
     const int64_t dim = h->row_floats;
-    if ((dim & 3) == 0) {
-        k_gather_shards<4><<<4 * GIDS_SMS, BLOCK, 0, gst>>>(
-            uniq, n, reinterpret_cast<const int4* const*>(h->shard_ptrs), h->n_shards,
-            (uint32_t)(dim >> 2), reinterpret_cast<int4*>(out));
+    const int64_t cpr = dim >> 2;
+    if ((dim & 3) == 0 && n * cpr < (int64_t)UINT32_MAX && h->N < (int64_t)INT32_MAX) {
+        auto pow2 = [](int64_t v) { return v > 0 && (v & (v - 1)) == 0; };
+        auto lg = [](int64_t v) { uint32_t s = 0; while ((int64_t(1) << s) < v) s++; return s; };
+        const uint32_t G = (uint32_t)h->n_shards;
+        const auto* sp = reinterpret_cast<const int4* const*>(h->shard_ptrs);
+        if (pow2(cpr) && pow2(G))
+            k_gather_shards<4, true><<<4 * GIDS_SMS, BLOCK, 0, gst>>>(
+                uniq, (uint32_t)n, sp, G, lg(G), (uint32_t)cpr, lg(cpr),
+                reinterpret_cast<int4*>(out));
+        else
+            k_gather_shards<4, false><<<4 * GIDS_SMS, BLOCK, 0, gst>>>(
+                uniq, (uint32_t)n, sp, G, 0, (uint32_t)cpr, 0, reinterpret_cast<int4*>(out));
     } else {
         k_gather_shards_f32<<<gids_grid(n * dim, BLOCK, 8 * GIDS_SMS), BLOCK, 0, gst>>>(
             uniq, n, h->shard_ptrs, h->n_shards, dim, out);

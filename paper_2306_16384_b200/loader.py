@@ -29,7 +29,7 @@ from fractions import Fraction
 
 import numpy as np
 
-from . import _native
+from . import _native, host_tier
 from .csc import (HEADER_BYTES, FeatureStore, GraphCsc, generate_synthetic, load_features,
                   load_graph, pinned_feature_table, write_synthetic_features)
 from .feature_cache import GpuCacheView, WindowBuffer
@@ -255,6 +255,7 @@ class Dataloader:
         # host-time trace of next_batch (diagnostics): run-ahead, output
         # allocation, serve launch, wait for the decisions -- seconds per call
         self._trace = [] if os.environ.get("GIDS_TRACE_HOST") == "1" else None
+        self._timeline = []  # with _trace: per batch (decided, gathered) CUDA events
         self._clock_us = Fraction(0)
         self._fetch_us_total = Fraction(0)
         self._train_us_total = Fraction(0)
@@ -271,6 +272,8 @@ class Dataloader:
         reference's generator or the GPU generator; pinned host rows, the
         .gfea file itself, or HBM shards.  Returns the graph in HBM."""
         cfg = self.cfg
+        import torch
+        self._shared = []  # node-shared host regions (host_tier.py)
         if cfg.graph_path is not None:
             self.graph = load_graph(cfg.graph_path)
             host = load_features(cfg.features_path, mmap=True)
@@ -278,7 +281,21 @@ class Dataloader:
                 raise ConfigError("feature table and graph disagree on node count")
             self._storage_file = str(cfg.features_path) if cfg.gids_storage == "file" else None
             # file tier: the rows stay in the file (memory-mapped for the host API)
-            self.features = host if self._storage_file else self._pin_table(host)
+            if self._storage_file:
+                self.features = host
+            elif self._shared_host():
+                tok = self._host_token = host_tier.job_token()
+
+                def fill(view):
+                    for r in range(0, host.num_nodes, 1 << 18):
+                        view[r:r + (1 << 18)] = host.table[r:r + (1 << 18)]
+                self._shared.append(host_tier.SharedRegion(
+                    f"gids-{tok}-table", (host.num_nodes, host.dim), np.float32,
+                    self._host_creator, fill))
+                self.features = FeatureStore(num_nodes=host.num_nodes, dim=host.dim,
+                                             table=self._shared[-1].array)
+            else:
+                self.features = self._pin_table(host)
             return self._upload_graph(self.graph)
         if cfg.gids_generator == "device":
             # counter-based uniform generator in HBM (csrc/graph_setup.cu)
@@ -308,10 +325,35 @@ class Dataloader:
             self.features = FeatureStore(num_nodes=host.num_nodes, dim=host.dim,
                                          table=host.table, seed=feat_seed)
             self._storage_file = str(cfg.gids_storage_path)
+        elif self._shared_host():
+            tok = self._host_token = host_tier.job_token()
+            n, dim = cfg.num_nodes, cfg.feature_dim
+            st = _native.stream_ptr(self.device)
+
+            def fill(view):  # the GPU writes the reference's rows into the mapping
+                for r0 in range(0, n, 1 << 20):
+                    k = min(1 << 20, n - r0)
+                    _native.synthesize_rows(self.device, feat_seed, r0, k, dim,
+                                            view[r0:r0 + k].ctypes.data, st)
+                torch.cuda.synchronize(self.device)
+            self._shared.append(host_tier.SharedRegion(
+                f"gids-{tok}-table", (n, dim), np.float32, self._host_creator, fill))
+            self.features = FeatureStore(num_nodes=n, dim=dim, table=self._shared[-1].array,
+                                         seed=feat_seed)
         else:
             self.features = pinned_feature_table(cfg.num_nodes, cfg.feature_dim, feat_seed,
                                                  self.device)
         return dev_graph
+
+    def _shared_host(self) -> bool:
+        """One node-shared host tier (host_tier.py) instead of a private copy."""
+        c = self.cfg
+        return (c.gids_shared_host and c.gids_dp_world > 1 and host_tier._dist() is not None
+                and not c.gids_sharded_table and c.gids_storage == "pinned")
+
+    @property
+    def _host_creator(self) -> bool:
+        return host_tier.local_rank(self.cfg.gids_dp_rank) == 0
 
     def _build_constant_buffer(self, dev_graph, row_bytes: int) -> None:
         """ConstantBuffer (dataloader.py:125-135): reverse PageRank + top-k on
@@ -322,8 +364,15 @@ class Dataloader:
             self.pagerank, dev_scores = reverse_pagerank_device(self.device, *dev_graph)
             chosen = top_k_nodes_device(dev_scores, budget // row_bytes)
             del dev_scores
+            pin = True
+            if self._shared:  # the buffer's GPU copy joins the node-shared host tier
+                def pin(shape, fill):
+                    self._shared.append(host_tier.SharedRegion(
+                        f"gids-{self._host_token}-buffer", shape, np.float32,
+                        self._host_creator, fill))
+                    return self._shared[-1].array
             self.buffer = build_constant_buffer(self.pagerank.scores, self.features, budget,
-                                                pinned=chosen, pin_memory=True)
+                                                pinned=chosen, pin_memory=pin)
         else:
             self.pagerank = None
             self.buffer = build_constant_buffer(np.empty(0), self.features, 0,
@@ -540,9 +589,13 @@ class Dataloader:
             self._last_contrib = None
         self._h.serve(unique, self._iteration, rows, self._ctl.cuda_stream,
                       self._gat.cuda_stream)
-        decided = torch.cuda.Event()
+        decided = torch.cuda.Event(enable_timing=tr is not None)
         decided.record(self._ctl)
         self._last_decided = decided
+        if tr is not None:  # device timeline per batch: decisions done, rows done
+            gathered = torch.cuda.Event(enable_timing=True)
+            gathered.record(self._gat)
+            self._timeline.append((decided, gathered))
         # the next batches' sampling is launched before the host waits for
         # the decisions' counts, so the sampling stream stays busy while the
         # host accounts and returns (the sampled content is fixed by the seed
@@ -632,6 +685,9 @@ class Dataloader:
             if self.cfg.gids_dp_world > 1 and dist.is_available() and dist.is_initialized():
                 dist.barrier()  # no peer may still be reading this rank's shard
             self.sharded.close()
+        for r in getattr(self, "_shared", []):  # this rank's mapping of the node's host tier
+            r.close()
+        self._shared = []
 
 
 def run(dl: Dataloader, iterations: int | None = None, warmup: int | None = None):

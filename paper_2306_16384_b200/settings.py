@@ -32,6 +32,12 @@ prefixed ``gids``) select the B200 path:
                       A synthetic config writes its table to
                       ``gids_storage_path`` first.
 * ``gids_io_threads`` / ``gids_io_direct``  pread threads / O_DIRECT for "file".
+* ``gids_shared_host`` with several data-parallel ranks (torch.distributed
+                      initialised), the ranks of a node share ONE host tier:
+                      the pinned storage table and the constant buffer's rows
+                      live in POSIX shared memory created by local rank 0 and
+                      mapped + page-locked by every rank (host_tier.py),
+                      instead of a private copy per rank.
 * ``gids_speculate``  batches sampled ahead of the run-ahead queue (their
                       contributions are still counted when they join it, so
                       results are unchanged; 0 disables).
@@ -109,6 +115,7 @@ class PipelineConfig:
     gids_io_threads: int = 8
     gids_io_direct: bool = False
     gids_speculate: int = 2
+    gids_shared_host: bool = True
 
     def ssd_spec(self) -> SsdSpec:
         if self.ssd_preset is None:
