@@ -56,7 +56,9 @@ constexpr int RING = 4096;        // staged accesses (ev, class)
 constexpr int HRING = 4096;       // staged draw halves
 constexpr int RING_LAG = 12;      // commit groups allowed in flight when a round reads
 constexpr int32_t NEG = -(1 << 29);
-constexpr int MOVW = 64;          // moved-line filter: 2048 buckets (lines >> MOVS)
+constexpr int MOVN = 2048;        // moved-line filter: buckets (lines >> movs)
+constexpr int CUMN = 256;         // change-line buckets of count_le (lines >> bsh)
+constexpr int CHBW = 128;         // candidate-line hash: 4096 bits
 
 enum { C_STAY = GIDS_XC_STAY, C_ADD = GIDS_XC_ADD, C_CAND = GIDS_XC_CAND, C_M0 = GIDS_XC_M0,
        C_MU = GIDS_XC_MU };
@@ -140,12 +142,12 @@ struct Xs {
     uint32_t* CNT;    // [nb] lines of T per block
     uint32_t* BLKP;   // [nb] exclusive prefix within the 32-block superblock
     uint32_t* SUPP;   // [ns+1] exclusive prefix over superblocks
-    uint32_t* STOT;   // [ns] superblock totals
-    uint32_t* TOUCH;  // [(ns+31)/32] superblocks whose counts changed
     uint32_t* CONV;   // [cand_cap/32] candidates whose line was taken
     uint32_t* GCNT;   // [2*nb] lines of T per 128-line group, one byte each
     int32_t* FIN;     // [XP_MAX_CHG] MU lines found by the current pass
-    uint32_t* MOVB;   // [MOVW] 1024-line buckets a moved MU line crossed this pass
+    unsigned long long* MOVM;  // [MOVN] per bucket: MU changes whose move crossed it (this pass)
+    int32_t* CUMB;    // [CUMN+1] changes with line < (b << bsh), b = 0..CUMN
+    uint32_t* CHB;    // [CHBW] hash of the round's candidate lines
     uint32_t* REV;    // [RING]
     uint32_t* RCL;    // [RING]
     uint32_t* RH;     // [HRING]
@@ -155,12 +157,15 @@ struct Xs {
     int32_t* CTYPE;   // [XP_MAX_CHG] +1 ADD, -1 MU
     int32_t* SS;      // [XP_MAX_CHG] change lines, ascending
     int32_t* SIDX;    // [XP_MAX_CHG] their change indices
+    int32_t* RANKS;   // [XP_MAX_CHG] rank of each change (by line)
+    int32_t* CHT;     // [XP_MAX_CHG] the access (thread) of each change
     unsigned long long* PM;  // [XP_MAX_CHG+1] change-index mask of the k lowest lines
     int32_t* CANL;    // [XT] lanes of this round's unconverted candidates
     int32_t* CANS;    // [XT] their lines
     int32_t* W;       // [XW * 8] warp partials
     int32_t* MISC;    // [16]
     int64_t nb, ns, L;
+    int bsh;
     const uint32_t* gbits;
 };
 
@@ -286,15 +291,27 @@ __device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total
     return sel_grp(G, q - G.base);
 }
 
-// lines among the round's changes <= y
+// lines among the round's changes <= y: the bucket's start, then the few
+// changes inside the bucket
 __device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
-    int lo = 0, hi = m;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (x.SS[mid] <= y) lo = mid + 1;
-        else hi = mid;
+    int j = x.CUMB[y >> x.bsh];
+    while (j < m && x.SS[j] <= y) j++;
+    return j;
+}
+
+// one line joins (+1) or leaves (-1) T: block / group counts and the two
+// prefix levels, updated in place by one warp (a lane per prefix entry;
+// the round's changes are spread over the warps)
+__device__ __forceinline__ void t_update_warp(const Xs& x, int32_t s, int delta, int lane) {
+    const int64_t g = s >> 10, sb = g >> 5;
+    const uint32_t d = (uint32_t)delta;
+    if (lane == 0) {
+        atomicAdd(&x.CNT[g], d);
+        atomicAdd(&x.GCNT[s >> 9], d << (((s >> 7) & 3) * 8));
     }
-    return lo;
+    const int64_t ge = (sb + 1) * 32 < x.nb ? (sb + 1) * 32 : x.nb;
+    if (g + 1 + lane < ge) atomicAdd(&x.BLKP[g + 1 + lane], d);
+    for (int64_t u = sb + 1 + lane; u <= x.ns; u += 32) atomicAdd(&x.SUPP[u], d);
 }
 
 // the r-th line of T minus `holes` (a mask over the change list): the least
@@ -304,15 +321,15 @@ __device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
 // answer, one bitmap load.  The hole counts it used: at line lb, and at the
 // lines of [ylo, answer].
 __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned long long holes,
-                                           int m, uint32_t total, Grp& B, int32_t& lb,
-                                           int32_t& ylo) {
+                                           int m, uint32_t total, int64_t rblk, Grp& B,
+                                           int32_t& lb, int32_t& ylo) {
     if (!holes) {
         const int32_t y = sel_T(x, r, total, B);
         ylo = y;
         lb = -1;
         return y;
     }
-    lb = (int32_t)(locate(x, r, total) * 1024) - 1;
+    lb = (int32_t)(rblk * 1024) - 1;  // (rblk: the block of T's r-th line)
     uint32_t q = r + (lb >= 0 ? (uint32_t)__popcll(x.PM[count_le(x, m, lb)] & holes) : 0u);
     int32_t y = sel_T(x, q, total, B);
     ylo = y;
@@ -325,12 +342,11 @@ __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned lon
     return y;
 }
 
-// re-prefix the superblocks flagged in TOUCH (all threads; ends synchronised)
-__device__ void rebuild(const Xs& x, int t) {
+// the prefix tables from CNT (all threads; ends synchronised).  Once, at
+// the start: rounds then update them in place (t_update).
+__device__ void prefix_all(const Xs& x, int t) {
     const int lane = t & 31, wid = t >> 5;
-    const int nsw = (int)((x.ns + 31) >> 5);
     for (int64_t sb = wid; sb < x.ns; sb += XW) {
-        if (!((x.TOUCH[sb >> 5] >> (sb & 31)) & 1u)) continue;
         const int64_t blk = sb * 32 + lane;
         const uint32_t c = blk < x.nb ? x.CNT[blk] : 0u;
         uint32_t inc = c;
@@ -340,33 +356,17 @@ __device__ void rebuild(const Xs& x, int t) {
             if (lane >= o) inc += u;
         }
         if (blk < x.nb) x.BLKP[blk] = inc - c;
-        if (lane == 31) x.STOT[sb] = inc;
+        if (lane == 31) x.SUPP[sb + 1] = inc;  // (superblock total, summed below)
     }
     __syncthreads();
-    if (wid == 0) {  // SUPP = exclusive prefix of STOT
-        const int per = (int)((x.ns + 31) >> 5);
-        uint32_t loc = 0;
-        for (int i = 0; i < per; i++) {
-            const int64_t s = (int64_t)lane * per + i;
-            loc += s < x.ns ? x.STOT[s] : 0u;
-        }
-        uint32_t inc = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += u;
-        }
-        uint32_t run = inc - loc;
-        for (int i = 0; i < per; i++) {
-            const int64_t s = (int64_t)lane * per + i;
-            if (s < x.ns) {
-                run += x.STOT[s];
-                x.SUPP[s + 1] = run;
-            }
+    if (t == 0) {
+        uint32_t run = 0;
+        x.SUPP[0] = 0;
+        for (int64_t u = 1; u <= x.ns; u++) {
+            run += x.SUPP[u];
+            x.SUPP[u] = run;
         }
     }
-    if (wid == 1 || XW == 1)
-        for (int i = lane; i < nsw; i += 32) x.TOUCH[i] = 0u;
     __syncthreads();
 }
 
@@ -408,8 +408,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += 2 * x.nb;
         x.FIN = reinterpret_cast<int32_t*>(p);
         p += XP_MAX_CHG;
-        x.MOVB = p;
-        p += MOVW;
+        x.CUMB = reinterpret_cast<int32_t*>(p);
+        p += CUMN + 2;
+        x.CHB = p;
+        p += CHBW;
         x.REV = p;
         p += RING;
         x.RCL = p;
@@ -422,10 +424,6 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += x.nb;
         x.SUPP = p;
         p += x.ns + 1;
-        x.STOT = p;
-        p += x.ns;
-        x.TOUCH = p;
-        p += (x.ns + 31) / 32;
         x.CONV = p;
         p += (a.cand_cap + 31) / 32;
         x.ANS = reinterpret_cast<int32_t*>(p);
@@ -440,6 +438,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += XP_MAX_CHG;
         x.SIDX = reinterpret_cast<int32_t*>(p);
         p += XP_MAX_CHG;
+        x.RANKS = reinterpret_cast<int32_t*>(p);
+        p += XP_MAX_CHG;
+        x.CHT = reinterpret_cast<int32_t*>(p);
+        p += XP_MAX_CHG;
         x.CANL = reinterpret_cast<int32_t*>(p);
         p += XT;
         x.CANS = reinterpret_cast<int32_t*>(p);
@@ -447,7 +449,12 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         x.W = reinterpret_cast<int32_t*>(p);
         p += XW * 8;
         x.MISC = reinterpret_cast<int32_t*>(p);
+        p += 16;
+        p += (reinterpret_cast<uintptr_t>(p) & 7) ? 1 : 0;
+        x.MOVM = reinterpret_cast<unsigned long long*>(p);
     }
+    x.bsh = 0;
+    while (((x.L - 1) >> x.bsh) >= CUMN) x.bsh++;
     const int64_t n = a.n, nb = x.nb, ns = x.ns;
     for (int64_t i = t; i < nb; i += XT) x.CNT[i] = a.blk_cnt[i];
     for (int64_t i = t; i < 2 * nb; i += XT) {  // four 128-line group counts per word
@@ -461,9 +468,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         x.GCNT[i] = packed;
     }
     for (int64_t i = t; i < (a.cand_cap + 31) / 32; i += XT) x.CONV[i] = 0u;
-    for (int64_t i = t; i < (ns + 31) / 32; i += XT) x.TOUCH[i] = ~0u;  // (all: first prefix)
+    for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;
     x.PANS[t] = -1;
-    if (t == 0) x.SUPP[0] = 0;
     // stage the first accesses and halves
     int64_t efill = n < RING ? n : RING;
     int64_t kfill = a.hcap < HRING ? a.hcap : HRING;
@@ -475,8 +481,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     asm volatile("cp.async.commit_group;");
     asm volatile("cp.async.wait_group 0;");
     __syncthreads();
-    rebuild(x, t);
+    prefix_all(x, t);
 
+    int movs = 0;  // moved-line filter: MOVN buckets over the lines
+    while (((x.L - 1) >> movs) >= MOVN) movs++;
     int64_t pos = 0, kpos = 0, nlog = 0;
     int32_t nsafe = (int32_t)a.meta->safe_count;
     int32_t pend_cidx = -1;  // cand_of_slot of this thread's last committed eviction
@@ -507,22 +515,6 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             d = -1;
             c = 0;
         }
-        int32_t di = d, ci = c;  // inclusive warp scan of the saturating map
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t d2 = __shfl_up_sync(0xffffffffu, di, o);
-            const int32_t c2 = __shfl_up_sync(0xffffffffu, ci, o);
-            if (lane >= o) sat_compose(d2, c2, di, ci);
-        }
-        int32_t de = __shfl_up_sync(0xffffffffu, di, 1), ce = __shfl_up_sync(0xffffffffu, ci, 1);
-        if (lane == 0) {
-            de = 0;
-            ce = NEG;
-        }
-        if (lane == 31) {
-            x.W[wid * 8 + 0] = di;
-            x.W[wid * 8 + 1] = ci;
-        }
         if (t == 0) {
             x.MISC[0] = XT;  // end of the round before conversions (min)
             x.MISC[1] = XT;  // first candidate that lost its line (min)
@@ -531,58 +523,113 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[8] = XT;  // end by a Lemire rejection
             x.MISC[9] = XT;  // end by a full change list
         }
-        __syncthreads();
-        {  // earlier warps, composed: lane w holds warp w's map, scanned across lanes
-            int32_t wd = lane < XW ? x.W[lane * 8 + 0] : 0, wc = lane < XW ? x.W[lane * 8 + 1] : NEG;
+        int32_t ni, pdr, psel, pchg;
+        bool sel, dr, chg;
+        if (nsafe >= XT + 2) {
+            // no access of the round can see fewer than 2 safe lines: every
+            // miss evicts and draws, so one packed scan of (misses, ADDs,
+            // MUs) gives the safe count, draw, log and change positions
+            const uint32_t pk = (miss ? 1u : 0u) | ((valid && cls == C_ADD) ? (1u << 10) : 0u) |
+                                ((miss && cls == C_MU) ? (1u << 20) : 0u);
+            uint32_t inc = pk;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += u;
+            }
+            if (lane == 31) x.W[wid * 8 + 0] = (int32_t)inc;
+            __syncthreads();
+            uint32_t wv = lane < XW ? (uint32_t)x.W[lane * 8 + 0] : 0u;
 #pragma unroll
             for (int o = 1; o < XW; o <<= 1) {
-                const int32_t d2 = __shfl_up_sync(0xffffffffu, wd, o);
-                const int32_t c2 = __shfl_up_sync(0xffffffffu, wc, o);
-                if (lane >= o) sat_compose(d2, c2, wd, wc);
+                const uint32_t u = __shfl_up_sync(0xffffffffu, wv, o);
+                if (lane >= o) wv += u;
             }
-            int32_t dp = __shfl_sync(0xffffffffu, wd, wid > 0 ? wid - 1 : 0);
-            int32_t cp = __shfl_sync(0xffffffffu, wc, wid > 0 ? wid - 1 : 0);
-            if (wid == 0) {
-                dp = 0;
-                cp = NEG;
-            }
-            sat_compose(dp, cp, de, ce);        // exclusive prefix at this thread
-        }
-        const int32_t ni = max(nsafe + de, ce);  // safe lines seen by this access
-        const bool sel = miss && ni >= 1;        // evicts (else bypass)
-        const bool dr = miss && ni >= 2;         // consumes a draw (integers(1) draws nothing)
-        const bool chg = valid && (cls == C_ADD || (cls == C_MU && sel));
-        const unsigned bdr = __ballot_sync(0xffffffffu, dr);
-        const unsigned bsel = __ballot_sync(0xffffffffu, sel);
-        const unsigned bchg = __ballot_sync(0xffffffffu, chg);
-        if (lane == 0) {
-            x.W[wid * 8 + 2] = __popc(bdr);
-            x.W[wid * 8 + 3] = __popc(bsel);
-            x.W[wid * 8 + 4] = __popc(bchg);
-        }
-        __syncthreads();
-        int32_t pdr = __popc(bdr & below), psel = __popc(bsel & below), pchg = __popc(bchg & below);
-        {  // earlier warps' counts: exclusive scan across lanes
-            int32_t v2 = lane < XW ? x.W[lane * 8 + 2] : 0, v3 = lane < XW ? x.W[lane * 8 + 3] : 0,
-                    v4 = lane < XW ? x.W[lane * 8 + 4] : 0;
+            const uint32_t wp = __shfl_sync(0xffffffffu, wv, wid > 0 ? wid - 1 : 0);
+            const uint32_t ex = inc - pk + (wid > 0 ? wp : 0u);
+            const int32_t em = (int32_t)(ex & 1023u), ea = (int32_t)((ex >> 10) & 1023u),
+                          eu = (int32_t)(ex >> 20);
+            ni = nsafe + ea - eu;
+            sel = miss;
+            dr = miss;
+            chg = valid && (cls == C_ADD || cls == C_MU);
+            pdr = em;
+            psel = em;
+            pchg = ea + eu;
+        } else {
+            int32_t di = d, ci = c;  // inclusive warp scan of the saturating map
 #pragma unroll
-            for (int o = 1; o < XW; o <<= 1) {
-                const int32_t u2 = __shfl_up_sync(0xffffffffu, v2, o);
-                const int32_t u3 = __shfl_up_sync(0xffffffffu, v3, o);
-                const int32_t u4 = __shfl_up_sync(0xffffffffu, v4, o);
-                if (lane >= o) {
-                    v2 += u2;
-                    v3 += u3;
-                    v4 += u4;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t d2 = __shfl_up_sync(0xffffffffu, di, o);
+                const int32_t c2 = __shfl_up_sync(0xffffffffu, ci, o);
+                if (lane >= o) sat_compose(d2, c2, di, ci);
+            }
+            int32_t de = __shfl_up_sync(0xffffffffu, di, 1), ce = __shfl_up_sync(0xffffffffu, ci, 1);
+            if (lane == 0) {
+                de = 0;
+                ce = NEG;
+            }
+            if (lane == 31) {
+                x.W[wid * 8 + 0] = di;
+                x.W[wid * 8 + 1] = ci;
+            }
+            __syncthreads();
+            {  // earlier warps, composed: lane w holds warp w's map, scanned across lanes
+                int32_t wd = lane < XW ? x.W[lane * 8 + 0] : 0,
+                        wc = lane < XW ? x.W[lane * 8 + 1] : NEG;
+#pragma unroll
+                for (int o = 1; o < XW; o <<= 1) {
+                    const int32_t d2 = __shfl_up_sync(0xffffffffu, wd, o);
+                    const int32_t c2 = __shfl_up_sync(0xffffffffu, wc, o);
+                    if (lane >= o) sat_compose(d2, c2, wd, wc);
                 }
+                int32_t dp = __shfl_sync(0xffffffffu, wd, wid > 0 ? wid - 1 : 0);
+                int32_t cp = __shfl_sync(0xffffffffu, wc, wid > 0 ? wid - 1 : 0);
+                if (wid == 0) {
+                    dp = 0;
+                    cp = NEG;
+                }
+                sat_compose(dp, cp, de, ce);  // exclusive prefix at this thread
             }
-            const int src = wid > 0 ? wid - 1 : 0;
-            const int32_t e2 = __shfl_sync(0xffffffffu, v2, src), e3 = __shfl_sync(0xffffffffu, v3, src),
-                          e4 = __shfl_sync(0xffffffffu, v4, src);
-            if (wid > 0) {
-                pdr += e2;
-                psel += e3;
-                pchg += e4;
+            ni = max(nsafe + de, ce);  // safe lines seen by this access
+            sel = miss && ni >= 1;     // evicts (else bypass)
+            dr = miss && ni >= 2;      // consumes a draw (integers(1) draws nothing)
+            chg = valid && (cls == C_ADD || (cls == C_MU && sel));
+            const unsigned bdr = __ballot_sync(0xffffffffu, dr);
+            const unsigned bsel = __ballot_sync(0xffffffffu, sel);
+            const unsigned bchg = __ballot_sync(0xffffffffu, chg);
+            if (lane == 0) {
+                x.W[wid * 8 + 2] = __popc(bdr);
+                x.W[wid * 8 + 3] = __popc(bsel);
+                x.W[wid * 8 + 4] = __popc(bchg);
+            }
+            __syncthreads();
+            pdr = __popc(bdr & below);
+            psel = __popc(bsel & below);
+            pchg = __popc(bchg & below);
+            {  // earlier warps' counts: exclusive scan across lanes
+                int32_t v2 = lane < XW ? x.W[lane * 8 + 2] : 0, v3 = lane < XW ? x.W[lane * 8 + 3] : 0,
+                        v4 = lane < XW ? x.W[lane * 8 + 4] : 0;
+#pragma unroll
+                for (int o = 1; o < XW; o <<= 1) {
+                    const int32_t u2 = __shfl_up_sync(0xffffffffu, v2, o);
+                    const int32_t u3 = __shfl_up_sync(0xffffffffu, v3, o);
+                    const int32_t u4 = __shfl_up_sync(0xffffffffu, v4, o);
+                    if (lane >= o) {
+                        v2 += u2;
+                        v3 += u3;
+                        v4 += u4;
+                    }
+                }
+                const int src = wid > 0 ? wid - 1 : 0;
+                const int32_t e2 = __shfl_sync(0xffffffffu, v2, src),
+                              e3 = __shfl_sync(0xffffffffu, v3, src),
+                              e4 = __shfl_sync(0xffffffffu, v4, src);
+                if (wid > 0) {
+                    pdr += e2;
+                    psel += e3;
+                    pchg += e4;
+                }
             }
         }
         // ---------------- B: draws
@@ -622,22 +669,26 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // ---------------- C: T = start set + the round's ADD lines; the start-of-T answers
         if (chg && in) {
             x.CTYPE[pchg] = cls == C_ADD ? 1 : -1;
+            x.CHT[pchg] = t;
             atomicMax(&x.MISC[3], pchg + 1);
             if (cls == C_ADD) {
                 x.CSLOT[pchg] = s;
                 atomicOr(&a.safe_bits[s >> 5], 1u << (s & 31));
-                atomicAdd(&x.CNT[s >> 10], 1u);
-                atomicAdd(&x.GCNT[s >> 9], 1u << (((s >> 7) & 3) * 8));
-                atomicOr(&x.TOUCH[s >> 20], 1u << ((s >> 15) & 31));
             }
         }
         if (valid && in && cls == C_CAND && !conv) {
             const int k = atomicAdd(&x.MISC[7], 1);
             x.CANL[k] = t;
             x.CANS[k] = s;
+            atomicOr(&x.CHB[(s >> 5) & (CHBW - 1)], 1u << (s & 31));
         }
         __syncthreads();
-        rebuild(x, t);
+        {  // the round's ADD lines join T's tables
+            const int nc0 = x.MISC[3];
+            for (int e = wid; e < nc0; e += XW)
+                if (x.CTYPE[e] > 0) t_update_warp(x, x.CSLOT[e], +1, lane);
+        }
+        __syncthreads();
         if (t == 0) {
             tn = clock64();
             prof[1] += tn - tc;  // C: T tables
@@ -648,11 +699,13 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         Grp B;
         B.g = -1;
         int32_t cur = -1, ylo = -1, lb = -1;
+        int64_t rblk = 0;
         if (sel && in) {
             // the group of T's r-th line: its load overlaps the change sort;
             // an MU access's first approximation of its line is interpolated
             // inside that group (no wait: the fixed point corrects it)
             find_grp(x, r, total, B);
+            rblk = B.g;
             if (chg && cls == C_MU)
                 x.CSLOT[pchg] = (int32_t)(B.g * 1024) + B.grp * 128 +
                                 (int32_t)(((r - B.base) * 128u) / (B.cnt ? B.cnt : 1u));
@@ -670,8 +723,6 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // range of lines its fixed-point iteration looked at -- checked
         // exactly, and another pass run (rare: the moves are short)
         const unsigned long long mine = pchg >= 64 ? ~0ull : ((1ull << pchg) - 1ull);
-        int movs = 0;  // bucket shift: 2048 buckets over the lines
-        while (((x.L - 1) >> movs) >= MOVW * 32) movs++;
         for (int pass = 0; pass <= XP_MAX_CHG + 1; pass++) {
             __syncthreads();
             // sort the change lines (rank sort), then the prefix masks
@@ -692,27 +743,11 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                     x.SIDX[rk] = e;
                 }
                 if (e < nchg && part == 1) x.FIN[e] = v;  // (ADD lines are final)
+                if (e < nchg && part == 2) x.RANKS[e] = rk;
             }
             if (t == 0) x.MISC[10] = 0;
-            if (t < MOVW) x.MOVB[t] = 0u;
-            __syncthreads();
-            if (t == 0) { tn = clock64(); prof[3] += tn - tc; tc = tn; }  // sort + masks
-            if (wid == 0) {
-                unsigned long long b0 = 0, b1 = 0;
-                if (2 * lane < nchg) b0 = 1ull << x.SIDX[2 * lane];
-                if (2 * lane + 1 < nchg) b1 = 1ull << x.SIDX[2 * lane + 1];
-                unsigned long long inc = b0 | b1;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned long long u = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc |= u;
-                }
-                const unsigned long long ex = inc & ~(b0 | b1);
-                // PM[k] = lines of the k lowest: PM[2l] = ex, PM[2l+1] = ex | b0
-                if (2 * lane <= nchg) x.PM[2 * lane] = ex;
-                if (2 * lane + 1 <= nchg) x.PM[2 * lane + 1] = ex | b0;
-                if (lane == 31 && nchg == 64) x.PM[64] = inc;
-                // ADD mask
+            for (int i = t; i < MOVN; i += XT) x.MOVM[i] = 0ull;
+            if (pass == 0 && wid == XW - 1) {  // ADD mask (CTYPE is fixed for the round)
                 const unsigned a0 = __ballot_sync(0xffffffffu, lane < nchg && x.CTYPE[lane] > 0);
                 const unsigned a1 =
                     __ballot_sync(0xffffffffu, lane + 32 < nchg && x.CTYPE[lane + 32] > 0);
@@ -722,6 +757,28 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 }
             }
             __syncthreads();
+            if (t == 0) { tn = clock64(); prof[3] += tn - tc; tc = tn; }  // sort
+            // PM[k] = change indices of the k lowest lines: thread (k, half)
+            // builds one 32-bit half from the ranks (no serial scan)
+            if (t < 2 * (nchg + 1)) {
+                const int k = t >> 1, h0 = (t & 1) * 32;
+                const int hn = nchg - h0 < 32 ? nchg - h0 : 32;
+                uint32_t m = 0;
+                for (int j = 0; j < hn; j++) m |= (x.RANKS[h0 + j] < k ? 1u : 0u) << j;
+                reinterpret_cast<uint32_t*>(x.PM)[2 * k + (t & 1)] = m;
+            } else if (t >= XT - (CUMN + 1)) {  // CUMB[b]: changes with line < b << bsh
+                const int b = t - (XT - (CUMN + 1));
+                const int32_t v = (int32_t)((int64_t)b << x.bsh) < 0 ? INT32_MAX
+                                                                      : (int32_t)((int64_t)b << x.bsh);
+                int lo = 0, hi = nchg;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (x.SS[mid] < v) lo = mid + 1;
+                    else hi = mid;
+                }
+                x.CUMB[b] = lo;
+            }
+            __syncthreads();
             if (t == 0) { tn = clock64(); prof[4] += tn - tc; tc = tn; }  // resolve
             const unsigned long long addm =
                 (unsigned long long)(uint32_t)x.MISC[11] |
@@ -729,27 +786,27 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             const unsigned long long allm = nchg >= 64 ? ~0ull : ((1ull << nchg) - 1ull);
             const unsigned long long holes = (addm & ~mine & allm) | (~addm & mine & allm);
             if (sel && in) {
-                cur = resolve(x, r, holes, nchg, total, B, lb, ylo);
+                cur = resolve(x, r, holes, nchg, total, rblk, B, lb, ylo);
                 if (chg && cls == C_MU) {
                     x.FIN[pchg] = cur;
                     const int32_t u0 = x.CSLOT[pchg];
                     if (u0 != cur)  // mark the buckets the move spans
                         for (int32_t b = min(u0, cur) >> movs; b <= (max(u0, cur) >> movs); b++)
-                            atomicOr(&x.MOVB[b >> 5], 1u << (b & 31));
+                            atomicOr(&x.MOVM[b], 1ull << pchg);
                 }
             }
             __syncthreads();
             if (t == 0) { tn = clock64(); prof[5] += tn - tc; tc = tn; }  // verify
             if (t == 0) prof[7]++;
-            // the earlier MU lines this access counted, used vs found
-            bool near = false;  // a moved MU line near the lines this access looked at?
+            // the earlier MU lines this access counted, used vs found: only
+            // those whose move crossed a bucket of the lines it looked at
+            unsigned long long mu = 0;
             if (sel && in) {
-                for (int32_t b = ylo >> movs; b <= (cur >> movs) && !near; b++)
-                    near = (x.MOVB[b >> 5] >> (b & 31)) & 1u;
-                if (lb >= 0) near = near || ((x.MOVB[(lb >> movs) >> 5] >> ((lb >> movs) & 31)) & 1u);
+                for (int32_t b = ylo >> movs; b <= (cur >> movs); b++) mu |= x.MOVM[b];
+                if (lb >= 0) mu |= x.MOVM[lb >> movs];
+                mu &= ~addm & mine & allm;
             }
-            if (near) {
-                unsigned long long mu = ~addm & mine & allm;
+            if (mu) {
                 bool moved = false;
                 while (mu) {
                     const int i = __ffsll((long long)mu) - 1;
@@ -778,10 +835,14 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         {
             const int nc = x.MISC[7];
             const int32_t my = x.ANS[t], mine_prev = x.PANS[t];
-            for (int k = 0; k < nc; k++) {
-                const int32_t cl = x.CANL[k], cs = x.CANS[k];
-                if ((my == cs && t < cl) || mine_prev == cs) atomicMin(&x.MISC[1], cl);
-            }
+            const bool h1 = my >= 0 && ((x.CHB[(my >> 5) & (CHBW - 1)] >> (my & 31)) & 1u);
+            const bool h2 = mine_prev >= 0 &&
+                            ((x.CHB[(mine_prev >> 5) & (CHBW - 1)] >> (mine_prev & 31)) & 1u);
+            if (h1 || h2)  // (hash hit: compare with the candidates)
+                for (int k = 0; k < nc; k++) {
+                    const int32_t cl = x.CANL[k], cs = x.CANS[k];
+                    if ((my == cs && t < cl) || mine_prev == cs) atomicMin(&x.MISC[1], cl);
+                }
         }
         __syncthreads();
         const int E = Epre < x.MISC[1] ? Epre : x.MISC[1];
@@ -824,16 +885,16 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         }
         // committed MU lines leave T; ADD lines of accesses past the end return
         {
-            int32_t off = -1;
-            if (t < E && chg && cls == C_MU) off = cur;
-            if (t >= E && in && chg && cls == C_ADD) off = s;
-            if (off >= 0) {
-                atomicAnd(&a.safe_bits[off >> 5], ~(1u << (off & 31)));
-                atomicSub(&x.CNT[off >> 10], 1u);
-                atomicSub(&x.GCNT[off >> 9], 1u << (((off >> 7) & 3) * 8));
-                atomicOr(&x.TOUCH[off >> 20], 1u << ((off >> 15) & 31));
+            const int nc0 = x.MISC[3];
+            for (int e = wid; e < nc0; e += XW) {
+                const bool add = x.CTYPE[e] > 0, done = x.CHT[e] < E;
+                if (add == done) continue;
+                const int32_t off = add ? x.CSLOT[e] : x.FIN[e];
+                if (lane == 0) atomicAnd(&a.safe_bits[off >> 5], ~(1u << (off & 31)));
+                t_update_warp(x, off, -1, lane);
             }
         }
+        for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;  // (read in F, before the barrier above)
         // state after the last committed access
         if (t == E - 1) {
             x.MISC[4] = max(ni + d, c);              // safe count after it
@@ -843,7 +904,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         __syncthreads();
         if (t == 0) {
             tn = clock64();
-            prof[6] += tn - tc;  // G commit (its re-prefix joins the next round's)
+            prof[6] += tn - tc;  // G commit
             tc = tn;
         }
         if (E > 0) {
@@ -869,10 +930,9 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     }
     asm volatile("cp.async.wait_group 0;");
     __syncthreads();
-    rebuild(x, t);  // the last round's commit
     // write back: block / superblock counts, counters, generator state
     for (int64_t i = t; i < nb; i += XT) a.blk_cnt[i] = x.CNT[i];
-    for (int64_t sb = t; sb < ns; sb += XT) a.sup_cnt[sb] = x.STOT[sb];
+    for (int64_t sb = t; sb < ns; sb += XT) a.sup_cnt[sb] = x.SUPP[sb + 1] - x.SUPP[sb];
     hits = __reduce_add_sync(0xffffffffu, (unsigned)hits);
     misses = __reduce_add_sync(0xffffffffu, (unsigned)misses);
     byp = __reduce_add_sync(0xffffffffu, (unsigned)byp);
@@ -932,10 +992,11 @@ int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
 // shared memory of k_exact_par for a cache of L lines
 size_t gids_xp_smem_bytes(int64_t L) {
     const int64_t nb = (L + 1023) / 1024, ns = (nb + 31) / 32;
-    return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * RING + HRING + 2 * nb +
-                                       2 * ns + 1 + (ns + 31) / 32 + 2 * nb + XP_MAX_CHG + MOVW +
-                                       (GIDS_XP_CAND_CAP + 31) / 32 + 4 * XT + 4 * XP_MAX_CHG +
-                                       XW * 8 + 16);
+    return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * nb + XP_MAX_CHG + CUMN + 2 +
+                                       CHBW + 2 * RING + HRING + nb + nb + ns + 1 +
+                                       (GIDS_XP_CAND_CAP + 31) / 32 + 2 * XT + 6 * XP_MAX_CHG +
+                                       2 * XT + XW * 8 + 16 + 1) +
+           sizeof(unsigned long long) * MOVN;
 }
 
 // launched before k_exact_seq; each checks on the device which of them runs

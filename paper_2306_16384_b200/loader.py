@@ -163,6 +163,7 @@ class Dataloader:
             np.random.SeedSequence(cfg.seed).spawn(6)
         self.sharded = None
         self._storage_file = None
+        self._file_offset = self._file_page = None
         dev_graph = self._build_graph_and_features(int(graph_ss.generate_state(1)[0]),
                                                    int(feat_ss.generate_state(1)[0]))
         row_bytes = self.features.row_bytes
@@ -187,6 +188,7 @@ class Dataloader:
         elif self._storage_file is not None:
             self._h.set_storage_file(self._storage_file, HEADER_BYTES, self.spec.page_bytes,
                                      io_threads=cfg.gids_io_threads, direct=cfg.gids_io_direct)
+            self._file_offset, self._file_page = HEADER_BYTES, self.spec.page_bytes
         else:
             pinned = self.features.pinned
             self._h.set_backing(pinned if isinstance(pinned, torch.Tensor) else self.features.table,
@@ -418,24 +420,58 @@ class Dataloader:
         return FeatureStore(num_nodes=host.num_nodes, dim=host.dim, table=view, pinned=buf)
 
     def gids_init(self, offset: int = 24, cacheline_bytes: int | None = None,
-                  num_elements: int | None = None, n_ssd: int | None = None) -> dict:
-        """The GIDS init call: checks the backing-store layout.
+                  num_elements: int | None = None, n_ssd: int | None = None,
+                  path: str | None = None) -> dict:
+        """The GIDS init call: lays out the backing store
+        before the first batch.
 
-        offset: byte offset of row 0 in the backing file (the .gfea header is
-        24 B, graph.py:304-309); cacheline_bytes: cache line (page) size;
-        num_elements: N * dim fp32 elements.  Returns the resolved layout."""
-        layout = {"offset": 24, "cacheline_bytes": self.spec.page_bytes,
-                  "num_elements": self.graph.num_nodes * self.features.dim,
-                  "n_ssd": self.spec.n_ssd, "row_bytes": self.features.row_bytes,
-                  "storage": "file" if self._storage_file else
-                             ("hbm-sharded" if self.sharded else "pinned"),
-                  "path": self._storage_file}
-        for key, val in (("offset", offset), ("cacheline_bytes", cacheline_bytes),
-                         ("num_elements", num_elements), ("n_ssd", n_ssd)):
-            if val is not None and val != layout[key]:
-                raise ConfigError(f"gids_init {key}={val} disagrees with the loader "
-                                  f"({layout[key]})")
-        return layout
+        path: serve the storage tier from this file -- fp32 rows of ``dim``
+        elements from byte ``offset`` (24 = the .gfea header, graph.py:304-309;
+        0 = a raw row dump), read in pages of ``cacheline_bytes`` through the
+        page-coalescing accumulator (csrc/storage_file.cu); without a path an
+        existing file tier is re-laid-out with the given offset / page.
+        num_elements: N * dim, checked against the graph and the table.
+        n_ssd: devices the storage tier stripes over -- the accumulator's
+        saturation threshold (storage.py:92-104) and the fetch clock scale
+        with it (SsdSpec.n_ssd).  Arguments left None keep the current value.
+        Returns the resolved layout."""
+        import dataclasses
+        if self._iteration > 0 or self._pending or self._spec:
+            raise ConfigError("gids_init configures the backing store before the first batch")
+        n, dim, rb = self.graph.num_nodes, self.features.dim, self.features.row_bytes
+        if num_elements is not None and num_elements != n * dim:
+            raise ConfigError(f"gids_init num_elements={num_elements} disagrees with the "
+                              f"loader ({n * dim} = {n} nodes x {dim})")
+        if offset < 0:
+            raise ConfigError("gids_init offset must be non-negative")
+        if n_ssd is not None:
+            if n_ssd < 1:
+                raise ConfigError("gids_init n_ssd must be >= 1")
+            self.spec = dataclasses.replace(self.spec, n_ssd=int(n_ssd))
+            self.base_threshold = required_accesses(self.spec, self.cfg.target_fraction)
+        page = int(cacheline_bytes) if cacheline_bytes is not None else self.spec.page_bytes
+        if rb > page:
+            raise InfeasibleError(f"feature row ({rb} B) exceeds one cache line / page "
+                                  f"({page} B)")
+        if path is not None or (self._storage_file is not None and
+                                (offset != self._file_offset or page != self._file_page)):
+            if self.sharded is not None:
+                raise ConfigError("the HBM-sharded table has no backing file")
+            target = str(path) if path is not None else self._storage_file
+            if os.path.getsize(target) < offset + n * rb:
+                raise ConfigError(f"{target}: shorter than offset + {n} rows x {rb} B")
+            self._h.set_storage_file(target, offset, page, io_threads=self.cfg.gids_io_threads,
+                                     direct=self.cfg.gids_io_direct)
+            table = np.memmap(target, dtype=np.float32, mode="r", offset=offset, shape=(n, dim))
+            self.features = FeatureStore(num_nodes=n, dim=dim, table=table,
+                                         seed=self.features.seed)
+            self._storage_file, self._file_offset, self._file_page = target, offset, page
+        return {"offset": self._file_offset if self._storage_file else offset,
+                "cacheline_bytes": self._file_page if self._storage_file else page,
+                "num_elements": n * dim, "n_ssd": self.spec.n_ssd, "row_bytes": rb,
+                "storage": "file" if self._storage_file else
+                           ("hbm-sharded" if self.sharded else "pinned"),
+                "path": self._storage_file, "base_threshold": self.base_threshold}
 
     # -- run-ahead accumulator (dataloader.py:184-228)
     def effective_threshold(self) -> int:

@@ -114,3 +114,39 @@ def test_gpu_file_tier_direct_io_matches_pinned_tier(tmp_path):
     assert st["pages"] > 0 and st["bytes"] == st["pages"] * 4096
     dl.close()
     ref.close()
+
+
+def test_gpu_gids_init_lays_out_the_backing_store(tmp_path):
+    """The GIDS init call configures the store: a raw row dump
+    at a 4 KiB offset, 4 KiB cache-line pages, two SSDs.  The loader then
+    serves exactly what a loader configured that way from the start serves
+    (rows, tiers, CSV rows -- n_ssd moves the accumulator threshold and the
+    clock), and the call is refused once a batch has been served or when
+    the element count disagrees."""
+    from paper_2306_16384_b200 import ConfigError
+    fx = fixture("alltiers")
+    want = Dataloader(config_of(fx, n_ssd=2))
+    dl = Dataloader(config_of(fx))
+    n, dim = dl.graph.num_nodes, dl.features.dim
+    raw = tmp_path / "rows.bin"
+    with open(raw, "wb") as fh:
+        fh.write(b"\0" * 4096)
+        fh.write(np.ascontiguousarray(dl.features.table, np.float32).tobytes())
+    with pytest.raises(ConfigError):
+        dl.gids_init(offset=4096, num_elements=n * dim + 1, path=str(raw))
+    one_ssd = dl.base_threshold
+    lay = dl.gids_init(offset=4096, cacheline_bytes=4096, num_elements=n * dim, n_ssd=2,
+                       path=str(raw))
+    assert lay["storage"] == "file" and lay["offset"] == 4096 and lay["n_ssd"] == 2
+    assert lay["base_threshold"] == want.base_threshold == 2 * one_ssd
+    for b in range(6):
+        mb, rows, st = dl.next_batch()
+        mb2, rows2, st2 = want.next_batch()
+        assert np.array_equal(mb.unique_nodes.cpu().numpy(), mb2.unique_nodes.cpu().numpy())
+        assert np.array_equal(rows.cpu().numpy(), rows2.cpu().numpy()), b
+        assert st.csv_row() == st2.csv_row(), b
+    assert dl.storage_stats()["pages"] > 0
+    with pytest.raises(ConfigError):
+        dl.gids_init(offset=4096)
+    dl.close()
+    want.close()

@@ -1,17 +1,9 @@
 cd $GRAFT_REPO_ROOT
-for v in "" "GIDS_PRIORITY=ctl"; do
-env $v GIDS_TRACE_HOST=1 timeout 600 python bench.py --workload c3 --policy exact --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/c3_tl.json 2>&1
+timeout 900 python -m pytest tests/test_gpu_exact_par.py -q -x 2>&1 | tail -3
+timeout 900 python bench.py --workload c4 --policy exact --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_exact.json 2> gpurun_out/c4_exact.err
 python - <<'P'
 import json
-d=json.loads(open("gpurun_out/c3_tl.json").read().strip().splitlines()[-1])
-print(d["value"], d["phase_ms_per_step"]); print(d["e2e_timeline_ms"])
+d=json.loads(open("gpurun_out/c4_exact.json").read().strip().splitlines()[-1])
+print(d["value"], d["phase_ms_per_step"]); x=d["exact_par"]; b=x["batches"]
+print({k:(round(v/x["rounds"]) if k.startswith("cyc") else v) for k,v in x.items()})
 P
-done
-GIDS_TRACE_HOST=1 timeout 600 python bench.py --workload c3 --policy setassoc --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/c3_tl.json 2>&1
-python - <<'P'
-import json
-d=json.loads(open("gpurun_out/c3_tl.json").read().strip().splitlines()[-1])
-print(d["value"], d["phase_ms_per_step"]); print(d["e2e_timeline_ms"])
-P
-timeout 600 python -m pytest tests/test_gpu_cache_api.py tests/test_gpu_loader.py -q -x 2>&1 | tail -3
-timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x 2>&1 | tail -5
