@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // exactly, and another pass run (rare: the moves are short)
         const unsigned long long mine = pchg >= 64 ? ~0ull : ((1ull << pchg) - 1ull);
         for (int pass = 0; pass <= XP_MAX_CHG + 1; pass++) {
-            __syncthreads();
+            if (pass > 0) __syncthreads();  // (pass 0: the first selects' barrier)
             // sort the change lines (rank sort), then the prefix masks
             {  // rank of change e = t / 8 among the changes of slice t % 8
                 const int e = t >> 3, part = t & 7;
@@ -827,14 +827,14 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             prof[5] += tn - tc;
             tc = tn;
         }
-        x.ANS[t] = (sel && in) ? cur : -1;
-        __syncthreads();
         // ---------------- F: a candidate whose line an earlier eviction took
         // (each access checks its own answer of this and the previous round
         // against the round's few candidates)
+        int32_t pans = -1;  // this thread's answer, for the next round's F
         {
             const int nc = x.MISC[7];
-            const int32_t my = x.ANS[t], mine_prev = x.PANS[t];
+            const int32_t my = (sel && in) ? cur : -1, mine_prev = x.PANS[t];
+            pans = my;
             const bool h1 = my >= 0 && ((x.CHB[(my >> 5) & (CHBW - 1)] >> (my & 31)) & 1u);
             const bool h2 = mine_prev >= 0 &&
                             ((x.CHB[(mine_prev >> 5) & (CHBW - 1)] >> (mine_prev & 31)) & 1u);
@@ -912,7 +912,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             kpos += x.MISC[5];
             nlog += x.MISC[6];
         }
-        x.PANS[t] = t < E ? x.ANS[t] : -1;
+        x.PANS[t] = t < E ? pans : -1;
         pos += E;
         // refill the rings past the consumed prefix
         {
