@@ -218,10 +218,11 @@ __device__ __forceinline__ int bit_select(uint32_t w, uint32_t k) {
 // the 128-line group of T an access last selected in: its four bitmap words
 // (one 16-B load from the L2-resident bitmap), rank base and count
 struct Grp {
-    int64_t g;      // block, -1 none
-    int grp;        // group within the block
+    int32_t gi;     // group (line >> 7), -1 none
     uint32_t base, cnt;
     uint4 w;
+    uint32_t cnt2;  // the next group, prefetched with it (0: none)
+    uint4 w2;
 };
 
 // the k-th set bit of the held group
@@ -246,7 +247,7 @@ __device__ __forceinline__ int32_t sel_grp(const Grp& G, uint32_t k) {
             }
         }
     }
-    return (int32_t)(G.g * 1024) + G.grp * 128 + wi * 32 + bit_select(w, k);
+    return G.gi * 128 + wi * 32 + bit_select(w, k);
 }
 
 // hold the 128-line group of T holding rank q (its words are loaded, not
@@ -254,40 +255,58 @@ __device__ __forceinline__ int32_t sel_grp(const Grp& G, uint32_t k) {
 __device__ __forceinline__ void find_grp(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
     int64_t g = -1;
     uint32_t base = 0;
-    if (G.g >= 0) {
-        base = pb(x, G.g);
-        if (q >= base && q < base + x.CNT[G.g]) g = G.g;
+    if (G.gi >= 0) {
+        base = pb(x, G.gi >> 3);
+        if (q >= base && q < base + x.CNT[G.gi >> 3]) g = G.gi >> 3;
     }
     if (g < 0) {
         g = locate(x, q, total);
         base = pb(x, g);
     }
     const uint2 cc = *reinterpret_cast<const uint2*>(x.GCNT + 2 * g);
-    const uint32_t rr = q - base;
-    uint32_t acc = 0, accb = 0, cg = 0;
-    int grp = 0;
-    bool got = false;
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-        const uint32_t cj = ((j < 4 ? cc.x : cc.y) >> ((j & 3) * 8)) & 0xffu;
-        if (!got && acc + cj > rr) {
-            grp = j;
-            accb = acc;
-            cg = cj;
-            got = true;
-        }
-        acc += cj;
-    }
-    G.g = g;
-    G.grp = grp;
+    // the group of in-block rank rr: a 3-step search over the byte counts
+    // (dp4a sums four bytes)
+    uint32_t rem = q - base;
+    const uint32_t s4 = __dp4a(cc.x, 0x01010101u, 0u);
+    const bool h4 = rem >= s4;
+    uint32_t w = h4 ? cc.y : cc.x, accb = h4 ? s4 : 0u;
+    rem -= h4 ? s4 : 0u;
+    const uint32_t s2 = (w & 0xffu) + ((w >> 8) & 0xffu);
+    const bool h2 = rem >= s2;
+    w = h2 ? (w >> 16) : w;
+    accb += h2 ? s2 : 0u;
+    rem -= h2 ? s2 : 0u;
+    const uint32_t c0 = w & 0xffu;
+    const bool h1 = rem >= c0;
+    const int grp = (h4 ? 4 : 0) + (h2 ? 2 : 0) + (h1 ? 1 : 0);
+    accb += h1 ? c0 : 0u;
+    G.gi = (int32_t)(g * 8 + grp);
     G.base = base + accb;
-    G.cnt = cg;
-    G.w = __ldcg(reinterpret_cast<const uint4*>(x.gbits + g * 32 + grp * 4));
+    G.cnt = h1 ? ((w >> 8) & 0xffu) : c0;
+    G.w = __ldcg(reinterpret_cast<const uint4*>(x.gbits) + G.gi);
+    // and the next group: a fixed point moves up by the few holes below, so
+    // its answer is usually here or there
+    const int32_t gn = G.gi + 1;
+    G.cnt2 = 0;
+    if (gn < (int32_t)(x.nb * 8)) {
+        G.cnt2 = (x.GCNT[gn >> 2] >> ((gn & 3) * 8)) & 0xffu;
+        G.w2 = __ldcg(reinterpret_cast<const uint4*>(x.gbits) + gn);
+    }
 }
 
 // the q-th line of T (the held group is reused when it covers q)
 __device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
-    if (!(G.g >= 0 && q - G.base < G.cnt)) find_grp(x, q, total, G);
+    if (!(G.gi >= 0 && q - G.base < G.cnt)) {
+        if (G.gi >= 0 && q - G.base - G.cnt < G.cnt2 && q >= G.base + G.cnt) {  // the next group
+            G.base += G.cnt;
+            G.cnt = G.cnt2;
+            G.w = G.w2;
+            G.gi += 1;
+            G.cnt2 = 0;
+        } else {
+            find_grp(x, q, total, G);
+        }
+    }
     return sel_grp(G, q - G.base);
 }
 
@@ -469,6 +488,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     }
     for (int64_t i = t; i < (a.cand_cap + 31) / 32; i += XT) x.CONV[i] = 0u;
     for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;
+    for (int i = t; i < MOVN; i += XT) x.MOVM[i] = 0ull;
     x.PANS[t] = -1;
     // stage the first accesses and halves
     int64_t efill = n < RING ? n : RING;
@@ -697,7 +717,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         const int nchg = x.MISC[3];
         const uint32_t total = x.SUPP[ns];
         Grp B;
-        B.g = -1;
+        B.gi = -1;
         int32_t cur = -1, ylo = -1, lb = -1;
         int64_t rblk = 0;
         if (sel && in) {
@@ -705,10 +725,9 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             // an MU access's first approximation of its line is interpolated
             // inside that group (no wait: the fixed point corrects it)
             find_grp(x, r, total, B);
-            rblk = B.g;
+            rblk = B.gi >> 3;
             if (chg && cls == C_MU)
-                x.CSLOT[pchg] = (int32_t)(B.g * 1024) + B.grp * 128 +
-                                (int32_t)(((r - B.base) * 128u) / (B.cnt ? B.cnt : 1u));
+                x.CSLOT[pchg] = B.gi * 128 + (int32_t)(((r - B.base) * 128u) / (B.cnt ? B.cnt : 1u));
         }
         __syncthreads();
         if (t == 0) {
@@ -723,6 +742,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // range of lines its fixed-point iteration looked at -- checked
         // exactly, and another pass run (rare: the moves are short)
         const unsigned long long mine = pchg >= 64 ? ~0ull : ((1ull << pchg) - 1ull);
+        int32_t mlo = 0, mhi = -1;  // buckets this MU marked in MOVM (cleared after use)
         for (int pass = 0; pass <= XP_MAX_CHG + 1; pass++) {
             if (pass > 0) __syncthreads();  // (pass 0: the first selects' barrier)
             // sort the change lines (rank sort), then the prefix masks
@@ -746,7 +766,6 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (e < nchg && part == 2) x.RANKS[e] = rk;
             }
             if (t == 0) x.MISC[10] = 0;
-            for (int i = t; i < MOVN; i += XT) x.MOVM[i] = 0ull;
             if (pass == 0 && wid == XW - 1) {  // ADD mask (CTYPE is fixed for the round)
                 const unsigned a0 = __ballot_sync(0xffffffffu, lane < nchg && x.CTYPE[lane] > 0);
                 const unsigned a1 =
@@ -790,9 +809,11 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (chg && cls == C_MU) {
                     x.FIN[pchg] = cur;
                     const int32_t u0 = x.CSLOT[pchg];
-                    if (u0 != cur)  // mark the buckets the move spans
-                        for (int32_t b = min(u0, cur) >> movs; b <= (max(u0, cur) >> movs); b++)
-                            atomicOr(&x.MOVM[b], 1ull << pchg);
+                    if (u0 != cur) {  // mark the buckets the move spans
+                        mlo = min(u0, cur) >> movs;
+                        mhi = max(u0, cur) >> movs;
+                        for (int32_t b = mlo; b <= mhi; b++) atomicOr(&x.MOVM[b], 1ull << pchg);
+                    }
                 }
             }
             __syncthreads();
@@ -819,6 +840,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (moved) x.MISC[10] = 1;
             }
             __syncthreads();
+            for (int32_t b = mlo; b <= mhi; b++) x.MOVM[b] = 0ull;  // (read above, all done)
+            mhi = -1;
             if (!x.MISC[10]) break;
             if (chg && in && cls == C_MU) x.CSLOT[pchg] = cur;  // next pass
         }
