@@ -373,11 +373,12 @@ class Handle:
         return int(lib().gids_exact_par_batches(self.h))
 
     def exact_par_stats(self) -> dict:
-        out = np.zeros(12, np.int64)
+        out = np.zeros(16, np.int64)
         check(lib().gids_exact_par_stats(self.h, out.ctypes.data), "exact_par_stats")
         return dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line",
                          "cyc_draws", "cyc_tables", "cyc_first_select", "cyc_sort",
-                         "cyc_resolve", "cyc_verify", "cyc_commit", "fixpoint_passes"),
+                         "cyc_masks", "cyc_resolve", "cyc_lost_lines", "fixpoint_passes",
+                         "cyc_verify", "cyc_commit", "cyc_ring", "cyc_spare"),
                         out.tolist()), batches=self.exact_par_batches())
 
 

@@ -585,7 +585,7 @@ int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {
     if (!h->counts_read && c.xp_done) {
         h->xp_batches++;
         for (int i = 0; i < 4; i++) h->xp_stats[i] += c.xp_stats[i];
-        for (int i = 0; i < 8; i++) h->xp_stats[4 + i] += c.xp_prof[i];
+        for (int i = 0; i < 12; i++) h->xp_stats[4 + i] += c.xp_prof[i];
     }
     h->counts_read = true;
     out->sampled = h->last_serve_n;
@@ -707,7 +707,7 @@ int64_t gids_launch_count(gids_handle* h) { return h ? h->launches : -1; }
 int64_t gids_exact_par_batches(gids_handle* h) { return h ? h->xp_batches : -1; }
 int gids_exact_par_stats(gids_handle* h, int64_t out[12]) {
     CHECK_H(h);
-    for (int i = 0; i < 12; i++) out[i] = h->xp_stats[i];
+    for (int i = 0; i < 16; i++) out[i] = h->xp_stats[i];
     return GIDS_OK;
 }
 

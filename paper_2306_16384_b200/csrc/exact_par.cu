@@ -58,7 +58,7 @@ constexpr int RING_LAG = 12;      // commit groups allowed in flight when a roun
 constexpr int32_t NEG = -(1 << 29);
 constexpr int MOVN = 2048;        // moved-line filter: buckets (lines >> movs)
 constexpr int CUMN = 256;         // change-line buckets of count_le (lines >> bsh)
-constexpr int CHBW = 128;         // candidate-line hash: 4096 bits
+constexpr int HSZ = 1024;         // candidate hash table (line -> lane), open addressing
 
 enum { C_STAY = GIDS_XC_STAY, C_ADD = GIDS_XC_ADD, C_CAND = GIDS_XC_CAND, C_M0 = GIDS_XC_M0,
        C_MU = GIDS_XC_MU };
@@ -147,7 +147,8 @@ struct Xs {
     int32_t* FIN;     // [XP_MAX_CHG] MU lines found by the current pass
     unsigned long long* MOVM;  // [MOVN] per bucket: MU changes whose move crossed it (this pass)
     int32_t* CUMB;    // [CUMN+1] changes with line < (b << bsh), b = 0..CUMN
-    uint32_t* CHB;    // [CHBW] hash of the round's candidate lines
+    int32_t* CHK;     // [HSZ] candidate lines of the round (-1 empty)
+    int32_t* CHV;     // [HSZ] their lanes
     uint32_t* REV;    // [RING]
     uint32_t* RCL;    // [RING]
     uint32_t* RH;     // [HRING]
@@ -160,40 +161,38 @@ struct Xs {
     int32_t* RANKS;   // [XP_MAX_CHG] rank of each change (by line)
     int32_t* CHT;     // [XP_MAX_CHG] the access (thread) of each change
     unsigned long long* PM;  // [XP_MAX_CHG+1] change-index mask of the k lowest lines
-    int32_t* CANL;    // [XT] lanes of this round's unconverted candidates
-    int32_t* CANS;    // [XT] their lines
     int32_t* W;       // [XW * 8] warp partials
     int32_t* MISC;    // [16]
-    int64_t nb, ns, L;
+    int32_t nb, ns, L;  // (a cache of L < 2^31 lines: int32 index math throughout)
     int bsh;
     const uint32_t* gbits;
 };
 
-__device__ __forceinline__ uint32_t pb(const Xs& x, int64_t g) { return x.SUPP[g >> 5] + x.BLKP[g]; }
+__device__ __forceinline__ uint32_t pb(const Xs& x, int32_t g) { return x.SUPP[g >> 5] + x.BLKP[g]; }
 
 // block holding the r-th line of T (r < total): interpolated guess, then
 // steps sized by the mean block count (float arithmetic: only a guess)
-__device__ int64_t locate(const Xs& x, uint32_t r, uint32_t total) {
-    const int64_t nb = x.nb;
+__device__ int32_t locate(const Xs& x, uint32_t r, uint32_t total) {
+    const int32_t nb = x.nb;
     const float per = __fdividef((float)nb, (float)total);  // blocks per line
-    int64_t g = (int64_t)((float)r * per);
+    int32_t g = (int32_t)((float)r * per);
     if (g >= nb) g = nb - 1;
     if (g < 0) g = 0;
     for (int it = 0; it < 6; it++) {
         const uint32_t base = pb(x, g), c = x.CNT[g];
         if (r < base) {
-            const int64_t st = (int64_t)((float)(base - r) * per) + 1;
+            const int32_t st = (int32_t)((float)(base - r) * per) + 1;
             g = g - st < 0 ? 0 : g - st;
         } else if (r >= base + c) {
-            const int64_t st = (int64_t)((float)(r - base - c) * per) + 1;
+            const int32_t st = (int32_t)((float)(r - base - c) * per) + 1;
             g = g + st >= nb ? nb - 1 : g + st;
         } else {
             return g;
         }
     }
-    int64_t lo = 0, hi = nb - 1;  // largest g with pb(g) <= r
+    int32_t lo = 0, hi = nb - 1;  // largest g with pb(g) <= r
     while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
+        const int32_t mid = (lo + hi + 1) >> 1;
         if (pb(x, mid) <= r) lo = mid;
         else hi = mid - 1;
     }
@@ -253,7 +252,7 @@ __device__ __forceinline__ int32_t sel_grp(const Grp& G, uint32_t k) {
 // hold the 128-line group of T holding rank q (its words are loaded, not
 // waited for: the first use waits)
 __device__ __forceinline__ void find_grp(const Xs& x, uint32_t q, uint32_t total, Grp& G) {
-    int64_t g = -1;
+    int32_t g = -1;
     uint32_t base = 0;
     if (G.gi >= 0) {
         base = pb(x, G.gi >> 3);
@@ -310,6 +309,18 @@ __device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total
     return sel_grp(G, q - G.base);
 }
 
+__device__ __forceinline__ uint32_t chash(int32_t line) {
+    return ((uint32_t)line * 0x9E3779B1u) >> (32 - 10);  // HSZ = 2^10
+}
+// lane of the round's candidate whose line this is, -1 none
+__device__ __forceinline__ int32_t cand_lane(const Xs& x, int32_t line) {
+    for (uint32_t h = chash(line);; h = (h + 1) & (HSZ - 1)) {
+        const int32_t k = x.CHK[h];
+        if (k == line) return x.CHV[h];
+        if (k < 0) return -1;
+    }
+}
+
 // lines among the round's changes <= y: the bucket's start, then the few
 // changes inside the bucket
 __device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
@@ -322,15 +333,15 @@ __device__ __forceinline__ int count_le(const Xs& x, int m, int32_t y) {
 // prefix levels, updated in place by one warp (a lane per prefix entry;
 // the round's changes are spread over the warps)
 __device__ __forceinline__ void t_update_warp(const Xs& x, int32_t s, int delta, int lane) {
-    const int64_t g = s >> 10, sb = g >> 5;
+    const int32_t g = s >> 10, sb = g >> 5;
     const uint32_t d = (uint32_t)delta;
     if (lane == 0) {
         atomicAdd(&x.CNT[g], d);
         atomicAdd(&x.GCNT[s >> 9], d << (((s >> 7) & 3) * 8));
     }
-    const int64_t ge = (sb + 1) * 32 < x.nb ? (sb + 1) * 32 : x.nb;
+    const int32_t ge = (sb + 1) * 32 < x.nb ? (sb + 1) * 32 : x.nb;
     if (g + 1 + lane < ge) atomicAdd(&x.BLKP[g + 1 + lane], d);
-    for (int64_t u = sb + 1 + lane; u <= x.ns; u += 32) atomicAdd(&x.SUPP[u], d);
+    for (int32_t u = sb + 1 + lane; u <= x.ns; u += 32) atomicAdd(&x.SUPP[u], d);
 }
 
 // the r-th line of T minus `holes` (a mask over the change list): the least
@@ -340,7 +351,7 @@ __device__ __forceinline__ void t_update_warp(const Xs& x, int32_t s, int delta,
 // answer, one bitmap load.  The hole counts it used: at line lb, and at the
 // lines of [ylo, answer].
 __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned long long holes,
-                                           int m, uint32_t total, int64_t rblk, Grp& B,
+                                           int m, uint32_t total, int32_t rblk, Grp& B,
                                            int32_t& lb, int32_t& ylo) {
     if (!holes) {
         const int32_t y = sel_T(x, r, total, B);
@@ -348,7 +359,7 @@ __device__ __forceinline__ int32_t resolve(const Xs& x, uint32_t r, unsigned lon
         lb = -1;
         return y;
     }
-    lb = (int32_t)(rblk * 1024) - 1;  // (rblk: the block of T's r-th line)
+    lb = rblk * 1024 - 1;  // (rblk: the block of T's r-th line)
     uint32_t q = r + (lb >= 0 ? (uint32_t)__popcll(x.PM[count_le(x, m, lb)] & holes) : 0u);
     int32_t y = sel_T(x, q, total, B);
     ylo = y;
@@ -389,10 +400,10 @@ __device__ void prefix_all(const Xs& x, int t) {
     __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t get_half(const Xs& x, const XpArgs& a, int64_t k,
-                                             int64_t kfill) {
+__device__ __forceinline__ uint32_t get_half(const Xs& x, const XpArgs& a, int32_t k,
+                                             int32_t kfill) {
     if (k < kfill && k >= kfill - HRING) return x.RH[k & (HRING - 1)];
-    if (k < a.hcap) return __ldcg(a.H + k);
+    if (k < (int32_t)a.hcap) return __ldcg(a.H + k);
     return half_direct(a.meta, k);
 }
 
@@ -415,8 +426,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const unsigned below = (1u << lane) - 1u;
     Xs x;
-    x.L = a.L;
-    x.nb = (a.L + 1023) >> 10;
+    x.L = (int32_t)a.L;
+    x.nb = (int32_t)((a.L + 1023) >> 10);
     x.ns = (x.nb + 31) >> 5;
     x.gbits = a.safe_bits;
     {
@@ -429,8 +440,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += XP_MAX_CHG;
         x.CUMB = reinterpret_cast<int32_t*>(p);
         p += CUMN + 2;
-        x.CHB = p;
-        p += CHBW;
+        x.CHK = reinterpret_cast<int32_t*>(p);
+        p += HSZ;
+        x.CHV = reinterpret_cast<int32_t*>(p);
+        p += HSZ;
         x.REV = p;
         p += RING;
         x.RCL = p;
@@ -461,10 +474,6 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += XP_MAX_CHG;
         x.CHT = reinterpret_cast<int32_t*>(p);
         p += XP_MAX_CHG;
-        x.CANL = reinterpret_cast<int32_t*>(p);
-        p += XT;
-        x.CANS = reinterpret_cast<int32_t*>(p);
-        p += XT;
         x.W = reinterpret_cast<int32_t*>(p);
         p += XW * 8;
         x.MISC = reinterpret_cast<int32_t*>(p);
@@ -474,7 +483,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     }
     x.bsh = 0;
     while (((x.L - 1) >> x.bsh) >= CUMN) x.bsh++;
-    const int64_t n = a.n, nb = x.nb, ns = x.ns;
+    const int32_t n = (int32_t)a.n, nb = x.nb, ns = x.ns;  // (n <= serve_cap < 2^31)
+    const int32_t hcap = (int32_t)a.hcap;
     for (int64_t i = t; i < nb; i += XT) x.CNT[i] = a.blk_cnt[i];
     for (int64_t i = t; i < 2 * nb; i += XT) {  // four 128-line group counts per word
         const uint4* src = reinterpret_cast<const uint4*>(a.safe_bits + i * 16);
@@ -487,17 +497,17 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         x.GCNT[i] = packed;
     }
     for (int64_t i = t; i < (a.cand_cap + 31) / 32; i += XT) x.CONV[i] = 0u;
-    for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;
+    for (int i = t; i < HSZ; i += XT) x.CHK[i] = -1;
     for (int i = t; i < MOVN; i += XT) x.MOVM[i] = 0ull;
     x.PANS[t] = -1;
     // stage the first accesses and halves
-    int64_t efill = n < RING ? n : RING;
-    int64_t kfill = a.hcap < HRING ? a.hcap : HRING;
-    for (int64_t i = t; i < efill; i += XT) {
+    int32_t efill = n < RING ? n : RING;
+    int32_t kfill = hcap < HRING ? hcap : HRING;
+    for (int32_t i = t; i < efill; i += XT) {
         stage(&x.REV[i & (RING - 1)], a.ev + i);
         stage(&x.RCL[i & (RING - 1)], a.xcls + i);
     }
-    for (int64_t i = t; i < kfill; i += XT) stage(&x.RH[i & (HRING - 1)], a.H + i);
+    for (int32_t i = t; i < kfill; i += XT) stage(&x.RH[i & (HRING - 1)], a.H + i);
     asm volatile("cp.async.commit_group;");
     asm volatile("cp.async.wait_group 0;");
     __syncthreads();
@@ -505,22 +515,22 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
 
     int movs = 0;  // moved-line filter: MOVN buckets over the lines
     while (((x.L - 1) >> movs) >= MOVN) movs++;
-    int64_t pos = 0, kpos = 0, nlog = 0;
+    int32_t pos = 0, kpos = 0, nlog = 0;
     int32_t nsafe = (int32_t)a.meta->safe_count;
     int32_t pend_cidx = -1;  // cand_of_slot of this thread's last committed eviction
     int64_t hits = 0, misses = 0, byp = 0;
     int64_t st_rounds = 0, st_rej = 0, st_chg = 0, st_conv = 0;  // round ends (thread 0)
-    long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // cycles per phase, D passes (thread 0)
+    long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // cycles per phase, passes (thread 0)
     long long tc = clock64();
 
     while (pos < n) {
         asm volatile("cp.async.wait_group %0;" ::"n"(RING_LAG));
         __syncthreads();
         long long tn = clock64();
-        prof[6] += tn - tc;  // (ring wait + refill: with G)
+        prof[10] += tn - tc;  // (ring wait + refill: with G)
         tc = tn;
         // ---------------- A: classify, saturating safe-count prefix, draw prefix
-        const int64_t p = pos + t;
+        const int32_t p = pos + t;
         const bool valid = p < n;
         const uint32_t e = valid ? x.REV[p & (RING - 1)] : 0u;
         const uint32_t xc = valid ? x.RCL[p & (RING - 1)] : 0u;
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         uint32_t r = 0;
         int extra = 0;
         if (dr) {
-            const int64_t k = kpos + pdr;
+            const int32_t k = kpos + pdr;
             uint64_t m = (uint64_t)get_half(x, a, k, kfill) * (uint32_t)ni;
             uint32_t left = (uint32_t)m;
             if (left < (uint32_t)ni) {
@@ -697,10 +707,11 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             }
         }
         if (valid && in && cls == C_CAND && !conv) {
-            const int k = atomicAdd(&x.MISC[7], 1);
-            x.CANL[k] = t;
-            x.CANS[k] = s;
-            atomicOr(&x.CHB[(s >> 5) & (CHBW - 1)], 1u << (s & 31));
+            for (uint32_t h = chash(s);; h = (h + 1) & (HSZ - 1))
+                if (atomicCAS(&x.CHK[h], -1, s) == -1) {
+                    x.CHV[h] = t;
+                    break;
+                }
         }
         __syncthreads();
         {  // the round's ADD lines join T's tables
@@ -719,7 +730,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         Grp B;
         B.gi = -1;
         int32_t cur = -1, ylo = -1, lb = -1;
-        int64_t rblk = 0;
+        int32_t rblk = 0;
         if (sel && in) {
             // the group of T's r-th line: its load overlaps the change sort;
             // an MU access's first approximation of its line is interpolated
@@ -847,7 +858,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         }
         if (t == 0) {
             tn = clock64();
-            prof[5] += tn - tc;
+            prof[8] += tn - tc;
             tc = tn;
         }
         // ---------------- F: a candidate whose line an earlier eviction took
@@ -855,17 +866,16 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // against the round's few candidates)
         int32_t pans = -1;  // this thread's answer, for the next round's F
         {
-            const int nc = x.MISC[7];
             const int32_t my = (sel && in) ? cur : -1, mine_prev = x.PANS[t];
             pans = my;
-            const bool h1 = my >= 0 && ((x.CHB[(my >> 5) & (CHBW - 1)] >> (my & 31)) & 1u);
-            const bool h2 = mine_prev >= 0 &&
-                            ((x.CHB[(mine_prev >> 5) & (CHBW - 1)] >> (mine_prev & 31)) & 1u);
-            if (h1 || h2)  // (hash hit: compare with the candidates)
-                for (int k = 0; k < nc; k++) {
-                    const int32_t cl = x.CANL[k], cs = x.CANS[k];
-                    if ((my == cs && t < cl) || mine_prev == cs) atomicMin(&x.MISC[1], cl);
-                }
+            if (my >= 0) {
+                const int32_t cl = cand_lane(x, my);
+                if (cl > t) atomicMin(&x.MISC[1], cl);
+            }
+            if (mine_prev >= 0) {
+                const int32_t cl = cand_lane(x, mine_prev);
+                if (cl >= 0) atomicMin(&x.MISC[1], cl);
+            }
         }
         __syncthreads();
         const int E = Epre < x.MISC[1] ? Epre : x.MISC[1];
@@ -894,7 +904,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 kd = GIDS_KIND_MISS;
                 ln = cur;
                 misses++;
-                const int64_t li = nlog + psel;
+                const int32_t li = nlog + psel;
                 a.log_line[li] = cur;
                 a.log_pos[li] = (int32_t)p;
                 pend_cidx = __ldcg(a.cand_of_slot + cur);
@@ -917,7 +927,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 t_update_warp(x, off, -1, lane);
             }
         }
-        for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;  // (read in F, before the barrier above)
+        for (int i = t; i < HSZ; i += XT) x.CHK[i] = -1;  // (read in F, before the barrier above)
         // state after the last committed access
         if (t == E - 1) {
             x.MISC[4] = max(ni + d, c);              // safe count after it
@@ -927,7 +937,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         __syncthreads();
         if (t == 0) {
             tn = clock64();
-            prof[6] += tn - tc;  // G commit
+            prof[9] += tn - tc;  // G commit
             tc = tn;
         }
         if (E > 0) {
@@ -939,14 +949,14 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         pos += E;
         // refill the rings past the consumed prefix
         {
-            const int64_t etop = (pos + RING) < n ? pos + RING : n;
-            for (int64_t i = efill + t; i < etop; i += XT) {
+            const int32_t etop = (pos + RING) < n ? pos + RING : n;
+            for (int32_t i = efill + t; i < etop; i += XT) {
                 stage(&x.REV[i & (RING - 1)], a.ev + i);
                 stage(&x.RCL[i & (RING - 1)], a.xcls + i);
             }
             efill = etop > efill ? etop : efill;
-            const int64_t ktop = (kpos + HRING) < a.hcap ? kpos + HRING : a.hcap;
-            for (int64_t i = kfill + t; i < ktop; i += XT) stage(&x.RH[i & (HRING - 1)], a.H + i);
+            const int32_t ktop = (kpos + HRING) < hcap ? kpos + HRING : hcap;
+            for (int32_t i = kfill + t; i < ktop; i += XT) stage(&x.RH[i & (HRING - 1)], a.H + i);
             kfill = ktop > kfill ? ktop : kfill;
             asm volatile("cp.async.commit_group;");
         }
@@ -991,7 +1001,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         a.svc->xp_stats[1] = st_rej;
         a.svc->xp_stats[2] = st_chg;
         a.svc->xp_stats[3] = st_conv;
-        for (int i = 0; i < 8; i++) a.svc->xp_prof[i] = prof[i];
+        for (int i = 0; i < 12; i++) a.svc->xp_prof[i] = prof[i];
     }
 }
 
@@ -1016,9 +1026,9 @@ int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
 size_t gids_xp_smem_bytes(int64_t L) {
     const int64_t nb = (L + 1023) / 1024, ns = (nb + 31) / 32;
     return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * nb + XP_MAX_CHG + CUMN + 2 +
-                                       CHBW + 2 * RING + HRING + nb + nb + ns + 1 +
+                                       2 * HSZ + 2 * RING + HRING + nb + nb + ns + 1 +
                                        (GIDS_XP_CAND_CAP + 31) / 32 + 2 * XT + 6 * XP_MAX_CHG +
-                                       2 * XT + XW * 8 + 16 + 1) +
+                                       XW * 8 + 16 + 1) +
            sizeof(unsigned long long) * MOVN;
 }
 

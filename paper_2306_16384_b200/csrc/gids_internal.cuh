@@ -144,7 +144,7 @@ struct ServeCounters {
     int64_t xp_done;       // the batch was decided by k_exact_par
     int64_t xp_stats[4];   // its rounds; rounds ended by a rejection / full change list / lost line
     int64_t bad_order;     // the served list was not strictly ascending (k_window_consume)
-    int64_t xp_prof[8];    // SM cycles per phase (A+B, C tables, selects+D+E, F, G, G prefix, ring) and D passes
+    int64_t xp_prof[12];   // SM cycles per phase (see exact_par.cu) and fixed-point passes
 };
 
 struct CacheMeta {  // persistent cache counters (CacheState)
@@ -206,7 +206,7 @@ struct gids_handle {
     int64_t xp_hcap;
     bool xp_enabled;       // GIDS_EXACT_PAR=0 keeps every batch on k_exact_seq
     int64_t xp_batches;    // served batches k_exact_par decided
-    int64_t xp_stats[12];  // their ServeCounters.xp_stats, xp_prof, summed
+    int64_t xp_stats[16];  // their ServeCounters.xp_stats, xp_prof, summed
     bool counts_read;      // the last serve's counts were read once already
 
     // sampler workspace (HBM)

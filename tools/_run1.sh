@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
+
 timeout 900 python -m pytest tests/test_gpu_exact_par.py -q -x 2>&1 | tail -3
 timeout 900 python bench.py --workload c4 --policy exact --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_exact.json 2> gpurun_out/c4_exact.err
 python - <<'P'
