@@ -71,8 +71,8 @@ WORKLOADS = {
                 cache_lines=0, buffer_fraction=0.0, window_depth=8, consume_rate=0.0, seed=42,
                 gids_generator="device", gids_sharded_table=True, gids_virtual_shards=8),
 }
-DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c2p": "exact", "c3": "setassoc",
-                  "c4": "setassoc", "c5": "exact", "c5v": "exact"}
+DEFAULT_POLICY = {"c1": "exact", "c2": "exact", "c2p": "exact", "c3": "exact",
+                  "c4": "exact", "c5": "exact", "c5v": "exact"}
 WORKLOAD_NAMES = {
     "c2": "IGB-small-shaped 1M nodes / 12M edges (uniform), 1024-d fp32, fanout [10,15], "
           "batch 1024, cache 100K lines (10%) + 10% constant CPU buffer, W=8",
@@ -289,6 +289,25 @@ def _timeline(dl):
     tl = tl[-12:]
     base = tl[0][0]
     return [[round(base.elapsed_time(d), 3), round(base.elapsed_time(g), 3)] for d, g in tl]
+
+
+def decision_kernel(cfg, h, ctl_ms, gat_ms, tiers, steps):
+    """The cache-decision stream's kernel when the exact (reference) policy
+    runs it: k_exact_par, the reference's sequential CacheState.access over a
+    batch decided by one CTA -- latency-bound on one SM (no bandwidth or
+    tensor roofline applies), so it is reported by its own unit costs next
+    to the gather's roofline."""
+    if cfg.gids_policy != "exact" or not ctl_ms:
+        return None
+    st = h.exact_par_stats()
+    accesses = float(tiers[0] + tiers[1] + tiers[2]) / steps  # (bypasses are among 1, 2)
+    return {"kernel": "k_exact_par" if st["batches"] else "k_exact_seq",
+            "bound": "latency (one SM: the reference policy's sequential eviction chain)",
+            "ms_per_batch": ctl_ms, "hidden_under_gather": ctl_ms <= gat_ms,
+            "ns_per_access": ctl_ms * 1e6 / accesses if accesses else None,
+            "rounds_per_batch": st["rounds"] / st["batches"] if st["batches"] else None,
+            "note": "step is bound by this stream when ms_per_batch > the gather's; "
+                    "profiles/r02_exact_par_*.txt"}
 
 
 _SHARED: dict = {}
@@ -622,6 +641,7 @@ def main() -> None:
                         "batches in, host-tier rows over the link, per-step stats read back"},
         "gpu_launches": launches, "clocks": clocks,
         "exact_par": h.exact_par_stats() if cfg.gids_policy == "exact" else None,
+        "decision_kernel": decision_kernel(cfg, h, ctl_ms, gat_ms, tiers, args.steps),
         "storage_file": dl.storage_stats(),
         "numa": numa,
         "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),
