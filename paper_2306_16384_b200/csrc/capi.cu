@@ -101,6 +101,7 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
         const char* e = getenv("GIDS_EXACT_PAR");
         h->xp_enabled = !(e && e[0] == '0') && gids_xp_smem_bytes(L) <= (size_t)dev_smem &&
                         h->cfg.policy == GIDS_POLICY_EXACT && L > 0;
+        h->xp_safe_div = (e && e[0] == '2') ? 0 : 16;  // 2: every full-cache batch (tests)
     }
     if (!h->exact_smem && without + static_smem > (size_t)dev_smem) {
         gids_set_error("cache_lines too large for the exact policy (use the set-associative one)");

@@ -57,6 +57,7 @@ constexpr int HRING = 4096;       // staged draw halves
 constexpr int RING_LAG = 12;      // commit groups allowed in flight when a round reads
 constexpr int32_t NEG = -(1 << 29);
 constexpr int MOVN = 2048;        // moved-line filter: buckets (lines >> movs)
+constexpr int MOVSPAN = 8;        // longer moves / ranges: every earlier MU is checked
 constexpr int CUMN = 256;         // change-line buckets of count_le (lines >> bsh)
 constexpr int HSZ = 1024;         // candidate hash table (line -> lane), open addressing
 
@@ -90,15 +91,22 @@ __device__ __forceinline__ uint32_t half_direct(const CacheMeta* meta, int64_t j
     return (j & 1) ? (uint32_t)(o >> 32) : (uint32_t)o;
 }
 
+// the CTA decides a batch when the cache is full and has safe lines for a
+// good share of the batch's misses (safe_div: safe_count * div >= misses;
+// 0 = always).  A starved cache -- the window protecting nearly every line,
+// misses mostly bypassing -- evicts little and stays on the sequential warp,
+// which is cheaper there (its cost follows the evictions, this kernel's the
+// accesses).
 __device__ __forceinline__ bool xp_runs(const CacheMeta* meta, const ServeCounters* svc,
-                                        int64_t L, int64_t cand_cap) {
-    return svc->n_miss0 != 0 && meta->fill >= L && svc->n_cand <= cand_cap;
+                                        int64_t L, int64_t cand_cap, int64_t safe_div) {
+    return svc->n_miss0 != 0 && meta->fill >= L && svc->n_cand <= cand_cap &&
+           (safe_div == 0 || meta->safe_count * safe_div >= svc->n_miss0);
 }
 
 // the batch's eviction half stream, 8 next64 outputs per thread
 __global__ void k_xp_halves(const CacheMeta* meta, const ServeCounters* svc, int64_t L,
-                            int64_t cand_cap, uint32_t* H, int64_t hcap) {
-    if (!xp_runs(meta, svc, L, cand_cap)) return;
+                            int64_t cand_cap, int64_t safe_div, uint32_t* H, int64_t hcap) {
+    if (!xp_runs(meta, svc, L, cand_cap, safe_div)) return;
     const uint32_t has = (uint32_t)meta->rng[4];
     const int64_t outs = (hcap + 1) / 2;
     const int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
@@ -126,6 +134,7 @@ struct XpArgs {
     uint32_t* sup_cnt;
     const int32_t* cand_of_slot;
     int64_t cand_cap;
+    int64_t safe_div;
     const uint32_t* H;
     int64_t hcap;
     int8_t* kind;
@@ -421,7 +430,7 @@ __device__ __forceinline__ void stage(uint32_t* dst, const uint32_t* src) {
 }
 
 __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
-    if (!xp_runs(a.meta, a.svc, a.L, a.cand_cap)) return;
+    if (!xp_runs(a.meta, a.svc, a.L, a.cand_cap, a.safe_div)) return;
     extern __shared__ __align__(16) uint32_t smem[];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const unsigned below = (1u << lane) - 1u;
@@ -776,7 +785,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (e < nchg && part == 1) x.FIN[e] = v;  // (ADD lines are final)
                 if (e < nchg && part == 2) x.RANKS[e] = rk;
             }
-            if (t == 0) x.MISC[10] = 0;
+            if (t == 0) {
+                x.MISC[10] = 0;
+                x.MISC[13] = 0;  // an MU moved across more than MOVSPAN buckets
+            }
             if (pass == 0 && wid == XW - 1) {  // ADD mask (CTYPE is fixed for the round)
                 const unsigned a0 = __ballot_sync(0xffffffffu, lane < nchg && x.CTYPE[lane] > 0);
                 const unsigned a1 =
@@ -820,9 +832,13 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (chg && cls == C_MU) {
                     x.FIN[pchg] = cur;
                     const int32_t u0 = x.CSLOT[pchg];
-                    if (u0 != cur) {  // mark the buckets the move spans
+                    if (u0 != cur) {  // mark the buckets the move spans (short moves)
                         mlo = min(u0, cur) >> movs;
                         mhi = max(u0, cur) >> movs;
+                        if (mhi - mlo >= MOVSPAN) {
+                            x.MISC[13] = 1;
+                            mhi = -1;
+                        }
                         for (int32_t b = mlo; b <= mhi; b++) atomicOr(&x.MOVM[b], 1ull << pchg);
                     }
                 }
@@ -834,8 +850,12 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             // those whose move crossed a bucket of the lines it looked at
             unsigned long long mu = 0;
             if (sel && in) {
-                for (int32_t b = ylo >> movs; b <= (cur >> movs); b++) mu |= x.MOVM[b];
-                if (lb >= 0) mu |= x.MOVM[lb >> movs];
+                if (x.MISC[13] || (cur >> movs) - (ylo >> movs) >= MOVSPAN) {
+                    mu = ~0ull;  // (a long move or range: all earlier MUs)
+                } else {
+                    for (int32_t b = ylo >> movs; b <= (cur >> movs); b++) mu |= x.MOVM[b];
+                    if (lb >= 0) mu |= x.MOVM[lb >> movs];
+                }
                 mu &= ~addm & mine & allm;
             }
             if (mu) {
@@ -1037,7 +1057,7 @@ int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st) {
     if (!h->xp_enabled || n == 0) return GIDS_OK;
     const int64_t outs = (h->xp_hcap + 1) / 2;
     k_xp_halves<<<gids_grid(ceil_div(outs, 8), 256, 1 << 20), 256, 0, st>>>(
-        h->meta, h->svc, h->L, GIDS_XP_CAND_CAP, h->xp_halves, h->xp_hcap);
+        h->meta, h->svc, h->L, GIDS_XP_CAND_CAP, h->xp_safe_div, h->xp_halves, h->xp_hcap);
     GIDS_LAUNCH_CHECK(h);
     XpArgs a;
     a.ev = h->ev;
@@ -1051,6 +1071,7 @@ int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st) {
     a.sup_cnt = h->sup_cnt;
     a.cand_of_slot = h->cand_of_slot;
     a.cand_cap = GIDS_XP_CAND_CAP;
+    a.safe_div = h->xp_safe_div;
     a.H = h->xp_halves;
     a.hcap = h->xp_hcap;
     a.kind = h->kind;

@@ -205,6 +205,7 @@ struct gids_handle {
     uint32_t* xp_halves;   // [xp_hcap] the batch's eviction draw halves
     int64_t xp_hcap;
     bool xp_enabled;       // GIDS_EXACT_PAR=0 keeps every batch on k_exact_seq
+    int64_t xp_safe_div;   // k_exact_par needs safe_count * div >= misses (0: any; GIDS_EXACT_PAR=2)
     int64_t xp_batches;    // served batches k_exact_par decided
     int64_t xp_stats[16];  // their ServeCounters.xp_stats, xp_prof, summed
     bool counts_read;      // the last serve's counts were read once already

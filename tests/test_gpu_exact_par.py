@@ -42,22 +42,23 @@ CASES = {
 
 
 def _run(case: str, env_off: bool = False):
+    """GIDS_EXACT_PAR=2: every full-cache batch goes to k_exact_par (by default
+    a starved cache -- few safe lines for the batch's misses -- stays on the
+    sequential warp); =0: none does."""
     c = dict(CASES[case])
     nb = c.pop("batches")
     import bench
     cfg = make_config(dict(degree_model="uniform", feature_dim=16, buffer_fraction=0.10,
                            consume_rate=0.0, seed=11, gids_generator="device", **c))
     old = os.environ.get("GIDS_EXACT_PAR")
-    if env_off:
-        os.environ["GIDS_EXACT_PAR"] = "0"
+    os.environ["GIDS_EXACT_PAR"] = "0" if env_off else "2"
     try:
         dl = Dataloader(cfg)
     finally:
-        if env_off:
-            if old is None:
-                del os.environ["GIDS_EXACT_PAR"]
-            else:
-                os.environ["GIDS_EXACT_PAR"] = old
+        if old is None:
+            del os.environ["GIDS_EXACT_PAR"]
+        else:
+            os.environ["GIDS_EXACT_PAR"] = old
     g, buf = bench.host_device_shape(cfg)
     r = bench.oracle_inputs(cfg, g, dl.features.table, buf)
     ld = O.OracleLoader(g.indptr, g.indices, dl.features.table, buf, r["batches"], cfg.fanouts,
