@@ -550,7 +550,9 @@ def main() -> None:
         roofline = {"bound": "host_link", "kernel": "k_gather_host",
                     "achieved": achieved_link, "peak": link_peak, "unit": "GB/s",
                     "frac": achieved_link / link_peak if achieved_link else None,
-                    "traffic": traffic["dram_bytes_per_launch"] if traffic else None,
+                    "traffic": traffic.get("link_bytes_per_launch") if traffic else None,
+                    "traffic_kind": "pcie__read_bytes per launch (the host link)",
+                    "hbm_traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                     "traffic_source": traffic["source"] if traffic else None,
                     "algorithmic_bytes_per_launch": host_bytes_per_launch,
                     "peak_source": "pinned H2D cudaMemcpy measured in this run "
