@@ -747,7 +747,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             find_grp(x, r, total, B);
             rblk = B.gi >> 3;
             if (chg && cls == C_MU)
-                x.CSLOT[pchg] = B.gi * 128 + (int32_t)(((r - B.base) * 128u) / (B.cnt ? B.cnt : 1u));
+                x.CSLOT[pchg] = B.gi * 128 + (int32_t)__fdividef((float)(r - B.base) * 128.f,
+                                                                  (float)(B.cnt ? B.cnt : 1u));
         }
         __syncthreads();
         if (t == 0) {
@@ -808,17 +809,13 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 uint32_t m = 0;
                 for (int j = 0; j < hn; j++) m |= (x.RANKS[h0 + j] < k ? 1u : 0u) << j;
                 reinterpret_cast<uint32_t*>(x.PM)[2 * k + (t & 1)] = m;
-            } else if (t >= XT - (CUMN + 1)) {  // CUMB[b]: changes with line < b << bsh
-                const int b = t - (XT - (CUMN + 1));
-                const int32_t v = (int32_t)((int64_t)b << x.bsh) < 0 ? INT32_MAX
-                                                                      : (int32_t)((int64_t)b << x.bsh);
-                int lo = 0, hi = nchg;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (x.SS[mid] < v) lo = mid + 1;
-                    else hi = mid;
-                }
-                x.CUMB[b] = lo;
+            } else if (t >= XT - (XP_MAX_CHG + 1) && t - (XT - (XP_MAX_CHG + 1)) <= nchg) {
+                // CUMB[b] = changes with line < b << bsh: sorted change j fills the
+                // buckets after its predecessor's up to its own (j = nchg: the rest)
+                const int j = t - (XT - (XP_MAX_CHG + 1));
+                const int lo = j == 0 ? 0 : (x.SS[j - 1] >> x.bsh) + 1;
+                const int hi = j == nchg ? CUMN : (x.SS[j] >> x.bsh);
+                for (int b = lo; b <= hi; b++) x.CUMB[b] = j;
             }
             __syncthreads();
             if (t == 0) { tn = clock64(); prof[4] += tn - tc; tc = tn; }  // resolve
@@ -947,7 +944,12 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 t_update_warp(x, off, -1, lane);
             }
         }
-        for (int i = t; i < HSZ; i += XT) x.CHK[i] = -1;  // (read in F, before the barrier above)
+        if (valid && in && cls == C_CAND && !conv)  // empty the candidate table (all read in F)
+            for (uint32_t h = chash(s);; h = (h + 1) & (HSZ - 1))
+                if (x.CHK[h] == s) {
+                    x.CHK[h] = -1;
+                    break;
+                }
         // state after the last committed access
         if (t == E - 1) {
             x.MISC[4] = max(ni + d, c);              // safe count after it
