@@ -304,9 +304,51 @@ GIDS_API int64_t gids_launch_count(gids_handle* h);
 GIDS_API int64_t gids_exact_par_batches(gids_handle* h);
 /* Over those batches: rounds of accesses, rounds ended early by a Lemire
  * rejection / a full change list / a candidate losing its line, then the
- * kernel's SM cycles per phase (draws, T tables, selects, candidates, commit,
- * re-prefix, staging) and its fixed-point passes (diagnostics). */
-GIDS_API int gids_exact_par_stats(gids_handle* h, int64_t out[12]);
+ * kernel's SM cycles per phase (draws, T tables, first selects, sort, masks,
+ * resolve, candidates, fixed-point passes, verify, commit, ring, spare). */
+GIDS_API int gids_exact_par_stats(gids_handle* h, int64_t out[16]);
+
+/* ---- Owner-sharded cache of data-parallel ranks (SURVEY 8(e) exchange step;
+ * csrc/shared_cache.cu).  Node v lives only in the cache of rank v % G; the
+ * owner decides every rank's accesses of its nodes with the reference policy
+ * (gids_cache_window_update + gids_cache_access, cache.py:144-218) in global
+ * batch order; requesters peer-load hits from the owner's lines.
+ *
+ * gids_owner_split: a batch's ascending unique nodes grouped by owner (stable:
+ * each group ascending) into out_dev, perm_dev[i] = input position of
+ * out_dev[i]; counts_host[G] per-owner sizes (synchronises the stream). */
+GIDS_API int gids_owner_split(gids_handle* h, const int64_t* unique_dev, int64_t n, int32_t G,
+                              int64_t* out_dev, int32_t* perm_dev, int64_t* counts_host,
+                              void* stream);
+/* Owner, after gids_cache_access of global batch `batch` (step's first batch
+ * step0): flags_dev[i] bit 0 = a hit on a line inserted earlier in this step
+ * ("fresh": its row may not have landed); the batch's inserts are stamped. */
+GIDS_API int gids_shared_marks(gids_handle* h, const int8_t* kind_dev, const int32_t* line_dev,
+                               int64_t n, int32_t batch, int32_t step0, uint8_t* flags_dev,
+                               void* stream);
+/* Owner, after the step's last batch: bit 1 = this miss is its line's final
+ * inserter in the step; packed_dev[i] = line | kind << 32 | flags << 40. */
+GIDS_API int gids_shared_final(gids_handle* h, const int8_t* kind_dev, const int32_t* line_dev,
+                               const uint8_t* flags_dev, int64_t n, int32_t batch,
+                               int64_t* packed_dev, void* stream);
+/* Requester: packed decisions (owner-grouped, as split) back in unique order. */
+GIDS_API int gids_shared_unsplit(gids_handle* h, const int64_t* packed_dev, const int32_t* perm_dev,
+                                 int64_t n, int64_t* dec_dev, void* stream);
+/* Requester: hits / constant buffer / storage / bypasses of the batch
+ * (dataloader.py:262-277; synchronises). */
+GIDS_API int gids_shared_tiers(gids_handle* h, const int64_t* unique_dev, const int64_t* dec_dev,
+                               int64_t n, int64_t tiers_out[4], void* stream);
+/* Requester: phase 0 gathers every row into out_dev (U x dim) -- non-fresh
+ * hits from owner_rows_host[v % G] (device pointers: this rank's cache rows or
+ * peers' opened by CUDA IPC), the rest from this handle's host tiers; phase 1
+ * (after every rank finished phase 0) writes the final inserters' rows into
+ * the owners' lines. */
+GIDS_API int gids_shared_gather(gids_handle* h, const int64_t* unique_dev, const int64_t* dec_dev,
+                                int64_t n, int32_t G, const uint64_t* owner_rows_host,
+                                float* out_dev, int32_t phase, void* stream);
+/* The handle's cache rows (device pointer; a whole cudaMalloc allocation, so
+ * it can be exported with gids_ipc_handle). */
+GIDS_API float* gids_cache_rows_ptr(gids_handle* h);
 
 #ifdef __cplusplus
 }

@@ -373,3 +373,52 @@ class OracleLoader:
         return {"seeds": seeds, "layers": layers, "unique": uniq,
                 "rows": rows if self.keep_rows else None, "tiers": tiers,
                 "inflight": inflight, "kind": kind, "slot": slot}
+
+
+def shared_cache_tiers(indptr, indices, buffer_nodes, rank_batches, fanouts, rank_words,
+                       evict_seed: int, lines: int, window_depth: int, steps: int):
+    """Multi-rank oracle of the owner-sharded cache (shared_cache.py):
+    G ranks, rank r serving global batches r, r+G, ... sampled from its own
+    stream; one reference CacheState per owner (nodes v with v % G == o, its
+    eviction stream PCG64(evict_seed).jumped(o)) driven by its nodes of every
+    batch in global batch order, the window being its nodes of the next W
+    batches (cache.py:66-218).  Returns, per global batch, (unique nodes,
+    [hits, buffer, storage, bypasses])."""
+    G = len(rank_batches)
+    n = len(indptr) - 1
+    total = steps * G + window_depth
+    uniq = []
+    words = [np.ascontiguousarray(w, dtype=np.uint64).copy() for w in rank_words]
+    nxt = [0] * G
+    for b in range(total):
+        r = b % G
+        seeds = rank_batches[r][nxt[r]]
+        nxt[r] += 1
+        _, u, _ = sample_subgraph(indptr, indices, seeds, fanouts, words[r])
+        uniq.append(np.asarray(u, dtype=np.int64))
+    pinned = np.zeros(n, bool)
+    pinned[np.asarray(buffer_nodes, dtype=np.int64)] = True
+    caches = []
+    for o in range(G):
+        bg = np.random.PCG64(evict_seed).jumped(o)
+        st = bg.state
+        m = (1 << 64) - 1
+        s, inc = st["state"]["state"], st["state"]["inc"]
+        w = np.array([s >> 64, s & m, inc >> 64, inc & m, st["has_uint32"], st["uinteger"]],
+                     dtype=np.uint64)
+        caches.append(OracleCache(n, lines, "exact", rng_words=w))
+    out = []
+    for b in range(steps * G):
+        u = uniq[b]
+        kind = np.empty(len(u), np.int8)
+        for o in range(G):
+            mine = (u % G) == o
+            cur = u[mine]
+            fut = [f[(f % G) == o] for f in uniq[b + 1:b + 1 + window_depth]]
+            caches[o].window_update(cur, fut)
+            k, _ = caches[o].access_batch(cur)
+            kind[mine] = k
+        hit = kind == 0
+        out.append((u, [int(hit.sum()), int((~hit & pinned[u]).sum()),
+                        int((~hit & ~pinned[u]).sum()), int((kind == 2).sum())]))
+    return out

@@ -72,6 +72,13 @@ def lib() -> C.CDLL:
         "gids_set_constant_buffer": ([vp, vp, i64, vp], C.c_int),
         "gids_sample": ([vp, vp, i64, vp, vp], C.c_int),
         "gids_sample_frontier": ([vp, vp, i64, vp, vp], C.c_int),
+        "gids_owner_split": ([vp, vp, i64, i32, vp, vp, vp, vp], C.c_int),
+        "gids_shared_marks": ([vp, vp, vp, i64, i32, i32, vp, vp], C.c_int),
+        "gids_shared_final": ([vp, vp, vp, vp, i64, i32, vp, vp], C.c_int),
+        "gids_shared_unsplit": ([vp, vp, vp, i64, vp, vp], C.c_int),
+        "gids_shared_tiers": ([vp, vp, vp, i64, vp, vp], C.c_int),
+        "gids_shared_gather": ([vp, vp, vp, i64, i32, vp, vp, i32, vp], C.c_int),
+        "gids_cache_rows_ptr": ([vp], vp),
         "gids_sample_sizes": ([vp, vp, vp, vp, vp], C.c_int),
         "gids_sample_export": ([vp, vp, vp, vp], C.c_int),
         "gids_sample_export_async": ([vp, vp, vp, vp, vp], C.c_int),
@@ -141,7 +148,9 @@ def exported_symbols() -> list[str]:
             "gids_synthesize_rows_strided", "gids_set_storage_file", "gids_storage_file_stats",
             "gids_cache_window_update", "gids_cache_access", "gids_cache_reuse",
             "gids_contribution_async", "gids_host_register", "gids_host_unregister",
-            "gids_exact_par_batches", "gids_exact_par_stats"]
+            "gids_exact_par_batches", "gids_exact_par_stats", "gids_owner_split",
+            "gids_shared_marks", "gids_shared_final", "gids_shared_unsplit", "gids_shared_tiers",
+            "gids_shared_gather", "gids_cache_rows_ptr"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -331,6 +340,39 @@ class Handle:
         check(lib().gids_cache_access(self.h, _p(nodes), nodes.numel(), _p(kind), _p(line),
                                       _p(victim) if victim is not None else None, stream),
               "cache_access")
+
+    # -- owner-sharded cache (csrc/shared_cache.cu)
+    def owner_split(self, unique, G: int, out, perm, stream: int) -> np.ndarray:
+        counts = np.zeros(G, np.int64)
+        check(lib().gids_owner_split(self.h, _p(unique), unique.numel(), G, _p(out), _p(perm),
+                                     counts.ctypes.data, stream), "owner_split")
+        return counts
+
+    def shared_marks(self, kind, line, batch: int, step0: int, flags, stream: int) -> None:
+        check(lib().gids_shared_marks(self.h, _p(kind), _p(line), kind.numel(), batch, step0,
+                                      _p(flags), stream), "shared_marks")
+
+    def shared_final(self, kind, line, flags, batch: int, packed, stream: int) -> None:
+        check(lib().gids_shared_final(self.h, _p(kind), _p(line), _p(flags), kind.numel(), batch,
+                                      _p(packed), stream), "shared_final")
+
+    def shared_unsplit(self, packed, perm, dec, stream: int) -> None:
+        check(lib().gids_shared_unsplit(self.h, _p(packed), _p(perm), packed.numel(), _p(dec),
+                                        stream), "shared_unsplit")
+
+    def shared_tiers(self, unique, dec, stream: int) -> np.ndarray:
+        out = np.zeros(4, np.int64)
+        check(lib().gids_shared_tiers(self.h, _p(unique), _p(dec), unique.numel(),
+                                      out.ctypes.data, stream), "shared_tiers")
+        return out
+
+    def shared_gather(self, unique, dec, owner_rows, out, phase: int, stream: int) -> None:
+        rows = np.ascontiguousarray(owner_rows, dtype=np.uint64)
+        check(lib().gids_shared_gather(self.h, _p(unique), _p(dec), unique.numel(), len(rows),
+                                       rows.ctypes.data, _p(out), phase, stream), "shared_gather")
+
+    def cache_rows_ptr(self) -> int:
+        return int(lib().gids_cache_rows_ptr(self.h) or 0)
 
     def cache_reuse(self, num_nodes: int) -> np.ndarray:
         out = np.zeros(num_nodes, np.uint32)

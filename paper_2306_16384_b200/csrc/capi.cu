@@ -297,7 +297,7 @@ int gids_destroy(gids_handle* h) {
                     h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
                     h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev,
                     h->serve_parts, h->serve_word_parts, h->cand_of_slot, h->cand_slot,
-                    h->xcls,      h->xp_halves};
+                    h->xcls,      h->xp_halves, h->line_mark, h->shared_rows};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)

@@ -59,7 +59,8 @@ constexpr int32_t NEG = -(1 << 29);
 constexpr int MOVN = 2048;        // moved-line filter: buckets (lines >> movs)
 constexpr int MOVSPAN = 8;        // longer moves / ranges: every earlier MU is checked
 constexpr int CUMN = 256;         // change-line buckets of count_le (lines >> bsh)
-constexpr int HSZ = 1024;         // candidate hash table (line -> lane), open addressing
+constexpr int HSZ = XT;           // the round's candidates: (line, lane) list
+constexpr int CHBW = 128;         // candidate-line filter: 4096 bits
 
 enum { C_STAY = GIDS_XC_STAY, C_ADD = GIDS_XC_ADD, C_CAND = GIDS_XC_CAND, C_M0 = GIDS_XC_M0,
        C_MU = GIDS_XC_MU };
@@ -156,8 +157,9 @@ struct Xs {
     int32_t* FIN;     // [XP_MAX_CHG] MU lines found by the current pass
     unsigned long long* MOVM;  // [MOVN] per bucket: MU changes whose move crossed it (this pass)
     int32_t* CUMB;    // [CUMN+1] changes with line < (b << bsh), b = 0..CUMN
-    int32_t* CHK;     // [HSZ] candidate lines of the round (-1 empty)
+    int32_t* CHK;     // [HSZ] candidate lines of the round (MISC[7] of them)
     int32_t* CHV;     // [HSZ] their lanes
+    uint32_t* CHB;    // [CHBW] filter bits of their lines (line & 4095)
     uint32_t* REV;    // [RING]
     uint32_t* RCL;    // [RING]
     uint32_t* RH;     // [HRING]
@@ -318,16 +320,14 @@ __device__ __forceinline__ int32_t sel_T(const Xs& x, uint32_t q, uint32_t total
     return sel_grp(G, q - G.base);
 }
 
-__device__ __forceinline__ uint32_t chash(int32_t line) {
-    return ((uint32_t)line * 0x9E3779B1u) >> (32 - 10);  // HSZ = 2^10
-}
-// lane of the round's candidate whose line this is, -1 none
+// lane of the round's candidate whose line this is, -1 none (a filter bit
+// first: almost every answer is no candidate's line)
 __device__ __forceinline__ int32_t cand_lane(const Xs& x, int32_t line) {
-    for (uint32_t h = chash(line);; h = (h + 1) & (HSZ - 1)) {
-        const int32_t k = x.CHK[h];
-        if (k == line) return x.CHV[h];
-        if (k < 0) return -1;
-    }
+    if (!((x.CHB[(line >> 5) & (CHBW - 1)] >> (line & 31)) & 1u)) return -1;
+    const int nc = x.MISC[7];
+    for (int k = 0; k < nc; k++)
+        if (x.CHK[k] == line) return x.CHV[k];
+    return -1;
 }
 
 // lines among the round's changes <= y: the bucket's start, then the few
@@ -453,6 +453,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         p += HSZ;
         x.CHV = reinterpret_cast<int32_t*>(p);
         p += HSZ;
+        x.CHB = p;
+        p += CHBW;
         x.REV = p;
         p += RING;
         x.RCL = p;
@@ -506,7 +508,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         x.GCNT[i] = packed;
     }
     for (int64_t i = t; i < (a.cand_cap + 31) / 32; i += XT) x.CONV[i] = 0u;
-    for (int i = t; i < HSZ; i += XT) x.CHK[i] = -1;
+    for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;
     for (int i = t; i < MOVN; i += XT) x.MOVM[i] = 0ull;
     x.PANS[t] = -1;
     // stage the first accesses and halves
@@ -716,11 +718,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             }
         }
         if (valid && in && cls == C_CAND && !conv) {
-            for (uint32_t h = chash(s);; h = (h + 1) & (HSZ - 1))
-                if (atomicCAS(&x.CHK[h], -1, s) == -1) {
-                    x.CHV[h] = t;
-                    break;
-                }
+            const int k = atomicAdd(&x.MISC[7], 1);
+            x.CHK[k] = s;
+            x.CHV[k] = t;
+            atomicOr(&x.CHB[(s >> 5) & (CHBW - 1)], 1u << (s & 31));
         }
         __syncthreads();
         {  // the round's ADD lines join T's tables
@@ -944,12 +945,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 t_update_warp(x, off, -1, lane);
             }
         }
-        if (valid && in && cls == C_CAND && !conv)  // empty the candidate table (all read in F)
-            for (uint32_t h = chash(s);; h = (h + 1) & (HSZ - 1))
-                if (x.CHK[h] == s) {
-                    x.CHK[h] = -1;
-                    break;
-                }
+        for (int i = t; i < CHBW; i += XT) x.CHB[i] = 0u;  // (read in F, before the barrier above)
         // state after the last committed access
         if (t == E - 1) {
             x.MISC[4] = max(ni + d, c);              // safe count after it
@@ -1048,7 +1044,7 @@ int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
 size_t gids_xp_smem_bytes(int64_t L) {
     const int64_t nb = (L + 1023) / 1024, ns = (nb + 31) / 32;
     return sizeof(uint32_t) * (size_t)(2 * (XP_MAX_CHG + 2) + 2 * nb + XP_MAX_CHG + CUMN + 2 +
-                                       2 * HSZ + 2 * RING + HRING + nb + nb + ns + 1 +
+                                       2 * HSZ + CHBW + 2 * RING + HRING + nb + nb + ns + 1 +
                                        (GIDS_XP_CAND_CAP + 31) / 32 + 2 * XT + 6 * XP_MAX_CHG +
                                        XW * 8 + 16 + 1) +
            sizeof(unsigned long long) * MOVN;

@@ -35,6 +35,7 @@ from .csc import (HEADER_BYTES, FeatureStore, GraphCsc, generate_synthetic, load
 from .feature_cache import GpuCacheView, WindowBuffer
 from .hot_buffer import build_constant_buffer, reverse_pagerank_device, top_k_nodes_device
 from .sampling import MiniBatch, Sampler, batch_iterator, check_seeds, pcg_words
+from .shared_cache import OwnerShardedCache
 from .sharded_table import ShardedTable
 from .settings import ConfigError, InfeasibleError, PipelineConfig
 from .storage_model import exact, fetch_total_us, required_accesses
@@ -173,6 +174,11 @@ class Dataloader:
         self._build_constant_buffer(dev_graph, row_bytes)
 
         evict_seed = int(evict_ss.generate_state(1)[0])
+        shared = cfg.gids_shared_cache
+        # owner-sharded cache: each owner's eviction stream is its own jump of
+        # the eviction generator (the replicas' caches all start from it)
+        ev_words = pcg_words(np.random.Generator(np.random.PCG64(evict_seed).jumped(
+            cfg.gids_dp_rank)) if shared else np.random.default_rng(evict_seed))
         self._h = _native.Handle(
             num_nodes=self.graph.num_nodes, num_edges=self.graph.num_edges,
             feature_dim=self.features.dim, device=self.device,
@@ -180,7 +186,7 @@ class Dataloader:
             policy="exact" if self.sharded else cfg.gids_policy, ways=32,
             evict_key=evict_seed, window_depth=cfg.window_depth, fanouts=cfg.fanouts,
             max_seeds=cfg.batch_size,
-            eviction_words=pcg_words(np.random.default_rng(evict_seed)))
+            eviction_words=ev_words)
         self._h.load_graph_device(*dev_graph)
         del dev_graph
         if self.sharded is not None:
@@ -221,6 +227,14 @@ class Dataloader:
         self._last_contrib = None
         self.cache = GpuCacheView(self._h, self.spec.page_bytes)
         self.window = WindowBuffer(cfg.window_depth, self._h, self._ctl.cuda_stream)
+        self.shared = None
+        if shared:
+            # the handle's window counters serve the owner role (owned parts of
+            # every rank's batches); the run-ahead ring stays unbound
+            self.window = WindowBuffer(0)
+            self.shared = OwnerShardedCache(self._h, cfg.gids_dp_rank, cfg.gids_dp_world,
+                                            cfg.window_depth, self.device)
+            self._sent = 0
         self._sampler = Sampler(self._h, self.graph.num_nodes, cfg.fanouts)
 
         self.base_threshold = required_accesses(self.spec, cfg.target_fraction)
@@ -590,6 +604,8 @@ class Dataloader:
 
     # -- serving (dataloader.py:232-299)
     def next_batch(self):
+        if self.shared is not None:
+            return self._next_batch_shared()
         import torch
         tr = self._trace
         if tr is not None:
@@ -656,6 +672,42 @@ class Dataloader:
         self._iteration += 1
         return batch, rows, stats
 
+    def _next_batch_shared(self):
+        """One global step of the owner-sharded cache (shared_cache.py): this
+        rank's batch, decided by the owners of its nodes, gathered from the
+        owners' lines and this rank's host tiers.  Collective over the ranks."""
+        sh = self.shared
+        G, r = sh.G, self.cfg.gids_dp_rank
+        st = _native.stream_ptr(self.device)
+        self.run_ahead()
+        if not self._pending:
+            raise StopIteration
+        # the owners need this rank's batches up to `ahead` steps on (window)
+        while self._sent <= self._iteration + sh.ahead and \
+                self._sent - self._iteration < len(self._pending):
+            q = self._pending[self._sent - self._iteration]
+            self._resolve(q)
+            sh.send_lists(self._sent * G + r, q.batch.unique_nodes, st)
+            self._sent += 1
+        inflight = self._pending_storage
+        entry = self._pending.popleft()
+        self._n_resolved -= 1
+        self._resolved_storage -= entry.storage_accesses
+        self.run_ahead()
+        batch = entry.batch
+        unique = batch.unique_nodes
+        n = unique.numel()
+        dec, tiers = sh.serve_step(self._iteration, unique, st)
+        rows = self._out_block()[:n]
+        sh.gather(unique, dec, rows, st)
+        if self.cfg.verify_gather:
+            self._verify(unique, rows)
+        hits, buf, ssd, byp = (int(v) for v in tiers)
+        self.last_counts = None
+        stats = self._account(n, hits, buf, ssd, byp, inflight)
+        self._iteration += 1
+        return batch, rows, stats
+
     def _verify(self, unique, rows) -> None:
         if self.features.seed is not None:
             bad = _native.verify_rows(self.device, self.features.seed, unique, rows,
@@ -715,6 +767,12 @@ class Dataloader:
     def close(self) -> None:
         import torch
         torch.cuda.synchronize(self.device)
+        if getattr(self, "shared", None) is not None:
+            import torch.distributed as dist
+            if self.cfg.gids_dp_world > 1 and dist.is_available() and dist.is_initialized():
+                dist.barrier()  # no peer may still be reading or writing this rank's lines
+            self.shared.close()
+            self.shared = None
         self._h.close()
         if self.sharded is not None:
             import torch.distributed as dist

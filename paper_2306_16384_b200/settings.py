@@ -38,6 +38,11 @@ prefixed ``gids``) select the B200 path:
                       live in POSIX shared memory created by local rank 0 and
                       mapped + page-locked by every rank (host_tier.py),
                       instead of a private copy per rank.
+* ``gids_shared_cache`` with several data-parallel ranks, one owner-sharded
+                      cache instead of G replicas: node v is cached only by rank
+                      v % G, which decides every rank's accesses of it with the
+                      reference policy in global batch order; hits are peer
+                      loads (shared_cache.py; exact policy).
 * ``gids_speculate``  batches sampled ahead of the run-ahead queue (their
                       contributions are still counted when they join it, so
                       results are unchanged; 0 disables).
@@ -116,6 +121,7 @@ class PipelineConfig:
     gids_io_direct: bool = False
     gids_speculate: int = 2
     gids_shared_host: bool = True
+    gids_shared_cache: bool = False
 
     def ssd_spec(self) -> SsdSpec:
         if self.ssd_preset is None:
@@ -264,6 +270,9 @@ _RULES = [
     (lambda c: c.gids_speculate >= 0, "gids_speculate must be non-negative"),
     (lambda c: c.gids_virtual_shards == 0 or c.gids_dp_world == 1,
      "gids_virtual_shards is for single-process runs (gids_dp_world 1)"),
+    (lambda c: not c.gids_shared_cache or (c.gids_policy == "exact" and not c.gids_sharded_table
+                                           and c.gids_storage == "pinned"),
+     "gids_shared_cache runs the exact policy over a pinned host tier"),
 ]
 
 
