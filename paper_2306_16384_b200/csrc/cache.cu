@@ -976,9 +976,12 @@ static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t
         h->ev, n, h->meta, h->safe_bits, h->blk_cnt, h->sup_cnt, h->svc, h->kind, h->line);
     GIDS_LAUNCH_CHECK(h);
     auto k = k_exact_seq;
-    if (smem > 48 * 1024)
+    static size_t attr_smem = 48 * 1024;  // (per function: set when it grows)
+    if (smem > attr_smem) {
         GIDS_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)smem));
+        attr_smem = smem;
+    }
     k<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits, h->evict_bits, h->blk_cnt,
                            h->sup_cnt, h->exact_smem ? 1 : 0, h->kind, h->line, h->log_line,
                            h->log_pos, h->svc);

@@ -99,8 +99,10 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
     h->exact_smem = with_bits + static_smem <= (size_t)dev_smem;
     {
         const char* e = getenv("GIDS_EXACT_PAR");
+        // (a cache with a line for every node never fills: the CTA kernel
+        // and its launches are skipped)
         h->xp_enabled = !(e && e[0] == '0') && gids_xp_smem_bytes(L) <= (size_t)dev_smem &&
-                        h->cfg.policy == GIDS_POLICY_EXACT && L > 0;
+                        h->cfg.policy == GIDS_POLICY_EXACT && L > 0 && L < h->N;
         h->xp_safe_div = (e && e[0] == '2') ? 0 : 16;  // 2: every full-cache batch (tests)
     }
     if (!h->exact_smem && without + static_smem > (size_t)dev_smem) {

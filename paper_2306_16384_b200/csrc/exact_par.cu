@@ -1035,6 +1035,7 @@ __global__ void k_xp_reset(const ServeCounters* svc, const int32_t* __restrict__
 }  // namespace
 
 int gids_launch_xp_reset(gids_handle* h, cudaStream_t st) {
+    if (!h->xp_enabled) return GIDS_OK;  // (nothing set cand_of_slot)
     k_xp_reset<<<64, 256, 0, st>>>(h->svc, h->cand_slot, h->cand_of_slot);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
@@ -1077,8 +1078,12 @@ int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st) {
     a.log_line = h->log_line;
     a.log_pos = h->log_pos;
     const size_t smem = gids_xp_smem_bytes(h->L);
-    GIDS_CUDA_TRY(cudaFuncSetAttribute(k_exact_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
+    static size_t attr_smem = 0;  // (the attribute is per function: set when it grows)
+    if (smem > attr_smem) {
+        GIDS_CUDA_TRY(cudaFuncSetAttribute(k_exact_par, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+        attr_smem = smem;
+    }
     k_exact_par<<<1, XT, smem, st>>>(a);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;

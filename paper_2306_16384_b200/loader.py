@@ -192,9 +192,10 @@ class Dataloader:
         if self.sharded is not None:
             self._h.set_sharded_table(self.sharded.ptrs, self.sharded.rank)
         elif self._storage_file is not None:
-            self._h.set_storage_file(self._storage_file, HEADER_BYTES, self.spec.page_bytes,
+            off = HEADER_BYTES if cfg.graph_path is not None else cfg.gids_storage_offset
+            self._h.set_storage_file(self._storage_file, off, self.spec.page_bytes,
                                      io_threads=cfg.gids_io_threads, direct=cfg.gids_io_direct)
-            self._file_offset, self._file_page = HEADER_BYTES, self.spec.page_bytes
+            self._file_offset, self._file_page = off, self.spec.page_bytes
         else:
             pinned = self.features.pinned
             self._h.set_backing(pinned if isinstance(pinned, torch.Tensor) else self.features.table,
@@ -336,10 +337,12 @@ class Dataloader:
             # the synthetic table written once to a .gfea file, then served
             # from the file (csrc/storage_file.cu)
             write_synthetic_features(cfg.gids_storage_path, cfg.num_nodes, cfg.feature_dim,
-                                     feat_seed, self.device)
-            host = load_features(cfg.gids_storage_path, mmap=True)
-            self.features = FeatureStore(num_nodes=host.num_nodes, dim=host.dim,
-                                         table=host.table, seed=feat_seed)
+                                     feat_seed, self.device, offset=cfg.gids_storage_offset)
+            table = np.memmap(cfg.gids_storage_path, dtype=np.float32, mode="r",
+                              offset=cfg.gids_storage_offset,
+                              shape=(cfg.num_nodes, cfg.feature_dim))
+            self.features = FeatureStore(num_nodes=cfg.num_nodes, dim=cfg.feature_dim,
+                                         table=table, seed=feat_seed)
             self._storage_file = str(cfg.gids_storage_path)
         elif self._shared_host():
             tok = self._host_token = host_tier.job_token()
@@ -433,7 +436,7 @@ class Dataloader:
             view[r:r + step] = host.table[r:r + step]
         return FeatureStore(num_nodes=host.num_nodes, dim=host.dim, table=view, pinned=buf)
 
-    def gids_init(self, offset: int = 24, cacheline_bytes: int | None = None,
+    def gids_init(self, offset: int | None = None, cacheline_bytes: int | None = None,
                   num_elements: int | None = None, n_ssd: int | None = None,
                   path: str | None = None) -> dict:
         """The GIDS init call: lays out the backing store
@@ -456,6 +459,8 @@ class Dataloader:
         if num_elements is not None and num_elements != n * dim:
             raise ConfigError(f"gids_init num_elements={num_elements} disagrees with the "
                               f"loader ({n * dim} = {n} nodes x {dim})")
+        if offset is None:  # keep the current layout (the .gfea header for a new file)
+            offset = self._file_offset if self._storage_file is not None else HEADER_BYTES
         if offset < 0:
             raise ConfigError("gids_init offset must be non-negative")
         if n_ssd is not None:

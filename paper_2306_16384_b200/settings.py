@@ -31,6 +31,9 @@ prefixed ``gids``) select the B200 path:
                       the page-coalescing accumulator (csrc/storage_file.cu).
                       A synthetic config writes its table to
                       ``gids_storage_path`` first.
+* ``gids_storage_offset`` byte offset of row 0 in a synthetic config's storage
+                      file (24: the .gfea layout; a page multiple aligns every
+                      row to pages -- the GIDS init call's offset).
 * ``gids_io_threads`` / ``gids_io_direct``  pread threads / O_DIRECT for "file".
 * ``gids_shared_host`` with several data-parallel ranks (torch.distributed
                       initialised), the ranks of a node share ONE host tier:
@@ -117,6 +120,7 @@ class PipelineConfig:
     gids_virtual_shards: int = 0
     gids_storage: str = "pinned"
     gids_storage_path: str | None = None
+    gids_storage_offset: int = 24
     gids_io_threads: int = 8
     gids_io_direct: bool = False
     gids_speculate: int = 2
@@ -267,6 +271,7 @@ _RULES = [
     (lambda c: c.gids_storage != "file" or not c.gids_sharded_table,
      "gids_storage 'file' and gids_sharded_table are exclusive"),
     (lambda c: c.gids_io_threads >= 1, "gids_io_threads must be >= 1"),
+    (lambda c: c.gids_storage_offset >= 24, "gids_storage_offset must be >= 24 (the header)"),
     (lambda c: c.gids_speculate >= 0, "gids_speculate must be non-negative"),
     (lambda c: c.gids_virtual_shards == 0 or c.gids_dp_world == 1,
      "gids_virtual_shards is for single-process runs (gids_dp_world 1)"),

@@ -150,3 +150,27 @@ def test_gpu_gids_init_lays_out_the_backing_store(tmp_path):
         dl.gids_init(offset=4096)
     dl.close()
     want.close()
+
+
+@pytest.mark.parametrize("name", ["alltiers", "c2small"])
+def test_gpu_page_aligned_file_layout_matches_reference_run(name, tmp_path):
+    """The storage file laid out with row 0 at a page boundary
+    (gids_storage_offset = page_bytes): every row is one page read instead of
+    the .gfea layout's two (a 24-byte header makes each row straddle a page
+    boundary); rows, tiers and CSV rows as the reference's run."""
+    fx = fixture(name)
+    cfg = config_of(fx, gids_storage="file", gids_storage_path=str(tmp_path / "t.bin"))
+    cfg = config_of(fx, gids_storage="file", gids_storage_path=str(tmp_path / "t.bin"),
+                    gids_storage_offset=cfg.page_bytes)
+    dl = Dataloader(cfg)
+    assert dl.gids_init(cacheline_bytes=cfg.page_bytes)["offset"] == cfg.page_bytes
+    storage_rows = 0
+    for b in range(int(fx["n_batches"])):
+        mb, rows, st = dl.next_batch()
+        assert np.array_equal(mb.unique_nodes.cpu().numpy(), fx[f"b{b}_unique"]), b
+        assert sha(rows.cpu().numpy()) == str(fx[f"b{b}_rows_sha"]), b
+        assert st.csv_row() == str(fx["csv"][b]), b
+        storage_rows += st.ssd_accesses
+    if cfg.feature_dim * 4 == cfg.page_bytes:  # a row is exactly one page
+        assert dl.storage_stats()["pages"] == storage_rows
+    dl.close()

@@ -1,9 +1,8 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2 3 4 5 6 7 8; do timeout 300 python tools/_dbg_shared2.py 2 2>&1 | grep -E "^mode"; done
-timeout 900 python -m pytest tests/test_gpu_exact_par.py tests/test_gpu_fuzz.py tests/test_gpu_shared_cache.py -q -x 2>&1 | tail -3
-timeout 900 python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/c4_exact.json 2> gpurun_out/c4_exact.err
-python - <<'P'
-import json
-d=json.loads(open("gpurun_out/c4_exact.json").read().strip().splitlines()[-1])
-print(d["value"], d["phase_ms_per_step"])
-P
+timeout 900 python -m pytest tests/test_gpu_storage_file.py -q -x 2>&1 | grep -E "assert|Error|passed|failed" | head -10
+for t in 128 256; do
+timeout 900 python bench.py --workload c2 --steps 8 --warmup 3 --no-cpu-baseline --set gids_storage=file --set gids_storage_path=/tmp/c2.gfea --set gids_io_direct=true --set gids_storage_offset=4096 --set gids_io_threads=$t > gpurun_out/c2f_$t.json 2>&1
+python -c "
+import json; d=json.loads(open('gpurun_out/c2f_$t.json').read().strip().splitlines()[-1]); print('c2 file threads $t', d['value'], d['storage_file'])" 2>&1 | tail -1
+rm -f /tmp/c2.gfea
+done
