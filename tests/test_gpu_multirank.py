@@ -25,8 +25,9 @@ def _port() -> int:
     return p
 
 
-@pytest.mark.parametrize("extra", [[], ["--workload", "c5", "--set", "num_nodes=200000"]],
-                         ids=["replicas", "sharded"])
+@pytest.mark.parametrize("extra", [[], ["--workload", "c5", "--set", "num_nodes=200000"],
+                                   ["--set", "gids_shared_cache=true", "--set", "cache_lines=20000"]],
+                         ids=["replicas", "sharded", "owner_cache"])
 def test_two_rank_bench_prints_one_line(extra):
     env = {**os.environ, "BENCH_DIST_BACKEND": "gloo", "PYTHONPATH": str(ROOT)}
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
