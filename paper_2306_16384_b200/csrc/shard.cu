@@ -8,6 +8,7 @@
 // NVSwitch (CUDA IPC mappings), 16-byte loads with many in flight -- one
 // kernel, no staging copy, no collective on the data path.  The whole table
 // is resident, so every access is a hit (no cache policy, no host tier).
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -148,13 +149,23 @@ int gids_launch_shard_serve(gids_handle* h, const int64_t* uniq, int64_t n, floa
         auto lg = [](int64_t v) { uint32_t s = 0; while ((int64_t(1) << s) < v) s++; return s; };
         const uint32_t G = (uint32_t)h->n_shards;
         const auto* sp = reinterpret_cast<const int4* const*>(h->shard_ptrs);
-        if (pow2(cpr) && pow2(G))
-            k_gather_shards<4, true><<<4 * GIDS_SMS, BLOCK, 0, gst>>>(
-                uniq, (uint32_t)n, sp, G, lg(G), (uint32_t)cpr, lg(cpr),
-                reinterpret_cast<int4*>(out));
-        else
-            k_gather_shards<4, false><<<4 * GIDS_SMS, BLOCK, 0, gst>>>(
-                uniq, (uint32_t)n, sp, G, 0, (uint32_t)cpr, 0, reinterpret_cast<int4*>(out));
+        // blocks per SM and 16-B loads in flight per lane (GIDS_SHARD_BPS /
+        // GIDS_SHARD_U: experiments; defaults measured best)
+        static int bps = getenv("GIDS_SHARD_BPS") ? atoi(getenv("GIDS_SHARD_BPS")) : 4;
+        static int un = getenv("GIDS_SHARD_U") ? atoi(getenv("GIDS_SHARD_U")) : 4;
+        const int grid = bps * GIDS_SMS;
+        auto* o4 = reinterpret_cast<int4*>(out);
+        if (pow2(cpr) && pow2(G)) {
+            if (un >= 8)
+                k_gather_shards<8, true><<<grid, BLOCK, 0, gst>>>(uniq, (uint32_t)n, sp, G, lg(G),
+                                                                 (uint32_t)cpr, lg(cpr), o4);
+            else
+                k_gather_shards<4, true><<<grid, BLOCK, 0, gst>>>(uniq, (uint32_t)n, sp, G, lg(G),
+                                                                 (uint32_t)cpr, lg(cpr), o4);
+        } else {
+            k_gather_shards<4, false><<<grid, BLOCK, 0, gst>>>(uniq, (uint32_t)n, sp, G, 0,
+                                                              (uint32_t)cpr, 0, o4);
+        }
     } else {
         k_gather_shards_f32<<<gids_grid(n * dim, BLOCK, 8 * GIDS_SMS), BLOCK, 0, gst>>>(
             uniq, n, h->shard_ptrs, h->n_shards, dim, out);
