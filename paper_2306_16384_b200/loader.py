@@ -541,8 +541,10 @@ class Dataloader:
         words = None if self._rng_on_device else pcg_words(self._sampler_rng)
         self._h.sample(seeds, words, st)
         self._rng_on_device = True
-        edges = self._empty_on(self._smp, (self._edge_cap, 2), torch.int64)
-        unique = self._empty_on(self._smp, self._unique_cap, torch.int64)
+        # one allocation for the batch's edges and unique nodes (views of it)
+        block = self._empty_on(self._smp, 2 * self._edge_cap + self._unique_cap, torch.int64)
+        edges = block[:2 * self._edge_cap].view(self._edge_cap, 2)
+        unique = block[2 * self._edge_cap:]
         sizes = self._sizes[self._sizes_next]
         self._sizes_next = (self._sizes_next + 1) % len(self._sizes)
         self._h.sample_export_async(edges, unique, sizes, st)
@@ -668,8 +670,8 @@ class Dataloader:
         cur = torch.cuda.current_stream(self.device)
         cur.wait_stream(self._gat)
         cur.wait_event(decided)
-        for t in (rows, unique, *batch.layers):
-            t.record_stream(cur)
+        rows.record_stream(cur)
+        unique.record_stream(cur)  # (the layers share unique's allocation)
         if self.cfg.verify_gather:
             self._verify(unique, rows)
         stats = self._account(c.sampled, c.cache_hits, c.cpu_buffer_hits, c.storage,
