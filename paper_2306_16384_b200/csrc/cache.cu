@@ -26,6 +26,8 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <chrono>
+
 #include "gids_internal.cuh"
 
 namespace {
@@ -1010,8 +1012,20 @@ size_t gids_exact_smem_bytes(int64_t L, bool with_bits) {
     return sizeof(uint32_t) * (size_t)(nb + ns + (with_bits ? 2 * nw : 0));
 }
 
+// host time per section of the serve launch sequence (GIDS_SERVE_TIMING=1,
+// printed at gids_destroy): where the API calls of a latency-bound batch go
+#define HT(i)                                                                        \
+    do {                                                                             \
+        if (h->host_timing) {                                                        \
+            const auto _n = std::chrono::steady_clock::now();                        \
+            h->host_ns[i] += std::chrono::duration<double, std::nano>(_n - _ht).count(); \
+            _ht = _n;                                                                \
+        }                                                                            \
+    } while (0)
+
 int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t epoch, float* out,
                       cudaStream_t st, cudaStream_t gst) {
+    auto _ht = std::chrono::steady_clock::now();
     const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
     // decision buffers: reuse the set of batch b-2 only after its gather finished
     h->parity ^= 1;
@@ -1026,9 +1040,11 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     gids_harvest_gather(h, par);  // batch b-2's gather timing (profiling only)
     gids_mark(h, 2, st);
     if (h->n_shards > 0) return gids_launch_shard_serve(h, uniq, n, out, st, gst, par);
+    HT(0);
     GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
     if (n > 0) {
         GIDS_CUDA_TRY(cudaMemsetAsync(h->ins, 0xff, sizeof(int32_t) * n, st));
+        HT(1);
         int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
         k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
                                               h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
@@ -1036,6 +1052,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                                               exact ? h->xcls : nullptr, h->cand_of_slot,
                                               h->cand_slot, &h->svc->n_cand, &h->svc->bad_order);
         GIDS_LAUNCH_CHECK(h);
+        HT(2);
         if (exact) {
             size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
             int rc = launch_exact_seq(h, n, smem, st);
@@ -1065,9 +1082,11 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                 h->safe_bits, h->cfg.evict_key, epoch, h->kind, h->line, h->ins, h->meta);
             GIDS_LAUNCH_CHECK(h);
         }
+        HT(3);
         k_tier_count<<<g, BLOCK, 0, st>>>(uniq, n, h->kind, h->pinned_off, h->svc, h->flag_hit,
                                           h->flag_host);
         GIDS_LAUNCH_CHECK(h);
+        HT(4);
         // ordered compaction of the gather's work lists (CUB, stable)
         thrust::counting_iterator<int32_t> pos(0);
         thrust::transform_iterator<HostItem, thrust::counting_iterator<int32_t>, int2> items(
@@ -1090,6 +1109,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(h->sel_tmp, tb, items, h->flag_host, h->host_list,
                                                  h->list_cnt + 1, n, st));
         h->launches += 2;
+        HT(5);
         if (h->ft) {  // file-backed storage tier: plan this batch's page reads
             int rc = gids_file_plan(h, par, st);
             if (rc) return rc;
@@ -1101,6 +1121,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     GIDS_CUDA_TRY(cudaEventRecord(h->counted, st));
     h->counted_valid = true;
     h->last_serve_n = n;
+    HT(6);
     if (n > 0) {
         if (gst != st) {
             GIDS_CUDA_TRY(cudaEventRecord(h->decided, st));
@@ -1114,6 +1135,8 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
         h->gather_pending[par] = h->profiling;
         h->serve_timed = h->profiling;
     }
+    HT(7);
+    if (h->host_timing) h->host_calls++;
     return GIDS_OK;
 }
 

@@ -98,6 +98,7 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
     const size_t static_smem = 4096;  // k_exact_seq's event ring
     h->exact_smem = with_bits + static_smem <= (size_t)dev_smem;
     {
+        h->host_timing = getenv("GIDS_SERVE_TIMING") && getenv("GIDS_SERVE_TIMING")[0] == '1';
         const char* e = getenv("GIDS_EXACT_PAR");
         // (a cache with a line for every node never fills: the CTA kernel
         // and its launches are skipped)
@@ -281,6 +282,14 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
 
 int gids_destroy(gids_handle* h) {
     if (!h) return GIDS_OK;
+    if (h->host_timing && h->host_calls)
+        fprintf(stderr, "gids serve host us/call: wait %.1f memset %.1f consume %.1f policy %.1f "
+                "tiers %.1f select %.1f counts %.1f gather %.1f (%lld calls)\n",
+                h->host_ns[0] / h->host_calls / 1e3, h->host_ns[1] / h->host_calls / 1e3,
+                h->host_ns[2] / h->host_calls / 1e3, h->host_ns[3] / h->host_calls / 1e3,
+                h->host_ns[4] / h->host_calls / 1e3, h->host_ns[5] / h->host_calls / 1e3,
+                h->host_ns[6] / h->host_calls / 1e3, h->host_ns[7] / h->host_calls / 1e3,
+                (long long)h->host_calls);
     cudaSetDevice(h->device);
     cudaDeviceSynchronize();
     gids_file_free(h);

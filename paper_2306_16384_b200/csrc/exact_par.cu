@@ -908,7 +908,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 else if (E == x.MISC[9]) st_chg++;
             }
         }
-        if (t == E && E < Epre) x.CONV[cidx >> 5] |= 1u << (cidx & 31);  // (only this lane writes)
+        if (t == E && E < Epre)  // (atomic: other lanes OR their pend_cidx bits into the same words)
+            atomicOr(&x.CONV[cidx >> 5], 1u << (cidx & 31));
         // ---------------- G: commit the accesses [pos, pos + E)
         if (pend_cidx >= 0) atomicOr(&x.CONV[pend_cidx >> 5], 1u << (pend_cidx & 31));
         pend_cidx = -1;

@@ -213,6 +213,9 @@ struct gids_handle {
     // sampler workspace (HBM)
     int64_t max_seeds;
     int window_lists = 0;  // lists pushed and not popped (future[] is 8-bit)
+    bool host_timing = false;  // GIDS_SERVE_TIMING=1: host ns per serve section
+    double host_ns[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int64_t host_calls = 0;
     unsigned long long* line_mark = nullptr;  // shared cache (owner role): (batch, pos) of each line's last insert
     uint64_t* shared_rows = nullptr; // shared cache (requester role): owners' cache_rows pointers
     int32_t shared_rows_g = 0;

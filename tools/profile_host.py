@@ -59,3 +59,4 @@ for key in ("tottime", "cumulative"):
     s = io.StringIO()
     pstats.Stats(pr, stream=s).sort_stats(key).print_stats(30)
     print(s.getvalue())
+dl.close()
