@@ -1,7 +1,7 @@
 """Owner-sharded cache of data-parallel ranks (SURVEY.md section 8(e) exchange
-step; shared_cache.py, csrc/shared_cache.cu).  Two ranks on one GPU (gloo
-control plane, CUDA IPC between the processes): node v is cached only by rank
-v % 2, which decides both ranks' accesses of it with the reference policy in
+step; shared_cache.py, csrc/shared_cache.cu).  Two and three ranks on one GPU
+(gloo control plane, CUDA IPC between the processes): node v is cached only
+by rank v % G, which decides both ranks' accesses of it with the reference policy in
 global batch order.  Per global batch, the unique nodes and the tier counts
 equal the multi-rank oracle -- one reference CacheState per owner
 (oracle.shared_cache_tiers) -- and every gathered row, whether peer-loaded
@@ -42,7 +42,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                             world_size=world)
     try:
-        dl = Dataloader(make_config({**CFG, "gids_dp_rank": rank}))
+        dl = Dataloader(make_config({**CFG, "gids_dp_rank": rank, "gids_dp_world": world}))
         out = []
         for _ in range(STEPS):
             mb, rows, st = dl.next_batch()
@@ -59,7 +59,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_ranks_one_owner_sharded_cache_match_oracle():
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_share_one_owner_sharded_cache_match_oracle(world):
     from _setup import resolve
     from oracle import oracle as O
     from paper_2306_16384_b200 import make_config
@@ -68,20 +69,20 @@ def test_two_ranks_one_owner_sharded_cache_match_oracle():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
     got = {r: rest for r, *rest in (q.get(timeout=600) for _ in ps)}
     for p in ps:
         p.join(timeout=120)
-    for r in range(2):
+    for r in range(world):
         assert got[r][2] is None, got[r][2]
 
     base = make_config({**CFG, "gids_shared_cache": False, "gids_dp_world": 1})
     r0 = resolve(base)
     batches, words = [], []
-    for rank in range(2):
-        cfg = make_config({**CFG, "gids_dp_rank": rank})
+    for rank in range(world):
+        cfg = make_config({**CFG, "gids_dp_rank": rank, "gids_dp_world": world})
         ss = np.random.SeedSequence(cfg.seed).spawn(6)
         words.append(pcg_words(np.random.Generator(np.random.PCG64(ss[2]).jumped(rank))))
         batches.append(list(_seed_stream(cfg, cfg.num_nodes, ss[5], ss[3])))
@@ -91,16 +92,16 @@ def test_two_ranks_one_owner_sharded_cache_match_oracle():
     table = r0["table"]
     hits = 0
     for s in range(STEPS):
-        for rank in range(2):
+        for rank in range(world):
             u, tiers, rows_sha = got[rank][0][s]
-            wu, wt = want[s * 2 + rank]
+            wu, wt = want[s * world + rank]
             assert np.array_equal(u, wu), (s, rank)
             assert tiers == wt, (s, rank, tiers, wt)
             assert rows_sha == hashlib.sha256(table[u].tobytes()).hexdigest(), (s, rank)
             hits += tiers[0]
     assert hits > 0  # some rows came from the owners' lines
     # each owner's lines hold only its own nodes
-    for rank in range(2):
+    for rank in range(world):
         lines = got[rank][1]
         held = lines[lines >= 0]
-        assert len(held) and np.all(held % 2 == rank)
+        assert len(held) and np.all(held % world == rank)
