@@ -54,7 +54,8 @@ constexpr int XW = XT / 32;
 constexpr int XP_MAX_CHG = 64;    // set changes per round (the round ends before the 65th)
 constexpr int RING = 4096;        // staged accesses (ev, class)
 constexpr int HRING = 4096;       // staged draw halves
-constexpr int RING_LAG = 12;      // commit groups allowed in flight when a round reads
+constexpr int RING_LAG = 4;       // commit groups allowed in flight when a round reads: a round
+                                  // reads entries staged >= (RING - 2 XT) / XT rounds ago
 constexpr int32_t NEG = -(1 << 29);
 constexpr int MOVN = 2048;        // moved-line filter: buckets (lines >> movs)
 constexpr int MOVSPAN = 8;        // longer moves / ranges: every earlier MU is checked
