@@ -173,6 +173,12 @@ GIDS_API int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, ui
  * caller may launch the next batches' sampling before asking. */
 GIDS_API int gids_serve_counts(gids_handle* h, gids_tier_counts* out);
 
+/* Hand the last gids_serve's batch to `stream` without blocking the host:
+ * `stream` waits (device-side) for that call's decisions and its gather.
+ * The host-side counterpart of next_batch returning rows the caller's stream
+ * may read (dataloader.py:232-299 returns host arrays instead). */
+GIDS_API int gids_wait_served(gids_handle* h, void* stream);
+
 /* Per-node decisions of the last gids_serve: kind int8[U] (GIDS_KIND_*) and
  * line int64[U] (-1 on bypass).  Device pointers. */
 GIDS_API int gids_serve_decisions(gids_handle* h, int8_t* kind_dev, int64_t* line_dev, void* stream);

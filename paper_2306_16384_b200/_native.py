@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         "gids_window_pop": ([vp, vp, i64, vp], C.c_int),
         "gids_serve": ([vp, vp, i64, u64, vp, vp, vp], C.c_int),
         "gids_serve_counts": ([vp, C.POINTER(TierCounts)], C.c_int),
+        "gids_wait_served": ([vp, vp], C.c_int),
         "gids_serve_decisions": ([vp, vp, vp, vp], C.c_int),
         "gids_cache_stats": ([vp, C.POINTER(CacheCounters)], C.c_int),
         "gids_cache_rng": ([vp, vp], C.c_int),
@@ -150,7 +151,7 @@ def exported_symbols() -> list[str]:
             "gids_contribution_async", "gids_host_register", "gids_host_unregister",
             "gids_exact_par_batches", "gids_exact_par_stats", "gids_owner_split",
             "gids_shared_marks", "gids_shared_final", "gids_shared_unsplit", "gids_shared_tiers",
-            "gids_shared_gather", "gids_cache_rows_ptr"]
+            "gids_shared_gather", "gids_cache_rows_ptr", "gids_wait_served"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -322,6 +323,10 @@ class Handle:
     def serve(self, unique, epoch: int, out, stream: int, gather_stream: int | None = None) -> None:
         check(lib().gids_serve(self.h, _p(unique), unique.numel(), epoch, _p(out), stream,
                                gather_stream), "serve")
+
+    def wait_served(self, stream: int) -> None:
+        """`stream` waits (device-side) for the last serve's decisions and gather."""
+        check(lib().gids_wait_served(self.h, stream), "wait_served")
 
     def serve_counts(self) -> TierCounts:
         t = TierCounts()

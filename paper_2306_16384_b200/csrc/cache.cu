@@ -22,9 +22,6 @@
 //                     in parallel (k_post_*).
 //   set-associative   32-way sets, one warp per set, lanes = ways; the same
 //                     contract per set with a counter-based eviction draw.
-#include <cub/cub.cuh>
-#include <thrust/iterator/counting_iterator.h>
-#include <thrust/iterator/transform_iterator.h>
 
 #include <chrono>
 
@@ -93,8 +90,12 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                                  int32_t* counts = nullptr, int64_t* nmiss0 = nullptr,
                                  uint32_t* xcls = nullptr, int32_t* cand_of_slot = nullptr,
                                  int32_t* cand_slot = nullptr, int64_t* n_cand = nullptr,
-                                 int64_t* bad_order = nullptr) {
+                                 int64_t* bad_order = nullptr, int64_t* zero2 = nullptr) {
     int64_t inc = 0, dec = 0, unsafe = 0, miss0 = 0;
+    if (zero2 && blockIdx.x == 0 && threadIdx.x == 0) {  // the batch's work-list counts
+        zero2[0] = 0;
+        zero2[1] = 0;
+    }
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = (int32_t)uniq[p];
@@ -770,47 +771,74 @@ __global__ void k_post_b(const int64_t* __restrict__ uniq, const ServeCounters* 
 // plus the flags from which the gather's work lists are compacted (in
 // position order: ascending node ids, so host-tier reads walk the backing
 // table upward -- measured 10% faster over the host link than a scrambled order)
-__global__ void k_tier_count(const int64_t* __restrict__ uniq, int64_t n,
-                             const int8_t* __restrict__ kind, const int32_t* __restrict__ pinned_off,
-                             ServeCounters* svc, uint8_t* __restrict__ flag_hit,
-                             uint8_t* __restrict__ flag_host) {
+// tier counts and the gather's two work lists in one pass: hit positions,
+// and (position, source row) of the host-tier rows -- constant-buffer row
+// >= 0 or backing row x encoded -(x+1).  Each block tile reserves its range
+// of a list with one atomic, so a list is ascending within a tile (the
+// tiles' order is the blocks' arrival order; the gather does not depend on it).
+__global__ void __launch_bounds__(BLOCK)
+k_tier_lists(const int64_t* __restrict__ uniq, int64_t n, const int8_t* __restrict__ kind,
+             const int32_t* __restrict__ pinned_off, ServeCounters* svc,
+             int32_t* __restrict__ hit_list, int2* __restrict__ host_list, int64_t* list_cnt) {
+    __shared__ uint32_t s_w[BLOCK / 32];
+    __shared__ uint32_t s_base[2];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     int64_t a = 0, b = 0, c = 0, d = 0;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        int k = kind[p];
-        flag_hit[p] = k == GIDS_KIND_HIT;
-        flag_host[p] = k != GIDS_KIND_HIT;
-        if (k == GIDS_KIND_HIT) {
-            a++;
-            continue;
+    for (int64_t p0 = (int64_t)blockIdx.x * BLOCK; p0 < n; p0 += (int64_t)gridDim.x * BLOCK) {
+        const int64_t p = p0 + t;
+        const bool valid = p < n;
+        const int k = valid ? kind[p] : GIDS_KIND_HIT;
+        const bool hit = valid && k == GIDS_KIND_HIT, host = valid && k != GIDS_KIND_HIT;
+        int2 item = make_int2(0, 0);
+        if (hit) a++;
+        if (host) {
+            const int64_t x = uniq[p];
+            const int32_t off = pinned_off[x];
+            item = make_int2((int32_t)p, off >= 0 ? off : (int32_t)(-(x + 1)));
+            d += k == GIDS_KIND_BYPASS;
+            if (off >= 0) b++;
+            else c++;
         }
-        d += k == GIDS_KIND_BYPASS;
-        if (pinned_off[uniq[p]] >= 0) b++;
-        else c++;
+        // block exclusive scan of (hit, host), packed in 16-bit halves
+        const uint32_t mine = (hit ? 1u : 0u) | (host ? 1u << 16 : 0u);
+        uint32_t inc = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += u;
+        }
+        if (lane == 31) s_w[wid] = inc;
+        __syncthreads();
+        uint32_t ws = lane < BLOCK / 32 ? s_w[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < BLOCK / 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += u;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, ws, BLOCK / 32 - 1);
+        const uint32_t ex = inc - mine + (wid > 0 ? __shfl_sync(0xffffffffu, ws, wid > 0 ? wid - 1 : 0) : 0u);
+        if (t == 0) {
+            s_base[0] = (uint32_t)atomicAdd((unsigned long long*)&list_cnt[0],
+                                            (unsigned long long)(tot & 0xffffu));
+            s_base[1] = (uint32_t)atomicAdd((unsigned long long*)&list_cnt[1],
+                                            (unsigned long long)(tot >> 16));
+        }
+        __syncthreads();
+        if (hit) hit_list[s_base[0] + (ex & 0xffffu)] = (int32_t)p;
+        if (host) host_list[s_base[1] + (ex >> 16)] = item;
+        __syncthreads();  // (s_w / s_base reused by the next tile)
     }
     a = warp_sum64(a);
     b = warp_sum64(b);
     c = warp_sum64(c);
     d = warp_sum64(d);
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
         if (a) atomicAdd((unsigned long long*)&svc->tiers[0], (unsigned long long)a);
         if (b) atomicAdd((unsigned long long*)&svc->tiers[1], (unsigned long long)b);
         if (c) atomicAdd((unsigned long long*)&svc->tiers[2], (unsigned long long)c);
         if (d) atomicAdd((unsigned long long*)&svc->tiers[3], (unsigned long long)d);
     }
 }
-
-// (position, source row) of a host-tier position: constant-buffer row >= 0,
-// or backing row x encoded -(x+1)
-struct HostItem {
-    const int64_t* uniq;
-    const int32_t* pinned_off;
-    __device__ __forceinline__ int2 operator()(int32_t p) const {
-        const int64_t x = uniq[p];
-        const int32_t off = pinned_off[x];
-        return make_int2(p, off >= 0 ? off : (int32_t)(-(x + 1)));
-    }
-};
 
 __global__ void k_post_c(const ServeCounters* svc, const int32_t* __restrict__ log_line,
                          int32_t* last_ins) {
@@ -1050,7 +1078,8 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                                               h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
                                               h->meta, h->ev, 3, nullptr, &h->svc->n_miss0,
                                               exact ? h->xcls : nullptr, h->cand_of_slot,
-                                              h->cand_slot, &h->svc->n_cand, &h->svc->bad_order);
+                                              h->cand_slot, &h->svc->n_cand, &h->svc->bad_order,
+                                              h->list_cnt);
         GIDS_LAUNCH_CHECK(h);
         HT(2);
         if (exact) {
@@ -1083,32 +1112,10 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
             GIDS_LAUNCH_CHECK(h);
         }
         HT(3);
-        k_tier_count<<<g, BLOCK, 0, st>>>(uniq, n, h->kind, h->pinned_off, h->svc, h->flag_hit,
-                                          h->flag_host);
+        k_tier_lists<<<g, BLOCK, 0, st>>>(uniq, n, h->kind, h->pinned_off, h->svc, h->hit_list,
+                                          h->host_list, h->list_cnt);
         GIDS_LAUNCH_CHECK(h);
         HT(4);
-        // ordered compaction of the gather's work lists (CUB, stable)
-        thrust::counting_iterator<int32_t> pos(0);
-        thrust::transform_iterator<HostItem, thrust::counting_iterator<int32_t>, int2> items(
-            pos, HostItem{uniq, h->pinned_off});
-        if (!h->sel_tmp) {
-            size_t b1 = 0, b2 = 0;
-            GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, b1, pos, h->flag_hit, h->hit_list,
-                                                     h->list_cnt, h->serve_cap, st));
-            GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(nullptr, b2, items, h->flag_host,
-                                                     h->host_list, h->list_cnt + 1, h->serve_cap,
-                                                     st));
-            h->sel_tmp_bytes = b1 > b2 ? b1 : b2;
-            GIDS_CUDA_TRY(cudaMalloc(&h->sel_tmp, h->sel_tmp_bytes));
-        }
-        size_t tb = h->sel_tmp_bytes;
-        GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(h->sel_tmp, tb, pos, h->flag_hit, h->hit_list,
-                                                 h->list_cnt, n, st));
-        h->launches += 2;  // CUB: init + select kernels
-        tb = h->sel_tmp_bytes;
-        GIDS_CUDA_TRY(cub::DeviceSelect::Flagged(h->sel_tmp, tb, items, h->flag_host, h->host_list,
-                                                 h->list_cnt + 1, n, st));
-        h->launches += 2;
         HT(5);
         if (h->ft) {  // file-backed storage tier: plan this batch's page reads
             int rc = gids_file_plan(h, par, st);

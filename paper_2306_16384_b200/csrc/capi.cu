@@ -241,7 +241,9 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->unique32, h->unique_cap);
     A(h->jump_tab, GIDS_JUMP_TAB);
     A(h->rng_dev, 2);
-    A(h->sc, 1);
+    h->lb_tiles = ceil_div(ceil_div(N, 32), 256);
+    A(h->sc, 1 + ceil_div((int64_t)sizeof(LbTile) * (cfg->n_layers + 1) * h->lb_tiles,
+                          (int64_t)sizeof(SampleCounters)));
     A(h->contrib_dev, 1);
     h->scan_parts_cap = 1024;
     A(h->scan_parts, 2 * h->scan_parts_cap);
@@ -496,19 +498,12 @@ int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique
                              int64_t* sizes_host, void* stream) {
     CHECK_H(h);
     cudaStream_t st = (cudaStream_t)stream;
-    if (edges_dev) TRY(gids_launch_export_edges(h, edges_dev, st));
-    if (unique_dev) TRY(gids_launch_export_unique(h, unique_dev, st));
+    if (edges_dev || unique_dev) TRY(gids_launch_export(h, edges_dev, unique_dev, st));
     if (sizes_host) {
-        // [layer_len[0..L), n_unique, draws, contribution, overflow]
-        const int L = h->cfg.n_layers;
-        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host, h->sc->layer_len, sizeof(int64_t) * L,
+        // [layer_len[0..L), n_unique, draws, contribution, overflow] (sc->exp)
+        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host, h->sc->exp,
+                                      sizeof(int64_t) * (h->cfg.n_layers + 4),
                                       cudaMemcpyDeviceToHost, st));
-        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host + L, &h->sc->n_unique, sizeof(int64_t),
-                                      cudaMemcpyDeviceToHost, st));
-        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host + L + 1, &h->sc->layer_draw_base[L],
-                                      sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host + L + 2, &h->sc->contribution,
-                                      sizeof(int64_t) * 2, cudaMemcpyDeviceToHost, st));
     }
     return GIDS_OK;
 }
@@ -571,6 +566,15 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
     h->counts_read = false;
     return gids_launch_serve(h, unique_dev, n, epoch, out_dev, (cudaStream_t)stream,
                              gather_stream ? (cudaStream_t)gather_stream : (cudaStream_t)stream);
+}
+
+int gids_wait_served(gids_handle* h, void* stream) {
+    CHECK_H(h);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (h->counted_valid) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->counted, 0));
+    if (h->last_serve_n > 0 && h->gathered_valid[h->parity])
+        GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->gathered[h->parity], 0));
+    return GIDS_OK;
 }
 
 int gids_serve_counts(gids_handle* h, gids_tier_counts* out) {

@@ -133,6 +133,20 @@ struct SampleCounters {
     int64_t n_unique;
     int64_t contribution;
     int64_t overflow;                     // workspace bound exceeded
+    // the batch's sizes as exported ([layer_len[0..L), n_unique, draws,
+    // contribution, overflow]), written by the last compaction
+    int64_t exp[GIDS_MAX_LAYERS + 4];
+    uint32_t tile_ctr[GIDS_MAX_LAYERS + 2];  // single-pass compactions: next tile
+};
+
+// decoupled look-back state of one 8192-node bitmap tile (sampler.cu):
+// the tile's own sums, then the inclusive prefix through it
+struct LbTile {
+    unsigned long long agg;  // take | count << 24 | draws-nodes << 38
+    unsigned long long inc_take;
+    uint32_t inc_cnt, inc_nd;
+    uint32_t flag;           // 0 nothing, 1 agg, 2 inclusive
+    uint32_t pad;
 };
 
 struct ServeCounters {
@@ -225,6 +239,7 @@ struct gids_handle {
     uint32_t* bm_all;      // [ceil(N/32)]
     int32_t* frontier;     // [front_cap]
     int64_t* seeds_dev;    // [max_seeds]
+    int64_t lb_tiles;      // bitmap tiles of 8192 nodes; LbTile[(n_layers+1) * lb_tiles] follow *sc
     int64_t* take_off;     // [front_cap+1] exclusive scan of min(deg, f)
     int64_t* draw_off;     // [front_cap+1] exclusive scan of draws
     int64_t* edges;        // [2*edge_cap]
@@ -387,6 +402,7 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_word
                        cudaStream_t st);
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
 int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st);
+int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st);
 // exact_par.cu
 constexpr int64_t GIDS_XP_CAND_CAP = 1 << 17;
 // access classes of a batch against a full cache (k_window_consume -> k_exact_par)

@@ -14,6 +14,8 @@
 // settled at position t is indices[lo + p] where p starts at j_t and walks
 // s = t-1 .. 0 taking p = s whenever j_s == p (the last earlier swap that
 // moved something into position p).  One warp handles one frontier node.
+#include <cuda/atomic>
+
 #include "gids_internal.cuh"
 
 namespace {
@@ -54,8 +56,200 @@ __global__ void k_seed_mark(const int64_t* __restrict__ seeds, int64_t n, uint32
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t v = (int32_t)seeds[i];
-        mark(bm_front, v);
+        if (bm_front) mark(bm_front, v);
         mark(bm_all, v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Single-pass bitmap compaction (np.unique of a layer's sources,
+// sampler.py:99,103,111): one bitmap word per thread, a tile of 8192 nodes
+// per CTA, tiles taken in launch order from a counter and chained by a
+// decoupled look-back (each tile publishes its own sums at once, then its
+// inclusive prefix), so the whole compaction is one launch with no
+// device-wide barrier.  With TD it also produces the next layer's per-node
+// take = min(deg, f) and draw offsets (scan.cu's three take/draw passes) from
+// the same walk.  The words are cleared for the next use.
+constexpr int LB_BLOCK = 256;
+
+__device__ __forceinline__ void lb_take(const int64_t* __restrict__ indptr, int64_t v, int fanout,
+                                        uint32_t& tk, uint32_t& nd) {
+    const int64_t deg = __ldg(indptr + v + 1) - __ldg(indptr + v);
+    tk += (uint32_t)(deg < fanout ? deg : fanout);
+    nd += deg > fanout ? 1u : 0u;
+}
+
+template <bool TD>
+__global__ void __launch_bounds__(LB_BLOCK)
+k_compact_lb(uint32_t* __restrict__ bm, int64_t nwords, int32_t* __restrict__ out, int64_t cap,
+             LbTile* tiles, uint32_t* tile_ctr, SampleCounters* sc, int layer, int fanout,
+             const int64_t* __restrict__ indptr, int64_t* __restrict__ take_off,
+             int64_t* __restrict__ draw_off, int64_t edge_cap, int n_layers, u128* rng_state,
+             const u128* __restrict__ tab) {
+    __shared__ uint32_t s_tile;
+    __shared__ unsigned long long s_warp[LB_BLOCK / 32];
+    __shared__ unsigned long long s_pre[3];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    if (t == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const int64_t wi = (int64_t)tile * LB_BLOCK + t;
+    const uint32_t w = wi < nwords ? bm[wi] : 0u;
+    if (w) bm[wi] = 0u;
+    uint32_t tk = 0, nd = 0;
+    if (TD && w) {  // up to 8 nodes' degree loads in flight per step
+        uint32_t ww = w;
+        const int64_t* ip = indptr + wi * 32;
+        while (ww) {  // (branch-free: every step issues its loads together)
+            int64_t lo[8], hi[8];
+            uint32_t ok = 0;
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const int b = ww ? __ffs(ww) - 1 : 0;
+                ok |= (ww ? 1u : 0u) << k;
+                ww &= ww - 1;
+                lo[k] = __ldg(ip + b);
+                hi[k] = __ldg(ip + b + 1);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const int64_t d = hi[k] - lo[k];
+                const bool on = (ok >> k) & 1u;
+                tk += on ? (uint32_t)(d < fanout ? d : fanout) : 0u;
+                nd += (on && d > fanout) ? 1u : 0u;
+            }
+        }
+    }
+    typedef unsigned long long u64;
+    const u64 mine = (u64)tk | ((u64)__popc(w) << 24) | ((u64)nd << 38);
+    // block exclusive scan of the packed (take, count, draw-nodes)
+    u64 inc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+    }
+    if (lane == 31) s_warp[wid] = inc;
+    __syncthreads();
+    u64 wsum = lane < LB_BLOCK / 32 ? s_warp[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < LB_BLOCK / 32; o <<= 1) {
+        const u64 u = __shfl_up_sync(0xffffffffu, wsum, o);
+        if (lane >= o) wsum += u;
+    }
+    const u64 agg = __shfl_sync(0xffffffffu, wsum, LB_BLOCK / 32 - 1);
+    const u64 ex = inc - mine + (wid > 0 ? __shfl_sync(0xffffffffu, wsum, wid > 0 ? wid - 1 : 0) : 0ull);
+    if (wid == 0) {  // look-back: the prefix of every earlier tile
+        u64 pc = 0, pt = 0, pn = 0;
+        const u64 at = agg & 0xffffffull, ac = (agg >> 24) & 0x3fffull, an = (agg >> 38) & 0x3fffull;
+        LbTile* me = tiles + tile;
+        if (tile > 0) {
+            if (lane == 0) {
+                me->agg = agg;
+                cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(me->flag).store(
+                    1u, cuda::memory_order_release);
+            }
+            int64_t j0 = (int64_t)tile - 1;
+            while (true) {
+                const int64_t j = j0 - lane;
+                uint32_t f = 2u;  // (before tile 0: an empty inclusive prefix)
+                if (j >= 0) {
+                    cuda::atomic_ref<uint32_t, cuda::thread_scope_device> fl(tiles[j].flag);
+                    do {
+                        f = fl.load(cuda::memory_order_acquire);
+                    } while (f == 0u);
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, f == 2u);
+                const int first = pm ? __ffs(pm) - 1 : 32;
+                u64 vt = 0, vc = 0, vn = 0;
+                if (j >= 0 && lane < first) {
+                    const u64 a = __ldcg(&tiles[j].agg);
+                    vt = a & 0xffffffull;
+                    vc = (a >> 24) & 0x3fffull;
+                    vn = (a >> 38) & 0x3fffull;
+                } else if (j >= 0 && lane == first) {
+                    vt = __ldcg(&tiles[j].inc_take);
+                    vc = __ldcg(&tiles[j].inc_cnt);
+                    vn = __ldcg(&tiles[j].inc_nd);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    vt += __shfl_xor_sync(0xffffffffu, vt, o);
+                    vc += __shfl_xor_sync(0xffffffffu, vc, o);
+                    vn += __shfl_xor_sync(0xffffffffu, vn, o);
+                }
+                pt += vt;
+                pc += vc;
+                pn += vn;
+                if (pm) break;
+                j0 -= 32;
+            }
+        }
+        if (lane == 0) {
+            me->inc_take = pt + at;
+            me->inc_cnt = (uint32_t)(pc + ac);
+            me->inc_nd = (uint32_t)(pn + an);
+            cuda::atomic_ref<uint32_t, cuda::thread_scope_device>(me->flag).store(
+                2u, cuda::memory_order_release);
+            s_pre[0] = pc;
+            s_pre[1] = pt;
+            s_pre[2] = pn;
+        }
+    }
+    __syncthreads();
+    // this thread's nodes at their global positions
+    int64_t pos = (int64_t)(s_pre[0] + ((ex >> 24) & 0x3fffull));
+    if (w) {
+        int64_t take = (int64_t)(s_pre[1] + (ex & 0xffffffull));
+        int64_t dn = (int64_t)(s_pre[2] + ((ex >> 38) & 0x3fffull));
+        uint32_t ww = w;
+        while (ww) {
+            const int64_t v = wi * 32 + (__ffs(ww) - 1);
+            ww &= ww - 1;
+            if (pos < cap) {
+                out[pos] = (int32_t)v;
+                if (TD) {
+                    take_off[pos] = take;
+                    draw_off[pos] = dn * fanout;
+                }
+            }
+            if (TD) {
+                uint32_t a = 0, b = 0;
+                lb_take(indptr, v, fanout, a, b);
+                take += a;
+                dn += b;
+            }
+            pos++;
+        }
+    }
+    if (tile == gridDim.x - 1 && t == 0) {  // the last tile holds the totals
+        const int64_t n = (int64_t)(s_pre[0] + ((agg >> 24) & 0x3fffull));
+        if (n > cap) sc->overflow = 1;
+        if (TD) {
+            const int64_t tt = (int64_t)(s_pre[1] + (agg & 0xffffffull));
+            const int64_t dd = (int64_t)(s_pre[2] + ((agg >> 38) & 0x3fffull)) * fanout;
+            if (n <= cap) {
+                take_off[n] = tt;
+                draw_off[n] = dd;
+            }
+            int64_t base = 0;
+            for (int l = 0; l < layer; l++) base += sc->layer_len[l];
+            sc->n_front = n;
+            sc->layer_len[layer] = tt;
+            sc->layer_draw_base[layer + 1] = sc->layer_draw_base[layer] + dd;
+            if (base + tt > edge_cap) sc->overflow = 1;
+        } else {
+            // the batch's unique nodes; the stream moves past its draws; the
+            // sizes the host reads back
+            sc->n_unique = n;
+            const int64_t draws = sc->layer_draw_base[n_layers];
+            rng_state[0] = jump(rng_state[0], (uint64_t)draws, tab);
+            for (int l = 0; l < n_layers; l++) sc->exp[l] = sc->layer_len[l];
+            sc->exp[n_layers] = n;
+            sc->exp[n_layers + 1] = draws;
+            sc->exp[n_layers + 2] = sc->contribution;
+            sc->exp[n_layers + 3] = sc->overflow;
+        }
     }
 }
 
@@ -73,6 +267,7 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
                int layer, int fanout, const u128* __restrict__ rng_state,
                const u128* __restrict__ tab, int64_t* __restrict__ edges, uint32_t* bm_front,
                uint32_t* bm_all) {
+    // (bm_front null: the last layer, no next frontier)
     extern __shared__ int64_t j_smem[];  // fanout > 32: swap targets per warp
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
@@ -104,7 +299,7 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
                 int32_t src = indices[lo + t];
                 out[2 * t] = src;
                 out[2 * t + 1] = v;
-                mark(bm_front, src);
+                if (bm_front) mark(bm_front, src);
                 mark(bm_all, src);
             }
             continue;
@@ -126,7 +321,7 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
                 int32_t src = indices[lo + p];
                 out[2 * lane] = src;
                 out[2 * lane + 1] = v;
-                mark(bm_front, src);
+                if (bm_front) mark(bm_front, src);
                 mark(bm_all, src);
             }
         } else {
@@ -143,7 +338,7 @@ k_sample_layer(const int64_t* __restrict__ indptr, const int32_t* __restrict__ i
                 int32_t src = indices[lo + p];
                 out[2 * t] = src;
                 out[2 * t + 1] = v;
-                mark(bm_front, src);
+                if (bm_front) mark(bm_front, src);
                 mark(bm_all, src);
             }
             __syncwarp();
@@ -158,29 +353,20 @@ __global__ void k_rng_set(u128* rng_state, u128 state, u128 inc) {
 }
 
 // the batch consumed `draws` doubles: move the device-resident stream past them
-__global__ void k_rng_advance(u128* rng_state, const SampleCounters* sc, int n_layers,
-                              const u128* __restrict__ tab) {
-    rng_state[0] = jump(rng_state[0], (uint64_t)sc->layer_draw_base[n_layers], tab);
-}
-
-// edges of all layers (device-side count) into a caller buffer
-__global__ void k_copy_edges(const int64_t* __restrict__ src, const SampleCounters* sc,
-                             int n_layers, int64_t* __restrict__ dst) {
+// the batch's edges (device-side count) and unique ids widened to int64 into
+// caller buffers, one launch
+__global__ void k_export(const int64_t* __restrict__ src, const SampleCounters* sc, int n_layers,
+                         int64_t* __restrict__ dst, const int32_t* __restrict__ uniq,
+                         int64_t* __restrict__ udst) {
     int64_t e = 0;
     for (int l = 0; l < n_layers; l++) e += sc->layer_len[l];
-    const int64_t n = 2 * e;
+    const int64_t ne = dst ? 2 * e : 0, nu = udst ? sc->n_unique : 0;
+    const int64_t n = ne > nu ? ne : nu;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
-}
-
-// int32 ids -> int64 (export of unique_nodes)
-__global__ void k_widen(const int32_t* __restrict__ in, const SampleCounters* sc,
-                        int64_t* __restrict__ out) {
-    int64_t n = sc->n_unique;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = in[i];
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < ne) dst[i] = src[i];
+        if (i < nu) udst[i] = uniq[i];
+    }
 }
 
 }  // namespace
@@ -209,41 +395,65 @@ static void build_jump_table(uint64_t inc_hi, uint64_t inc_lo, u128* tab) {
 // The per-batch sampling sequence (~20 kernels and copies, all sized by
 // n_seeds and the handle's bounds, every count staying on the device):
 // capturable as one CUDA graph.
+// compaction of one bitmap (LB instance `inst`): with TD the frontier of
+// layer `layer` and its take / draw offsets, else the unique nodes
+static int compact_lb(gids_handle* h, bool td, int inst, int layer, cudaStream_t st) {
+    const int64_t nwords = ceil_div(h->N, 32), nt = h->lb_tiles;
+    LbTile* tiles = reinterpret_cast<LbTile*>(h->sc + 1) + (int64_t)inst * nt;
+    uint32_t* ctr = &h->sc->tile_ctr[inst];
+    if (td)
+        k_compact_lb<true><<<(unsigned)nt, LB_BLOCK, 0, st>>>(
+            h->bm_front, nwords, h->frontier, h->front_cap, tiles, ctr, h->sc, layer,
+            h->cfg.fanouts[layer], h->indptr, h->take_off, h->draw_off, h->edge_cap,
+            h->cfg.n_layers, h->rng_dev, h->jump_tab);
+    else
+        k_compact_lb<false><<<(unsigned)nt, LB_BLOCK, 0, st>>>(
+            h->bm_all, nwords, h->unique32, h->unique_cap, tiles, ctr, h->sc, 0, 1, h->indptr,
+            nullptr, nullptr, h->edge_cap, h->cfg.n_layers, h->rng_dev, h->jump_tab);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
+}
+
+// The per-batch sampling sequence, every count staying on the device:
+// counters, seed marks, then per layer one compaction (frontier + offsets)
+// and one sampling launch, and the unique-node compaction (which also moves
+// the stream on and lays out the exported sizes) -- 2L + 4 graph nodes.
 static int sample_body(gids_handle* h, int64_t n_seeds, bool raw, cudaStream_t st) {
     const gids_config& c = h->cfg;
-    GIDS_CUDA_TRY(cudaMemsetAsync(h->sc, 0, sizeof(SampleCounters), st));
+    GIDS_CUDA_TRY(cudaMemsetAsync(
+        h->sc, 0,
+        sizeof(SampleCounters) + sizeof(LbTile) * (size_t)(c.n_layers + 1) * (size_t)h->lb_tiles,
+        st));
     int rc = GIDS_OK;
     if (raw) {
         k_front_raw<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(
             h->seeds_dev, n_seeds, h->frontier, h->sc, h->bm_all);
         GIDS_LAUNCH_CHECK(h);
+        if (c.n_layers > 0) {
+            rc = gids_scan_take_draw(h, c.fanouts[0], 0, st);
+            if (rc) return rc;
+        }
     } else {
-        k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(h->seeds_dev, n_seeds,
-                                                                         h->bm_front, h->bm_all);
+        k_seed_mark<<<gids_grid(n_seeds, 256, 4 * GIDS_SMS), 256, 0, st>>>(
+            h->seeds_dev, n_seeds, c.n_layers > 0 ? h->bm_front : nullptr, h->bm_all);
         GIDS_LAUNCH_CHECK(h);
-        rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
-                                 st);
-        if (rc) return rc;
     }
     for (int l = 0; l < c.n_layers; l++) {
         int f = c.fanouts[l];
-        rc = gids_scan_take_draw(h, f, l, st);
-        if (rc) return rc;
+        if (l > 0 || !raw) {
+            rc = compact_lb(h, true, l, l, st);
+            if (rc) return rc;
+        }
         size_t smem = f > 32 ? (size_t)SAMPLE_WARPS * f * sizeof(int64_t) : 0;
         int64_t bound = l == 0 ? n_seeds : h->front_cap;
         int grid = gids_grid(bound, SAMPLE_WARPS, 16 * GIDS_SMS);
         k_sample_layer<<<grid, SAMPLE_BLOCK, smem, st>>>(
             h->indptr, h->indices, h->frontier, h->take_off, h->draw_off, h->sc, l, f, h->rng_dev,
-            h->jump_tab, h->edges, h->bm_front, h->bm_all);
+            h->jump_tab, h->edges, l + 1 < c.n_layers ? h->bm_front : nullptr, h->bm_all);
         GIDS_LAUNCH_CHECK(h);
-        rc = gids_bitmap_compact(h, h->bm_front, h->frontier, &h->sc->n_front, h->front_cap, true,
-                                 st);
-        if (rc) return rc;
     }
-    rc = gids_bitmap_compact(h, h->bm_all, h->unique32, &h->sc->n_unique, h->unique_cap, true, st);
+    rc = compact_lb(h, false, c.n_layers, 0, st);
     if (rc) return rc;
-    k_rng_advance<<<1, 1, 0, st>>>(h->rng_dev, h->sc, c.n_layers, h->jump_tab);
-    GIDS_LAUNCH_CHECK(h);
     GIDS_CUDA_TRY(cudaMemcpyAsync(h->sc_host, h->sc, sizeof(SampleCounters),
                                   cudaMemcpyDeviceToHost, st));
     return GIDS_OK;
@@ -326,16 +536,18 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, bool 
     return GIDS_OK;
 }
 
-int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st) {
-    k_copy_edges<<<gids_grid(2 * h->edge_cap, 256, 8 * GIDS_SMS), 256, 0, st>>>(
-        h->edges, h->sc, h->cfg.n_layers, edges_dev);
+int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st) {
+    const int64_t bound = 2 * h->edge_cap > h->unique_cap ? 2 * h->edge_cap : h->unique_cap;
+    k_export<<<gids_grid(bound, 256, 8 * GIDS_SMS), 256, 0, st>>>(
+        h->edges, h->sc, h->cfg.n_layers, edges_dev, h->unique32, unique_dev);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }
 
+int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st) {
+    return gids_launch_export(h, edges_dev, nullptr, st);
+}
+
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st) {
-    k_widen<<<gids_grid(h->unique_cap, 256, 8 * GIDS_SMS), 256, 0, st>>>(h->unique32, h->sc,
-                                                                       unique_dev);
-    GIDS_LAUNCH_CHECK(h);
-    return GIDS_OK;
+    return gids_launch_export(h, nullptr, unique_dev, st);
 }

@@ -1,0 +1,67 @@
+"""Inclusive host time per call of the functions on Dataloader.next_batch's
+path (perf_counter wrappers, ~0.3 us each; no profiler), at a bench workload.
+
+    python tools/host_breakdown.py [c1|c2|...] [steps]
+"""
+import collections
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2306_16384_b200 import Dataloader, _native, make_config  # noqa: E402
+from paper_2306_16384_b200 import loader as L  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "c1"
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 300
+acc = collections.defaultdict(lambda: [0, 0])
+
+
+def wrap(owner, name, label=None):
+    f = getattr(owner, name)
+    key = label or f"{getattr(owner, '__name__', type(owner).__name__)}.{name}"
+
+    def w(*a, **k):
+        t = time.perf_counter_ns()
+        try:
+            return f(*a, **k)
+        finally:
+            e = acc[key]
+            e[0] += 1
+            e[1] += time.perf_counter_ns() - t
+    setattr(owner, name, w)
+
+
+for n in ("next_batch", "run_ahead", "_sample_one", "_launch_sample", "_speculate", "_resolve",
+          "_out_block", "_account", "_storage_at_least"):
+    wrap(L.Dataloader, n)
+for n in ("sample", "sample_export_async", "contribution_async", "window_push", "window_pop",
+          "serve", "serve_counts"):
+    wrap(_native.Handle, n)
+wrap(L._Queued, "resolve")
+wrap(torch.cuda.Event, "record", "Event.record")
+wrap(torch.cuda.Stream, "wait_event", "Stream.wait_event")
+wrap(torch.cuda, "current_stream", "torch.cuda.current_stream")
+
+cfg = make_config({**bench.WORKLOADS[wl], "gids_policy": bench.DEFAULT_POLICY[wl]})
+dl = Dataloader(cfg)
+for n in ("push_iteration", "pop_iteration"):
+    wrap(type(dl.window), n)
+for _ in range(40):
+    dl.next_batch()
+torch.cuda.synchronize()
+acc.clear()
+t0 = time.perf_counter()
+for _ in range(steps):
+    dl.next_batch()
+torch.cuda.synchronize()
+el = (time.perf_counter() - t0) / steps * 1e6
+print(f"{wl}: {el:.1f} us per next_batch (with wrappers)")
+for k, (c, ns) in sorted(acc.items(), key=lambda x: -x[1][1]):
+    print(f"  {k:40s} calls/batch {c / steps:5.2f}  us/call {ns / c / 1e3:7.2f}  "
+          f"us/batch {ns / steps / 1e3:7.2f}")
+dl.close()
