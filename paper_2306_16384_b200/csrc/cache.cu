@@ -90,7 +90,12 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
                                  int32_t* counts = nullptr, int64_t* nmiss0 = nullptr,
                                  uint32_t* xcls = nullptr, int32_t* cand_of_slot = nullptr,
                                  int32_t* cand_slot = nullptr, int64_t* n_cand = nullptr,
-                                 int64_t* bad_order = nullptr, int64_t* zero2 = nullptr) {
+                                 int64_t* bad_order = nullptr, int64_t* zero2 = nullptr,
+                                 int32_t* ins = nullptr, const ServeArgs* sa = nullptr) {
+    if (sa) {
+        uniq = sa->uniq;
+        n = sa->n;
+    }
     int64_t inc = 0, dec = 0, unsafe = 0, miss0 = 0;
     if (zero2 && blockIdx.x == 0 && threadIdx.x == 0) {  // the batch's work-list counts
         zero2[0] = 0;
@@ -99,6 +104,7 @@ __global__ void k_window_consume(const int64_t* __restrict__ uniq, int64_t n,
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int32_t x = (int32_t)uniq[p];
+        if (ins) ins[p] = -1;  // (no insertion unless a policy logs one)
         // the serving precondition (strictly ascending, hence distinct): the
         // counters below are updated without atomics
         if (bad_order && p > 0 && uniq[p - 1] >= uniq[p]) *bad_order = 1;
@@ -397,8 +403,9 @@ __device__ __forceinline__ int32_t list_rebuild(const ExactTables& t, int64_t nw
 __global__ void k_exact_allhit(const uint32_t* __restrict__ ev, int64_t n, CacheMeta* meta,
                                uint32_t* safe_bits, uint32_t* blk, uint32_t* sup,
                                const ServeCounters* __restrict__ svc, int8_t* __restrict__ kind,
-                               int32_t* __restrict__ line) {
+                               int32_t* __restrict__ line, const ServeArgs* sa = nullptr) {
     if (svc->n_miss0 != 0) return;
+    if (sa) n = sa->n;
     int64_t adds = 0;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
@@ -428,10 +435,11 @@ __global__ void __launch_bounds__(32, 1)
 k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* meta,
             uint32_t* g_safe, uint32_t* g_evict, uint32_t* g_blk, uint32_t* g_sup, int smem_bits,
             int8_t* __restrict__ kind, int32_t* __restrict__ line, int32_t* __restrict__ log_line,
-            int32_t* __restrict__ log_pos, ServeCounters* svc) {
+            int32_t* __restrict__ log_pos, ServeCounters* svc, const ServeArgs* sa = nullptr) {
     extern __shared__ uint32_t sm[];
     if (svc->n_miss0 == 0) return;  // all hits: decided by k_exact_allhit
     if (svc->xp_done) return;       // full cache: decided by k_exact_par
+    if (sa) n = sa->n;
     const int lane = threadIdx.x;
     const unsigned below = (1u << lane) - 1u;
     const int64_t nw = (L + 31) / 32, nb = (L + 1023) / 1024, ns = (L + 32767) / 32768;
@@ -719,7 +727,8 @@ k_exact_seq(const uint32_t* __restrict__ ev, int64_t n, int64_t L, CacheMeta* me
 __global__ void k_post_a(const int64_t* __restrict__ uniq, const ServeCounters* svc,
                          const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
                          const int32_t* __restrict__ line_node, int32_t* slot_of, int32_t* last_ins,
-                         uint32_t* g_evict, int clear_evict) {
+                         uint32_t* g_evict, int clear_evict, const ServeArgs* sa = nullptr) {
+    if (sa) uniq = sa->uniq;
     int64_t n = svc->n_log;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -752,7 +761,8 @@ __global__ void k_victims(const int64_t* __restrict__ uniq, const ServeCounters*
 __global__ void k_post_b(const int64_t* __restrict__ uniq, const ServeCounters* svc,
                          const int32_t* __restrict__ log_line, const int32_t* __restrict__ log_pos,
                          int32_t* line_node, int32_t* slot_of, const int32_t* __restrict__ last_ins,
-                         int32_t* __restrict__ ins) {
+                         int32_t* __restrict__ ins, const ServeArgs* sa = nullptr) {
+    if (sa) uniq = sa->uniq;
     int64_t n = svc->n_log;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -779,7 +789,12 @@ __global__ void k_post_b(const int64_t* __restrict__ uniq, const ServeCounters* 
 __global__ void __launch_bounds__(BLOCK)
 k_tier_lists(const int64_t* __restrict__ uniq, int64_t n, const int8_t* __restrict__ kind,
              const int32_t* __restrict__ pinned_off, ServeCounters* svc,
-             int32_t* __restrict__ hit_list, int2* __restrict__ host_list, int64_t* list_cnt) {
+             int32_t* __restrict__ hit_list, int2* __restrict__ host_list, int64_t* list_cnt,
+             const ServeArgs* sa = nullptr) {
+    if (sa) {
+        uniq = sa->uniq;
+        n = sa->n;
+    }
     __shared__ uint32_t s_w[BLOCK / 32];
     __shared__ uint32_t s_base[2];
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -859,14 +874,22 @@ __device__ __forceinline__ uint32_t sa_draw(uint64_t key, uint64_t epoch, int64_
 }
 
 __global__ void k_sa_hist(const int64_t* __restrict__ uniq, int64_t n, int64_t sets,
-                          int32_t* set_cnt) {
+                          int32_t* set_cnt, const ServeArgs* sa = nullptr) {
+    if (sa) {
+        uniq = sa->uniq;
+        n = sa->n;
+    }
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x)
         atomicAdd(&set_cnt[sa_set_of(uniq[p], sets)], 1);
 }
 __global__ void k_sa_scatter(const int64_t* __restrict__ uniq, int64_t n, int64_t sets,
                              const int64_t* __restrict__ set_off, int32_t* set_cur,
-                             int32_t* bucket) {
+                             int32_t* bucket, const ServeArgs* sa = nullptr) {
+    if (sa) {
+        uniq = sa->uniq;
+        n = sa->n;
+    }
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
          p += (int64_t)gridDim.x * blockDim.x) {
         int64_t s = sa_set_of(uniq[p], sets);
@@ -882,7 +905,11 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
              const int32_t* __restrict__ set_cnt, const int64_t* __restrict__ set_off,
              int32_t* bucket, int32_t* line_node, int32_t* slot_of, uint32_t* safe_bits,
              uint64_t key, uint64_t epoch, int8_t* kind, int32_t* line, int32_t* ins,
-             CacheMeta* meta) {
+             CacheMeta* meta, const ServeArgs* sa = nullptr) {
+    if (sa) {
+        uniq = sa->uniq;
+        epoch = sa->epoch;
+    }
     __shared__ int32_t order[SA_WARPS][SA_SORT_MAX];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int64_t hits = 0, misses = 0, byp = 0, evs = 0;
@@ -997,13 +1024,14 @@ k_sa_process(const int64_t* __restrict__ uniq, const uint32_t* __restrict__ ev, 
 
 }  // namespace
 
-static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t st) {
+static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t st,
+                            const ServeArgs* sa) {
     {
-        int rc = gids_launch_exact_par(h, n, st);
+        int rc = gids_launch_exact_par(h, n, st, sa);
         if (rc) return rc;
     }
     k_exact_allhit<<<gids_grid(n, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
-        h->ev, n, h->meta, h->safe_bits, h->blk_cnt, h->sup_cnt, h->svc, h->kind, h->line);
+        h->ev, n, h->meta, h->safe_bits, h->blk_cnt, h->sup_cnt, h->svc, h->kind, h->line, sa);
     GIDS_LAUNCH_CHECK(h);
     auto k = k_exact_seq;
     static size_t attr_smem = 48 * 1024;  // (per function: set when it grows)
@@ -1014,7 +1042,7 @@ static int launch_exact_seq(gids_handle* h, int64_t n, size_t smem, cudaStream_t
     }
     k<<<1, 32, smem, st>>>(h->ev, n, h->L, h->meta, h->safe_bits, h->evict_bits, h->blk_cnt,
                            h->sup_cnt, h->exact_smem ? 1 : 0, h->kind, h->line, h->log_line,
-                           h->log_pos, h->svc);
+                           h->log_pos, h->svc, sa);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }
@@ -1051,10 +1079,103 @@ size_t gids_exact_smem_bytes(int64_t L, bool with_bits) {
         }                                                                            \
     } while (0)
 
+// a serve replayed as a graph reads its per-call arguments from here
+__global__ void k_serve_args(ServeArgs* sa, const int64_t* uniq, int64_t n, uint64_t epoch,
+                             float* out) {
+    sa->uniq = uniq;
+    sa->n = n;
+    sa->epoch = epoch;
+    sa->out = out;
+}
+
+// the decisions of one batch on `st`: counters, window update + reuse
+// consumption, the policy, tier counts and the gather's work lists, the
+// counts' copy to the host.  sa != NULL: a graph capture -- n is then the
+// workspace bound (grid sizes) and the kernels read the call's uniq / n /
+// epoch from sa.
+static int serve_decisions(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t epoch,
+                           cudaStream_t st, const ServeArgs* sa,
+                           std::chrono::steady_clock::time_point& _ht) {
+    const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
+    GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
+    HT(1);
+    int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
+    k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
+                                          h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
+                                          h->meta, h->ev, 3, nullptr, &h->svc->n_miss0,
+                                          exact ? h->xcls : nullptr, h->cand_of_slot,
+                                          h->cand_slot, &h->svc->n_cand, &h->svc->bad_order,
+                                          h->list_cnt, h->ins, sa);
+    GIDS_LAUNCH_CHECK(h);
+    HT(2);
+    if (exact) {
+        size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
+        int rc = launch_exact_seq(h, n, smem, st, sa);
+        if (rc) return rc;
+        k_post_a<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
+                                      h->slot_of, h->last_ins, h->evict_bits,
+                                      h->exact_smem ? 0 : 1, sa);
+        GIDS_LAUNCH_CHECK(h);
+        k_post_b<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
+                                      h->slot_of, h->last_ins, h->ins, sa);
+        GIDS_LAUNCH_CHECK(h);
+        k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
+        GIDS_LAUNCH_CHECK(h);
+        int rc2 = gids_launch_xp_reset(h, st);
+        if (rc2) return rc2;
+    } else {
+        GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cnt, 0, sizeof(int32_t) * h->sets, st));
+        GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cur, 0, sizeof(int32_t) * h->sets, st));
+        k_sa_hist<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_cnt, sa);
+        GIDS_LAUNCH_CHECK(h);
+        int rc = gids_scan_i32_to_i64(h, h->set_cnt, h->sets, h->set_off, st);
+        if (rc) return rc;
+        k_sa_scatter<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_off, h->set_cur, h->bucket,
+                                          sa);
+        GIDS_LAUNCH_CHECK(h);
+        k_sa_process<<<gids_grid(h->sets, SA_WARPS, 16 * GIDS_SMS), BLOCK, 0, st>>>(
+            uniq, h->ev, h->sets, h->set_cnt, h->set_off, h->bucket, h->line_node, h->slot_of,
+            h->safe_bits, h->cfg.evict_key, epoch, h->kind, h->line, h->ins, h->meta, sa);
+        GIDS_LAUNCH_CHECK(h);
+    }
+    HT(3);
+    k_tier_lists<<<g, BLOCK, 0, st>>>(uniq, n, h->kind, h->pinned_off, h->svc, h->hit_list,
+                                      h->host_list, h->list_cnt, sa);
+    GIDS_LAUNCH_CHECK(h);
+    HT(4);
+    GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
+                                  cudaMemcpyDeviceToHost, st));
+    return GIDS_OK;
+}
+
+// one capture of `st`'s work into *exec (kernel count into *kernels); false
+// (capture abandoned, the direct launches are used) on any failure
+template <typename F>
+static bool capture(gids_handle* h, cudaStream_t st, cudaGraphExec_t* exec, int64_t* kernels,
+                    F&& body) {
+    const int64_t l0 = h->launches;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    const int rc = body();
+    cudaGraph_t graph = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(st, &graph);
+    *kernels = h->launches - l0;
+    h->launches = l0;
+    bool ok = rc == GIDS_OK && e == cudaSuccess && graph &&
+              cudaGraphInstantiate(exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+        *exec = nullptr;
+        cudaGetLastError();
+    }
+    return ok;
+}
+
 int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t epoch, float* out,
                       cudaStream_t st, cudaStream_t gst) {
     auto _ht = std::chrono::steady_clock::now();
-    const bool exact = h->cfg.policy == GIDS_POLICY_EXACT;
     // decision buffers: reuse the set of batch b-2 only after its gather finished
     h->parity ^= 1;
     const int par = h->parity;
@@ -1069,61 +1190,38 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     gids_mark(h, 2, st);
     if (h->n_shards > 0) return gids_launch_shard_serve(h, uniq, n, out, st, gst, par);
     HT(0);
-    GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
-    if (n > 0) {
-        GIDS_CUDA_TRY(cudaMemsetAsync(h->ins, 0xff, sizeof(int32_t) * n, st));
-        HT(1);
-        int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
-        k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
-                                              h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
-                                              h->meta, h->ev, 3, nullptr, &h->svc->n_miss0,
-                                              exact ? h->xcls : nullptr, h->cand_of_slot,
-                                              h->cand_slot, &h->svc->n_cand, &h->svc->bad_order,
-                                              h->list_cnt);
+    // replay as two graphs (decisions on st, rows on gst) once the first
+    // serves have set every function attribute: the ~12 launches of a batch
+    // cost more host time than a small batch's device work
+    bool graphs = h->use_graphs && !h->graphs_failed && !h->ft && !h->profiling && n > 0 &&
+                  h->serves >= 2 && st != 0 && st != cudaStreamLegacy && gst != 0 &&
+                  gst != cudaStreamLegacy && gst != st;
+    if (graphs) {
+        ServeArgs* sa = h->sargs + par;
+        k_serve_args<<<1, 1, 0, st>>>(sa, uniq, n, epoch, out);
         GIDS_LAUNCH_CHECK(h);
-        HT(2);
-        if (exact) {
-            size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
-            int rc = launch_exact_seq(h, n, smem, st);
-            if (rc) return rc;
-            k_post_a<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
-                                          h->slot_of, h->last_ins, h->evict_bits,
-                                          h->exact_smem ? 0 : 1);
-            GIDS_LAUNCH_CHECK(h);
-            k_post_b<<<g, BLOCK, 0, st>>>(uniq, h->svc, h->log_line, h->log_pos, h->line_node,
-                                          h->slot_of, h->last_ins, h->ins);
-            GIDS_LAUNCH_CHECK(h);
-            k_post_c<<<g, BLOCK, 0, st>>>(h->svc, h->log_line, h->last_ins);
-            GIDS_LAUNCH_CHECK(h);
-            int rc2 = gids_launch_xp_reset(h, st);
-            if (rc2) return rc2;
-        } else {
-            GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cnt, 0, sizeof(int32_t) * h->sets, st));
-            GIDS_CUDA_TRY(cudaMemsetAsync(h->set_cur, 0, sizeof(int32_t) * h->sets, st));
-            k_sa_hist<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_cnt);
-            GIDS_LAUNCH_CHECK(h);
-            int rc = gids_scan_i32_to_i64(h, h->set_cnt, h->sets, h->set_off, st);
-            if (rc) return rc;
-            k_sa_scatter<<<g, BLOCK, 0, st>>>(uniq, n, h->sets, h->set_off, h->set_cur, h->bucket);
-            GIDS_LAUNCH_CHECK(h);
-            k_sa_process<<<gids_grid(h->sets, SA_WARPS, 16 * GIDS_SMS), BLOCK, 0, st>>>(
-                uniq, h->ev, h->sets, h->set_cnt, h->set_off, h->bucket, h->line_node, h->slot_of,
-                h->safe_bits, h->cfg.evict_key, epoch, h->kind, h->line, h->ins, h->meta);
-            GIDS_LAUNCH_CHECK(h);
-        }
-        HT(3);
-        k_tier_lists<<<g, BLOCK, 0, st>>>(uniq, n, h->kind, h->pinned_off, h->svc, h->hit_list,
-                                          h->host_list, h->list_cnt);
-        GIDS_LAUNCH_CHECK(h);
-        HT(4);
+        if (!h->dgraph[par] &&
+            !capture(h, st, &h->dgraph[par], &h->dgraph_kernels[par], [&] {
+                return serve_decisions(h, nullptr, h->serve_cap, epoch, st, sa, _ht);
+            }))
+            graphs = false, h->graphs_failed = true;  // (direct launches from now on)
+    }
+    if (graphs) {
+        GIDS_CUDA_TRY(cudaGraphLaunch(h->dgraph[par], st));
+        h->launches += h->dgraph_kernels[par];
+    } else if (n > 0) {
+        int rc = serve_decisions(h, uniq, n, epoch, st, nullptr, _ht);
+        if (rc) return rc;
         HT(5);
         if (h->ft) {  // file-backed storage tier: plan this batch's page reads
-            int rc = gids_file_plan(h, par, st);
-            if (rc) return rc;
+            int rc2 = gids_file_plan(h, par, st);
+            if (rc2) return rc2;
         }
+    } else {
+        GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
+        GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
+                                      cudaMemcpyDeviceToHost, st));
     }
-    GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
-                                  cudaMemcpyDeviceToHost, st));
     gids_mark(h, 3, st);  // (before `counted`: serve_counts reads this mark's time)
     GIDS_CUDA_TRY(cudaEventRecord(h->counted, st));
     h->counted_valid = true;
@@ -1134,14 +1232,28 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
             GIDS_CUDA_TRY(cudaEventRecord(h->decided, st));
             GIDS_CUDA_TRY(cudaStreamWaitEvent(gst, h->decided, 0));
         }
-        if (h->profiling) cudaEventRecord(h->gev[par][0], gst);
-        int rc = gids_launch_gather(h, uniq, n, out, gst);
-        if (rc) return rc;
+        if (graphs) {
+            const ServeArgs* sa = h->sargs + par;
+            if (!h->ggraph[par] &&
+                !capture(h, gst, &h->ggraph[par], &h->ggraph_kernels[par], [&] {
+                    return gids_launch_gather(h, nullptr, h->serve_cap, nullptr, gst, sa);
+                }))
+                graphs = false, h->graphs_failed = true;
+        }
+        if (graphs) {
+            GIDS_CUDA_TRY(cudaGraphLaunch(h->ggraph[par], gst));
+            h->launches += h->ggraph_kernels[par];
+        } else {
+            if (h->profiling) cudaEventRecord(h->gev[par][0], gst);
+            int rc = gids_launch_gather(h, uniq, n, out, gst);
+            if (rc) return rc;
+        }
         GIDS_CUDA_TRY(cudaEventRecord(h->gathered[par], gst));
         h->gathered_valid[par] = true;
         h->gather_pending[par] = h->profiling;
         h->serve_timed = h->profiling;
     }
+    h->serves++;
     HT(7);
     if (h->host_timing) h->host_calls++;
     return GIDS_OK;
@@ -1201,7 +1313,7 @@ extern "C" int gids_cache_access(gids_handle* h, const int64_t* nodes, int64_t n
     GIDS_LAUNCH_CHECK(h);
     size_t smem = gids_exact_smem_bytes(h->L, h->exact_smem);
     {
-        int rc = launch_exact_seq(h, n, smem, st);
+        int rc = launch_exact_seq(h, n, smem, st, nullptr);
         if (rc) return rc;
     }
     if (victim_out) {

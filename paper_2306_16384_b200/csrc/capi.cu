@@ -259,6 +259,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         A(h->host_list_buf[b], h->serve_cap);
         A(h->list_cnt_buf[b], 2);
     }
+    A(h->sargs, 2);
     A(h->flag_hit, h->serve_cap);
     A(h->flag_host, h->serve_cap);
     A(h->log_line, h->serve_cap);
@@ -297,6 +298,10 @@ int gids_destroy(gids_handle* h) {
     gids_file_free(h);
     for (int i = 0; i < h->n_sgraphs; i++)
         if (h->sgraphs[i].exec) cudaGraphExecDestroy(h->sgraphs[i].exec);
+    for (int i = 0; i < 2; i++) {
+        if (h->dgraph[i]) cudaGraphExecDestroy(h->dgraph[i]);
+        if (h->ggraph[i]) cudaGraphExecDestroy(h->ggraph[i]);
+    }
     void* ptrs[] = {h->indptr,    h->indices,  h->pinned_off, h->cache_rows, h->slot_of,
                     h->line_node, h->safe_bits, h->evict_bits, h->blk_cnt,   h->sup_cnt,
                     h->reuse,     h->future,   h->meta,       h->last_ins,   h->bm_front,
@@ -310,7 +315,7 @@ int gids_destroy(gids_handle* h) {
                     h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
                     h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev,
                     h->serve_parts, h->serve_word_parts, h->cand_of_slot, h->cand_slot,
-                    h->xcls,      h->xp_halves, h->line_mark, h->shared_rows};
+                    h->xcls,      h->xp_halves, h->line_mark, h->shared_rows, h->sargs};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 8; i++)

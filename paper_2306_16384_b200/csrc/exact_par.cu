@@ -143,6 +143,7 @@ struct XpArgs {
     int32_t* line;
     int32_t* log_line;
     int32_t* log_pos;
+    const ServeArgs* sa;     // (graph replay: n from here)
 };
 
 // shared-memory view of the round state.  Within a round the tables and the
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     }
     x.bsh = 0;
     while (((x.L - 1) >> x.bsh) >= CUMN) x.bsh++;
-    const int32_t n = (int32_t)a.n, nb = x.nb, ns = x.ns;  // (n <= serve_cap < 2^31)
+    const int32_t n = (int32_t)(a.sa ? a.sa->n : a.n), nb = x.nb, ns = x.ns;  // (n <= serve_cap < 2^31)
     const int32_t hcap = (int32_t)a.hcap;
     for (int64_t i = t; i < nb; i += XT) x.CNT[i] = a.blk_cnt[i];
     for (int64_t i = t; i < 2 * nb; i += XT) {  // four 128-line group counts per word
@@ -1054,7 +1055,7 @@ size_t gids_xp_smem_bytes(int64_t L) {
 }
 
 // launched before k_exact_seq; each checks on the device which of them runs
-int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st) {
+int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st, const ServeArgs* sa) {
     if (!h->xp_enabled || n == 0) return GIDS_OK;
     const int64_t outs = (h->xp_hcap + 1) / 2;
     k_xp_halves<<<gids_grid(ceil_div(outs, 8), 256, 1 << 20), 256, 0, st>>>(
@@ -1079,6 +1080,7 @@ int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st) {
     a.line = h->line;
     a.log_line = h->log_line;
     a.log_pos = h->log_pos;
+    a.sa = sa;
     const size_t smem = gids_xp_smem_bytes(h->L);
     static size_t attr_smem = 0;  // (the attribute is per function: set when it grows)
     if (smem > attr_smem) {

@@ -64,7 +64,8 @@ template <typename T, int UNROLL>
 __global__ void __launch_bounds__(BLOCK)
 k_gather_hits(const int32_t* __restrict__ hit_list, const int64_t* __restrict__ list_cnt,
               const int32_t* __restrict__ line, const T* __restrict__ cache_rows,
-              T* __restrict__ out, ChunkIdx ci) {
+              T* __restrict__ out, ChunkIdx ci, const ServeArgs* sa = nullptr) {
+    if (sa) out = reinterpret_cast<T*>(sa->out);
     const uint32_t total = (uint32_t)list_cnt[0] * ci.cpr;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
@@ -97,7 +98,8 @@ __global__ void __launch_bounds__(BLOCK)
 k_gather_host(const int2* __restrict__ host_list, const int64_t* __restrict__ list_cnt,
               const int32_t* __restrict__ ins, const T* __restrict__ buffer_rows,
               const T* __restrict__ backing, T* __restrict__ cache_rows, T* __restrict__ out,
-              ChunkIdx ci) {
+              ChunkIdx ci, const ServeArgs* sa = nullptr) {
+    if (sa) out = reinterpret_cast<T*>(sa->out);
     const uint32_t total = (uint32_t)list_cnt[1] * ci.cpr;
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * BLOCK + threadIdx.x) >> 5;
@@ -181,8 +183,8 @@ static ChunkIdx chunk_idx(int64_t cpr) {
 }
 
 int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* out,
-                       cudaStream_t st) {
-    (void)uniq;
+                       cudaStream_t st, const ServeArgs* sa) {
+    (void)uniq;  // (sa: a graph capture; n is the bound, out and the counts are read on the device)
     const int64_t dim = h->row_floats;
     if ((dim & 3) == 0 ? (n * (dim >> 2) >= ((int64_t)1 << 32)) : (n * dim >= ((int64_t)1 << 32))) {
         gids_set_error("batch too large for the gather's 32-bit chunk index");
@@ -198,10 +200,10 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
         if ((dim & 3) == 0) {
             k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(
                 h->hit_list, h->list_cnt, h->line, reinterpret_cast<const int4*>(h->cache_rows),
-                reinterpret_cast<int4*>(out), chunk_idx(dim >> 2));
+                reinterpret_cast<int4*>(out), chunk_idx(dim >> 2), sa);
         } else {
             k_gather_hits<float, 4><<<hit_grid, BLOCK, 0, st>>>(h->hit_list, h->list_cnt, h->line,
-                                                                h->cache_rows, out, chunk_idx(dim));
+                                                                h->cache_rows, out, chunk_idx(dim), sa);
         }
         GIDS_LAUNCH_CHECK(h);
         if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
@@ -214,7 +216,7 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
         ChunkIdx ci = chunk_idx(dim >> 2);
         k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(
             h->hit_list, h->list_cnt, h->line, reinterpret_cast<const int4*>(h->cache_rows),
-            reinterpret_cast<int4*>(out), ci);
+            reinterpret_cast<int4*>(out), ci, sa);
         GIDS_LAUNCH_CHECK(h);
         if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
         auto kh = h->gather_unroll == 1   ? k_gather_host<int4, 1>
@@ -224,17 +226,17 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
         kh<<<host_grid, BLOCK, 0, st>>>(
             h->host_list, h->list_cnt, h->ins, reinterpret_cast<const int4*>(h->buffer_rows),
             reinterpret_cast<const int4*>(h->backing), reinterpret_cast<int4*>(h->cache_rows),
-            reinterpret_cast<int4*>(out), ci);
+            reinterpret_cast<int4*>(out), ci, sa);
         GIDS_LAUNCH_CHECK(h);
     } else {
         ChunkIdx ci = chunk_idx(dim);
         k_gather_hits<float, 4><<<hit_grid, BLOCK, 0, st>>>(h->hit_list, h->list_cnt, h->line,
-                                                            h->cache_rows, out, ci);
+                                                            h->cache_rows, out, ci, sa);
         GIDS_LAUNCH_CHECK(h);
         if (h->profiling) cudaEventRecord(h->gev[h->parity][1], st);
         k_gather_host<float, 8><<<host_grid, BLOCK, 0, st>>>(h->host_list, h->list_cnt, h->ins,
                                                              h->buffer_rows, h->backing,
-                                                             h->cache_rows, out, ci);
+                                                             h->cache_rows, out, ci, sa);
         GIDS_LAUNCH_CHECK(h);
     }
     if (h->profiling) cudaEventRecord(h->gev[h->parity][2], st);

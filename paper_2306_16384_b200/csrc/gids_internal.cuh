@@ -149,6 +149,15 @@ struct LbTile {
     uint32_t pad;
 };
 
+// per-call arguments of a serve replayed as a CUDA graph (the kernels read
+// them from device memory; NULL = the launch's own arguments)
+struct ServeArgs {
+    const int64_t* uniq;
+    int64_t n;
+    uint64_t epoch;
+    float* out;
+};
+
 struct ServeCounters {
     int64_t tiers[4];      // hits, buffer, storage, bypasses (this batch)
     int64_t n_log;         // insertions logged by the exact policy this batch
@@ -310,7 +319,13 @@ struct gids_handle {
     int32_t my_shard;
     const float** shard_ptrs;  // device array [n_shards]
 
-    // CUDA graphs of the sampling sequence (GIDS_NO_GRAPHS=1 disables)
+    // CUDA graphs of the sampling sequence and of the serve (GIDS_NO_GRAPHS=1
+    // disables): per decision-buffer parity, decisions and rows
+    ServeArgs* sargs;  // device [2]
+    cudaGraphExec_t dgraph[2], ggraph[2];
+    int64_t dgraph_kernels[2], ggraph_kernels[2];
+    int64_t serves;
+    bool graphs_failed;
     bool use_graphs;
     int n_sgraphs;
     SampleGraph sgraphs[GIDS_MAX_SGRAPHS];
@@ -407,7 +422,8 @@ int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, 
 constexpr int64_t GIDS_XP_CAND_CAP = 1 << 17;
 // access classes of a batch against a full cache (k_window_consume -> k_exact_par)
 enum { GIDS_XC_STAY = 0, GIDS_XC_ADD = 1, GIDS_XC_CAND = 2, GIDS_XC_M0 = 3, GIDS_XC_MU = 4 };
-int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st);
+int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st,
+                          const ServeArgs* sa = nullptr);
 int gids_launch_xp_reset(gids_handle* h, cudaStream_t st);
 size_t gids_xp_smem_bytes(int64_t L);
 // cache.cu
@@ -425,7 +441,7 @@ int gids_file_fetch_and_gather(gids_handle* h, int par, float* out, cudaStream_t
 void gids_file_free(gids_handle* h);
 // gather.cu
 int gids_launch_gather(gids_handle* h, const int64_t* unique, int64_t n, float* out,
-                       cudaStream_t st);
+                       cudaStream_t st, const ServeArgs* sa = nullptr);
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 static inline int gids_grid(int64_t work, int block, int max_blocks) {

@@ -91,7 +91,7 @@ class _Queued:
     the sizes, the run-ahead contribution and the host Generator's offset."""
 
     __slots__ = ("seeds", "edges", "unique", "sizes", "event", "batch", "storage_accesses",
-                 "error", "home")
+                 "error")
 
     def __init__(self, seeds, edges, unique, sizes, event):
         self.seeds, self.edges, self.unique, self.sizes, self.event = \
@@ -99,7 +99,6 @@ class _Queued:
         self.batch = None
         self.storage_accesses = None
         self.error = None
-        self.home = None  # raw stream whose pool holds the batch's block
 
     def resolve(self, n_layers: int, rng) -> None:
         if self.batch is not None:
@@ -400,15 +399,33 @@ class Dataloader:
         self._pinned_mask = np.zeros(self.graph.num_nodes, dtype=bool)
         self._pinned_mask[self.buffer.node_ids] = True
 
+    def _empty_on(self, stream, shape, dtype):
+        """torch.empty from `stream`'s allocator pool: the block is written on
+        that stream, so a freed block is reused there only after every stream
+        recorded on it passed its last use (allocating from the caller's pool
+        instead would let the sampler / gather overwrite a block the caller's
+        queued kernels still read).  Raw stream switches: torch.cuda.stream()
+        costs ~20 us of device-index lookups per use."""
+        import torch
+        dev0 = torch._C._cuda_getDevice()
+        prev = torch._C._cuda_getCurrentStream(self.device)
+        torch._C._cuda_setStream(stream_id=stream.stream_id, device_index=stream.device_index,
+                                 device_type=stream.device_type)  # (makes self.device current)
+        try:
+            return torch.empty(shape, dtype=dtype, device=self._torch_dev)
+        finally:
+            torch._C._cuda_setStream(stream_id=prev[0], device_index=prev[1],
+                                     device_type=prev[2])
+            if dev0 != self.device:
+                torch._C._cuda_setDevice(dev0)
+
     def _out_block(self):
         """Output rows of one batch: a block of the workspace bound (a view of
-        the first U rows is returned), from the caller's stream pool -- torch's
-        caching allocator keeps cycling the same pre-warmed blocks (exact-size
-        requests, U varies, made it cudaMalloc fresh segments, stalling
-        next_batch by 10-90 ms); the streams that write it are recorded."""
+        the first U rows is returned), so torch's caching allocator keeps
+        cycling the same pre-warmed blocks (exact-size requests, U varies,
+        made it cudaMalloc fresh segments, stalling next_batch by 10-90 ms)."""
         import torch
-        return torch.empty((self._unique_cap, self.features.dim), dtype=torch.float32,
-                           device=self._torch_dev)
+        return self._empty_on(self._gat, (self._unique_cap, self.features.dim), torch.float32)
 
     def _upload_graph(self, g: GraphCsc):
         """Host GraphCsc -> (indptr int64, indices int32) CUDA tensors."""
@@ -534,11 +551,8 @@ class Dataloader:
         words = None if self._rng_on_device else pcg_words(self._sampler_rng)
         self._h.sample(seeds, words, st)
         self._rng_on_device = True
-        # one allocation for the batch's edges and unique nodes (views of it),
-        # from the caller's stream pool; the sampling stream writes it
-        block = torch.empty(2 * self._edge_cap + self._unique_cap, dtype=torch.int64,
-                            device=self._torch_dev)
-        block.record_stream(self._smp)
+        # one allocation for the batch's edges and unique nodes (views of it)
+        block = self._empty_on(self._smp, 2 * self._edge_cap + self._unique_cap, torch.int64)
         edges = block[:2 * self._edge_cap].view(self._edge_cap, 2)
         unique = block[2 * self._edge_cap:]
         sizes = self._sizes[self._sizes_next]
@@ -546,9 +560,7 @@ class Dataloader:
         self._h.sample_export_async(edges, unique, sizes, st)
         sampled = torch.cuda.Event()
         sampled.record(self._smp)
-        q = _Queued(seeds, edges, unique, sizes, sampled)
-        q.home = torch._C._cuda_getCurrentRawStream(self.device)
-        return q
+        return _Queued(seeds, edges, unique, sizes, sampled)
 
     def _sample_one(self) -> bool:
         """One batch joins the run-ahead queue (dataloader.py:194-205): the next
@@ -632,9 +644,7 @@ class Dataloader:
         batch = entry.batch
         unique = batch.unique_nodes
         n = unique.numel()
-        block = self._out_block()
-        block.record_stream(self._gat)
-        rows = block[:n]
+        rows = self._out_block()[:n]
         unique.record_stream(self._gat)
         unique.record_stream(self._ctl)
         if tr is not None:
@@ -662,13 +672,11 @@ class Dataloader:
         if tr is not None:
             tr.append((t1 - t0, t2 - t1, t3 - t2, time.perf_counter() - t3))
         self.last_counts = c
-        # hand the batch to the caller's stream without blocking the host (the
-        # rows come from its pool; the sampled block too unless the caller
-        # switched streams since)
-        cur = torch._C._cuda_getCurrentRawStream(self.device)
-        self._h.wait_served(cur)
-        if entry.home != cur:
-            unique.record_stream(torch.cuda.current_stream(self.device))
+        # hand the batch to the caller's stream without blocking the host
+        cur = torch.cuda.current_stream(self.device)
+        self._h.wait_served(cur.cuda_stream)
+        rows.record_stream(cur)
+        unique.record_stream(cur)  # (the layers share unique's allocation)
         if self.cfg.verify_gather:
             self._verify(unique, rows)
         stats = self._account(c.sampled, c.cache_hits, c.cpu_buffer_hits, c.storage,

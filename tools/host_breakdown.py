@@ -19,6 +19,7 @@ from paper_2306_16384_b200 import loader as L  # noqa: E402
 wl = sys.argv[1] if len(sys.argv) > 1 else "c1"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 300
 acc = collections.defaultdict(lambda: [0, 0])
+samples = collections.defaultdict(list)
 
 
 def wrap(owner, name, label=None):
@@ -32,7 +33,9 @@ def wrap(owner, name, label=None):
         finally:
             e = acc[key]
             e[0] += 1
-            e[1] += time.perf_counter_ns() - t
+            d = time.perf_counter_ns() - t
+            e[1] += d
+            samples[key].append(d)
     setattr(owner, name, w)
 
 
@@ -55,13 +58,21 @@ for _ in range(40):
     dl.next_batch()
 torch.cuda.synchronize()
 acc.clear()
+samples.clear()
+ms0 = torch.cuda.memory_stats()
 t0 = time.perf_counter()
 for _ in range(steps):
     dl.next_batch()
 torch.cuda.synchronize()
 el = (time.perf_counter() - t0) / steps * 1e6
 print(f"{wl}: {el:.1f} us per next_batch (with wrappers)")
+ms1 = torch.cuda.memory_stats()
+print("allocator:", {k: ms1.get(k, 0) - ms0.get(k, 0) for k in
+                     ("num_device_alloc", "num_device_free", "num_alloc_retries",
+                      "num_sync_all_streams", "allocation.all.allocated")})
 for k, (c, ns) in sorted(acc.items(), key=lambda x: -x[1][1]):
+    sm = sorted(samples[k])
     print(f"  {k:40s} calls/batch {c / steps:5.2f}  us/call {ns / c / 1e3:7.2f}  "
-          f"us/batch {ns / steps / 1e3:7.2f}")
+          f"us/batch {ns / steps / 1e3:7.2f}  median {sm[len(sm) // 2] / 1e3:7.2f}  "
+          f"p90 {sm[int(len(sm) * 0.9)] / 1e3:7.2f}")
 dl.close()
