@@ -168,6 +168,16 @@ GIDS_API int gids_window_pop(gids_handle* h, const int64_t* nodes_dev, int64_t n
 GIDS_API int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
                float* out_dev, void* stream, void* gather_stream);
 
+/* gids_window_pop(pop_dev), gids_window_push(push_dev), gids_serve(...) as
+ * one call (either list may be NULL): the window shift of next_batch
+ * (dataloader.py:232-299 -- the served batch leaves the window, the batch W
+ * ahead joins) runs on `stream` right before the decisions, inside the
+ * serve's launch sequence. */
+GIDS_API int gids_serve_shift(gids_handle* h, const int64_t* unique_dev, int64_t n,
+                              uint64_t epoch, float* out_dev, void* stream, void* gather_stream,
+                              const int64_t* pop_dev, int64_t n_pop, const int64_t* push_dev,
+                              int64_t n_push);
+
 /* Tier counts of the last gids_serve: waits for that call's decisions only
  * (an event recorded on its `stream`), not for work queued after it -- the
  * caller may launch the next batches' sampling before asking. */

@@ -89,6 +89,7 @@ def lib() -> C.CDLL:
         "gids_serve": ([vp, vp, i64, u64, vp, vp, vp], C.c_int),
         "gids_serve_counts": ([vp, C.POINTER(TierCounts)], C.c_int),
         "gids_wait_served": ([vp, vp], C.c_int),
+        "gids_serve_shift": ([vp, vp, i64, u64, vp, vp, vp, vp, i64, vp, i64], C.c_int),
         "gids_serve_decisions": ([vp, vp, vp, vp], C.c_int),
         "gids_cache_stats": ([vp, C.POINTER(CacheCounters)], C.c_int),
         "gids_cache_rng": ([vp, vp], C.c_int),
@@ -151,7 +152,8 @@ def exported_symbols() -> list[str]:
             "gids_contribution_async", "gids_host_register", "gids_host_unregister",
             "gids_exact_par_batches", "gids_exact_par_stats", "gids_owner_split",
             "gids_shared_marks", "gids_shared_final", "gids_shared_unsplit", "gids_shared_tiers",
-            "gids_shared_gather", "gids_cache_rows_ptr", "gids_wait_served"]
+            "gids_shared_gather", "gids_cache_rows_ptr", "gids_wait_served",
+            "gids_serve_shift"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -323,6 +325,15 @@ class Handle:
     def serve(self, unique, epoch: int, out, stream: int, gather_stream: int | None = None) -> None:
         check(lib().gids_serve(self.h, _p(unique), unique.numel(), epoch, _p(out), stream,
                                gather_stream), "serve")
+
+    def serve_shift(self, unique, epoch: int, out, stream: int, gather_stream: int | None,
+                    pop, push) -> None:
+        """window_pop(pop); window_push(push); serve(...) -- one call (None: no list)."""
+        check(lib().gids_serve_shift(
+            self.h, _p(unique), unique.numel(), epoch, _p(out), stream, gather_stream,
+            None if pop is None else _p(pop), 0 if pop is None else pop.numel(),
+            None if push is None else _p(push), 0 if push is None else push.numel()),
+            "serve_shift")
 
     def wait_served(self, stream: int) -> None:
         """`stream` waits (device-side) for the last serve's decisions and gather."""

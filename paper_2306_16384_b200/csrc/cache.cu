@@ -45,6 +45,32 @@ __global__ void k_window(const int64_t* __restrict__ nodes, int64_t n, uint8_t* 
         future[nodes[i]] += (uint8_t)delta;
 }
 
+// a window pop then push in one pass (window.py: the served batch leaves,
+// the batch W ahead joins): byte counts updated with 32-bit atomics on their
+// lane -- a node may be in both lists, and a count never borrows (>= 1 when
+// popped) nor carries (<= 254 when pushed)
+__global__ void k_window_shift(const int64_t* __restrict__ pop, int64_t n_pop,
+                               const int64_t* __restrict__ push, int64_t n_push, uint8_t* future,
+                               const ServeArgs* sa) {
+    if (sa) {
+        pop = sa->pop;
+        n_pop = sa->n_pop;
+        push = sa->push;
+        n_push = sa->n_push;
+    }
+    uint32_t* words = reinterpret_cast<uint32_t*>(future);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pop + n_push;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n_pop) {
+            const int64_t x = pop[i];
+            atomicSub(&words[x >> 2], 1u << ((x & 3) * 8));
+        } else {
+            const int64_t x = push[i - n_pop];
+            atomicAdd(&words[x >> 2], 1u << ((x & 3) * 8));
+        }
+    }
+}
+
 // run-ahead contribution: unpinned and not resident (dataloader.py:188-192)
 __global__ void k_contribution(const int32_t* __restrict__ uniq, SampleCounters* sc,
                                const int32_t* __restrict__ pinned_off,
@@ -1080,12 +1106,16 @@ size_t gids_exact_smem_bytes(int64_t L, bool with_bits) {
     } while (0)
 
 // a serve replayed as a graph reads its per-call arguments from here
-__global__ void k_serve_args(ServeArgs* sa, const int64_t* uniq, int64_t n, uint64_t epoch,
-                             float* out) {
-    sa->uniq = uniq;
-    sa->n = n;
-    sa->epoch = epoch;
-    sa->out = out;
+__global__ void k_serve_args(ServeArgs* sa, ServeArgs v) { *sa = v; }
+
+// the folded window shift launched on its own (no decisions follow in this call)
+static int launch_shift(gids_handle* h, cudaStream_t st) {
+    const int64_t m = h->shift.n_pop + h->shift.n_push;
+    if (m == 0) return GIDS_OK;
+    k_window_shift<<<gids_grid(m, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
+        h->shift.pop, h->shift.n_pop, h->shift.push, h->shift.n_push, h->future, nullptr);
+    GIDS_LAUNCH_CHECK(h);
+    return GIDS_OK;
 }
 
 // the decisions of one batch on `st`: counters, window update + reuse
@@ -1100,6 +1130,12 @@ static int serve_decisions(gids_handle* h, const int64_t* uniq, int64_t n, uint6
     GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
     HT(1);
     int g = gids_grid(n, BLOCK, 8 * GIDS_SMS);
+    if (sa || h->shift.n_pop + h->shift.n_push > 0) {  // the folded window shift
+        const int64_t m = sa ? 2 * h->serve_cap : h->shift.n_pop + h->shift.n_push;
+        k_window_shift<<<gids_grid(m, BLOCK, 8 * GIDS_SMS), BLOCK, 0, st>>>(
+            h->shift.pop, h->shift.n_pop, h->shift.push, h->shift.n_push, h->future, sa);
+        GIDS_LAUNCH_CHECK(h);
+    }
     k_window_consume<<<g, BLOCK, 0, st>>>(uniq, n, h->future, h->reuse, h->slot_of,
                                           h->safe_bits, h->blk_cnt, h->sup_cnt, exact ? 1 : 0,
                                           h->meta, h->ev, 3, nullptr, &h->svc->n_miss0,
@@ -1188,7 +1224,10 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     if (h->gathered_valid[par]) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->gathered[par], 0));
     gids_harvest_gather(h, par);  // batch b-2's gather timing (profiling only)
     gids_mark(h, 2, st);
-    if (h->n_shards > 0) return gids_launch_shard_serve(h, uniq, n, out, st, gst, par);
+    if (h->n_shards > 0) {
+        const int rc = launch_shift(h, st);
+        return rc ? rc : gids_launch_shard_serve(h, uniq, n, out, st, gst, par);
+    }
     HT(0);
     // replay as two graphs (decisions on st, rows on gst) once the first
     // serves have set every function attribute: the ~12 launches of a batch
@@ -1198,7 +1237,9 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
                   gst != cudaStreamLegacy && gst != st;
     if (graphs) {
         ServeArgs* sa = h->sargs + par;
-        k_serve_args<<<1, 1, 0, st>>>(sa, uniq, n, epoch, out);
+        k_serve_args<<<1, 1, 0, st>>>(sa, ServeArgs{uniq, n, epoch, out, h->shift.pop,
+                                                      h->shift.n_pop, h->shift.push,
+                                                      h->shift.n_push});
         GIDS_LAUNCH_CHECK(h);
         if (!h->dgraph[par] &&
             !capture(h, st, &h->dgraph[par], &h->dgraph_kernels[par], [&] {
@@ -1218,6 +1259,8 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
             if (rc2) return rc2;
         }
     } else {
+        const int rc = launch_shift(h, st);
+        if (rc) return rc;
         GIDS_CUDA_TRY(cudaMemsetAsync(h->svc, 0, sizeof(ServeCounters), st));
         GIDS_CUDA_TRY(cudaMemcpyAsync(h->svc_host, h->svc, sizeof(ServeCounters),
                                       cudaMemcpyDeviceToHost, st));

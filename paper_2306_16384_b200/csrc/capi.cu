@@ -228,7 +228,7 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     A(h->blk_cnt, ceil_div(L, 1024));
     A(h->sup_cnt, ceil_div(L, 32768));
     A(h->reuse, N);
-    A(h->future, N);
+    A(h->future, ceil_div(N, 4) * 4);  // (k_window_shift: 32-bit atomics on byte lanes)
     A(h->meta, 1);
     A(h->last_ins, L);
     A(h->bm_front, ceil_div(N, 32));
@@ -503,13 +503,10 @@ int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique
                              int64_t* sizes_host, void* stream) {
     CHECK_H(h);
     cudaStream_t st = (cudaStream_t)stream;
-    if (edges_dev || unique_dev) TRY(gids_launch_export(h, edges_dev, unique_dev, st));
-    if (sizes_host) {
-        // [layer_len[0..L), n_unique, draws, contribution, overflow] (sc->exp)
-        GIDS_CUDA_TRY(cudaMemcpyAsync(sizes_host, h->sc->exp,
-                                      sizeof(int64_t) * (h->cfg.n_layers + 4),
-                                      cudaMemcpyDeviceToHost, st));
-    }
+    // sizes: [layer_len[0..L), n_unique, draws, contribution, overflow] (sc->exp),
+    // stored into the pinned row by the export kernel itself
+    if (edges_dev || unique_dev || sizes_host)
+        TRY(gids_launch_export(h, edges_dev, unique_dev, st, sizes_host));
     return GIDS_OK;
 }
 
@@ -571,6 +568,31 @@ int gids_serve(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t ep
     h->counts_read = false;
     return gids_launch_serve(h, unique_dev, n, epoch, out_dev, (cudaStream_t)stream,
                              gather_stream ? (cudaStream_t)gather_stream : (cudaStream_t)stream);
+}
+
+int gids_serve_shift(gids_handle* h, const int64_t* unique_dev, int64_t n, uint64_t epoch,
+                     float* out_dev, void* stream, void* gather_stream, const int64_t* pop_dev,
+                     int64_t n_pop, const int64_t* push_dev, int64_t n_push) {
+    CHECK_H(h);
+    if (n_pop < 0 || n_push < 0 || n_pop > h->serve_cap || n_push > h->serve_cap ||
+        (n_pop > 0 && !pop_dev) || (n_push > 0 && !push_dev)) {
+        gids_set_error("serve_shift: bad window lists");
+        return GIDS_E_INVALID;
+    }
+    const int32_t lists = h->window_lists - (pop_dev ? 1 : 0);
+    if (pop_dev && h->window_lists <= 0) {
+        gids_set_error("window is empty");
+        return GIDS_E_STATE;
+    }
+    if (push_dev && lists >= 255) {
+        gids_set_error("window holds 255 lists (the per-node lookahead count is 8-bit)");
+        return GIDS_E_CAPACITY;
+    }
+    h->shift = WindowShift{pop_dev, pop_dev ? n_pop : 0, push_dev, push_dev ? n_push : 0};
+    const int rc = gids_serve(h, unique_dev, n, epoch, out_dev, stream, gather_stream);
+    h->shift = WindowShift{nullptr, 0, nullptr, 0};
+    if (rc == GIDS_OK) h->window_lists = lists + (push_dev ? 1 : 0);
+    return rc;
 }
 
 int gids_wait_served(gids_handle* h, void* stream) {

@@ -156,6 +156,18 @@ struct ServeArgs {
     int64_t n;
     uint64_t epoch;
     float* out;
+    const int64_t* pop;  // window shift applied before the decisions
+    int64_t n_pop;
+    const int64_t* push;
+    int64_t n_push;
+};
+
+// a window pop / push folded into the next serve (gids_serve_shift)
+struct WindowShift {
+    const int64_t* pop;
+    int64_t n_pop;
+    const int64_t* push;
+    int64_t n_push;
 };
 
 struct ServeCounters {
@@ -322,6 +334,7 @@ struct gids_handle {
     // CUDA graphs of the sampling sequence and of the serve (GIDS_NO_GRAPHS=1
     // disables): per decision-buffer parity, decisions and rows
     ServeArgs* sargs;  // device [2]
+    WindowShift shift;  // of the serve being launched (zero: none)
     cudaGraphExec_t dgraph[2], ggraph[2];
     int64_t dgraph_kernels[2], ggraph_kernels[2];
     int64_t serves;
@@ -417,7 +430,8 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_word
                        cudaStream_t st);
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
 int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st);
-int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st);
+int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st,
+                       int64_t* sizes_host = nullptr);
 // exact_par.cu
 constexpr int64_t GIDS_XP_CAND_CAP = 1 << 17;
 // access classes of a batch against a full cache (k_window_consume -> k_exact_par)

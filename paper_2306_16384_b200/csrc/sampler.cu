@@ -357,7 +357,9 @@ __global__ void k_rng_set(u128* rng_state, u128 state, u128 inc) {
 // caller buffers, one launch
 __global__ void k_export(const int64_t* __restrict__ src, const SampleCounters* sc, int n_layers,
                          int64_t* __restrict__ dst, const int32_t* __restrict__ uniq,
-                         int64_t* __restrict__ udst) {
+                         int64_t* __restrict__ udst, int64_t* sizes) {
+    if (sizes && blockIdx.x == 0 && threadIdx.x < n_layers + 4)  // (pinned host row)
+        sizes[threadIdx.x] = sc->exp[threadIdx.x];
     int64_t e = 0;
     for (int l = 0; l < n_layers; l++) e += sc->layer_len[l];
     const int64_t ne = dst ? 2 * e : 0, nu = udst ? sc->n_unique : 0;
@@ -536,10 +538,11 @@ int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* w, bool 
     return GIDS_OK;
 }
 
-int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st) {
+int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st,
+                       int64_t* sizes_host) {
     const int64_t bound = 2 * h->edge_cap > h->unique_cap ? 2 * h->edge_cap : h->unique_cap;
     k_export<<<gids_grid(bound, 256, 8 * GIDS_SMS), 256, 0, st>>>(
-        h->edges, h->sc, h->cfg.n_layers, edges_dev, h->unique32, unique_dev);
+        h->edges, h->sc, h->cfg.n_layers, edges_dev, h->unique32, unique_dev, sizes_host);
     GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }

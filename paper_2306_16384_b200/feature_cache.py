@@ -72,6 +72,10 @@ class WindowBuffer:
         self.lists: deque = deque()
         self._h = handle
         self._stream = stream
+        # deferred device updates (the loader folds a pop + push into its
+        # next serve, gids_serve_shift): ("pop" | "push", nodes) in order
+        self.defer = False
+        self._ops: list = []
 
     def _st(self) -> int:
         return self._stream if self._stream is not None else _native.stream_ptr(self._h.device)
@@ -96,15 +100,46 @@ class WindowBuffer:
             raise CacheProtocolError("iteration list must be ascending and unique")
         self.lists.append(nodes)
         if self._h is not None:
-            self._h.window_push(nodes, self._st())
+            if self.defer:
+                self._ops.append(("push", nodes))
+            else:
+                self._h.window_push(nodes, self._st())
 
     def pop_iteration(self):
         if not self.lists:
             raise CacheProtocolError("window is empty")
         nodes = self.lists.popleft()
         if self._h is not None:
-            self._h.window_pop(nodes, self._st())
+            if self.defer:
+                self._ops.append(("pop", nodes))
+            else:
+                self._h.window_pop(nodes, self._st())
         return nodes
+
+    def flush(self) -> None:
+        """Launch the deferred device updates, in order."""
+        ops, self._ops = self._ops, []
+        for op, nodes in ops:
+            if op == "push":
+                self._h.window_push(nodes, self._st())
+            else:
+                self._h.window_pop(nodes, self._st())
+
+    def take_shift(self):
+        """(pop, push) lists for gids_serve_shift when the deferred updates are
+        at most one pop then at most one push; otherwise they are launched
+        now and (None, None) is returned."""
+        ops = self._ops
+        if not ops:
+            return None, None
+        if len(ops) == 1:
+            self._ops = []
+            return (ops[0][1], None) if ops[0][0] == "pop" else (None, ops[0][1])
+        if len(ops) == 2 and ops[0][0] == "pop" and ops[1][0] == "push":
+            self._ops = []
+            return ops[0][1], ops[1][1]
+        self.flush()
+        return None, None
 
 
 class GpuCacheView:

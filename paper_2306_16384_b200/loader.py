@@ -228,6 +228,7 @@ class Dataloader:
         self._last_contrib = None
         self.cache = GpuCacheView(self._h, self.spec.page_bytes)
         self.window = WindowBuffer(cfg.window_depth, self._h, self._ctl.cuda_stream)
+        self.window.defer = True  # (folded into the next serve: gids_serve_shift)
         self.shared = None
         if shared:
             # the handle's window counters serve the owner role (owned parts of
@@ -652,8 +653,9 @@ class Dataloader:
         if self._last_contrib is not None:  # admissions read the cache this serve changes
             self._ctl.wait_event(self._last_contrib)
             self._last_contrib = None
-        self._h.serve(unique, self._iteration, rows, self._ctl.cuda_stream,
-                      self._gat.cuda_stream)
+        pop, push = self.window.take_shift()
+        self._h.serve_shift(unique, self._iteration, rows, self._ctl.cuda_stream,
+                            self._gat.cuda_stream, pop, push)
         decided = torch.cuda.Event(enable_timing=tr is not None)
         decided.record(self._ctl)
         self._last_decided = decided
