@@ -141,7 +141,8 @@ GIDS_API int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* un
  * its unpinned, non-resident nodes -- against the cache as `stream` reaches
  * the call: n is read through n_ptr (device-visible, e.g. the pinned sizes
  * row of gids_sample_export_async), the count lands in out_host (pinned).
- * Lets a caller sample ahead of the point where the reference samples. */
+ * Lets a caller sample ahead of the point where the reference samples.
+ * Calls on one handle are serialised on one stream (they share a scratch). */
 GIDS_API int gids_contribution_async(gids_handle* h, const int64_t* unique_dev,
                                      const int64_t* n_ptr, int64_t* out_host, void* stream);
 /* Device-resident sampler stream state (synchronises; for tests). */

@@ -87,11 +87,17 @@ __global__ void k_contribution(const int32_t* __restrict__ uniq, SampleCounters*
 }
 
 // the same count for an exported batch, at the moment it joins the run-ahead
-// queue: n read through a device-visible pointer (pinned host is fine)
+// queue: n read once per block through a device-visible pointer (pinned host
+// is fine); the last block to finish stores the total into the pinned result
+// and leaves the scratch zeroed -- one launch, no memset or copy around it
 __global__ void k_contribution64(const int64_t* __restrict__ uniq, const int64_t* n_ptr,
                                  const int32_t* __restrict__ pinned_off,
-                                 const int32_t* __restrict__ slot_of, unsigned long long* out) {
-    const int64_t n = *n_ptr;
+                                 const int32_t* __restrict__ slot_of,
+                                 unsigned long long* scratch, int64_t* out_host) {
+    __shared__ int64_t s_n;
+    if (threadIdx.x == 0) s_n = *n_ptr;
+    __syncthreads();
+    const int64_t n = s_n;
     int64_t c = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -99,7 +105,16 @@ __global__ void k_contribution64(const int64_t* __restrict__ uniq, const int64_t
         c += (pinned_off[x] < 0 && slot_of[x] < 0) ? 1 : 0;
     }
     c = warp_sum64(c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&scratch[0], (unsigned long long)c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&scratch[1], 1ull) == gridDim.x - 1) {  // every block's sum is in
+            __threadfence();
+            *out_host = (int64_t)atomicExch(&scratch[0], 0ull);
+            scratch[1] = 0;
+        }
+    }
 }
 
 // window_update + reuse consumption; ev[p] = (line_at_start+1)<<1 | (count_after>0)
@@ -1408,12 +1423,12 @@ extern "C" int gids_contribution_async(gids_handle* h, const int64_t* unique_dev
     GIDS_CUDA_TRY(cudaSetDevice(h->device));
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(h->contrib_dev);
-    GIDS_CUDA_TRY(cudaMemsetAsync(scratch, 0, sizeof(int64_t), st));
-    if (h->n_shards == 0) {  // a sharded table keeps every row resident: 0
-        k_contribution64<<<gids_grid(h->unique_cap, BLOCK, 4 * GIDS_SMS), BLOCK, 0, st>>>(
-            unique_dev, n_ptr, h->pinned_off, h->slot_of, scratch);
-        GIDS_LAUNCH_CHECK(h);
+    if (h->n_shards > 0) {  // a sharded table keeps every row resident: 0
+        GIDS_CUDA_TRY(cudaMemsetAsync(out_host, 0, sizeof(int64_t), st));
+        return GIDS_OK;
     }
-    GIDS_CUDA_TRY(cudaMemcpyAsync(out_host, scratch, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    k_contribution64<<<gids_grid(h->unique_cap, BLOCK, 4 * GIDS_SMS), BLOCK, 0, st>>>(
+        unique_dev, n_ptr, h->pinned_off, h->slot_of, scratch, out_host);
+    GIDS_LAUNCH_CHECK(h);
     return GIDS_OK;
 }

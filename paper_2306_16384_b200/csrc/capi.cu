@@ -126,6 +126,15 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
         int blocks = (wps * GIDS_SMS + 7) / 8;
         h->gather_blocks = blocks;
         h->gather_unroll = 2;
+        // hit gather: 2 blocks per SM with 8 loads in flight per lane keep HBM
+        // saturated while leaving each SM room for the other streams' kernels
+        // (4 blocks of 256 threads filled every SM for the whole gather, so the
+        // next batch's contribution / sampling / decisions waited behind it)
+        int hbps = 2;
+        if (const char* e = getenv("GIDS_HIT_BPS")) hbps = atoi(e);
+        h->hit_blocks = (hbps < 1 ? 1 : hbps > 8 ? 8 : hbps) * GIDS_SMS;
+        h->hit_unroll = 8;
+        if (const char* e = getenv("GIDS_HIT_UNROLL")) h->hit_unroll = atoi(e) >= 8 ? 8 : 4;
         const char* ng = getenv("GIDS_NO_GRAPHS");
         h->use_graphs = !(ng && ng[0] == '1');
         if (const char* e = getenv("GIDS_GATHER_UNROLL")) {
@@ -244,7 +253,9 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
     h->lb_tiles = ceil_div(ceil_div(N, 32), 256);
     A(h->sc, 1 + ceil_div((int64_t)sizeof(LbTile) * (cfg->n_layers + 1) * h->lb_tiles,
                           (int64_t)sizeof(SampleCounters)));
-    A(h->contrib_dev, 1);
+    A(h->contrib_dev, 2);
+    if (!rc) rc = cudaMemset(h->contrib_dev, 0, 2 * sizeof(int64_t)) == cudaSuccess ? GIDS_OK
+                                                                                 : GIDS_E_CUDA;
     h->scan_parts_cap = 1024;
     A(h->scan_parts, 2 * h->scan_parts_cap);
     A(h->word_parts, h->scan_parts_cap);

@@ -194,11 +194,11 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
     // host rows: grid sized by GIDS_GATHER_WPS (capi.cu) -- a few warps per SM
     // with 8 loads in flight per lane saturate the host link and leave the
     // rest of the GPU to the next batch's sampling and cache decisions
-    const int hit_grid = gids_grid(n, WARPS, 4 * GIDS_SMS);
+    const int hit_grid = gids_grid(n, WARPS, h->hit_blocks);
     const int host_grid = gids_grid(n, WARPS, h->gather_blocks);
     if (h->ft) {  // file-backed storage tier: hits, then pages -> HBM staging -> rows
         if ((dim & 3) == 0) {
-            k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(
+            (h->hit_unroll == 8 ? k_gather_hits<int4, 8> : k_gather_hits<int4, 4>)<<<hit_grid, BLOCK, 0, st>>>(
                 h->hit_list, h->list_cnt, h->line, reinterpret_cast<const int4*>(h->cache_rows),
                 reinterpret_cast<int4*>(out), chunk_idx(dim >> 2), sa);
         } else {
@@ -214,7 +214,7 @@ int gids_launch_gather(gids_handle* h, const int64_t* uniq, int64_t n, float* ou
     }
     if ((dim & 3) == 0) {
         ChunkIdx ci = chunk_idx(dim >> 2);
-        k_gather_hits<int4, 4><<<hit_grid, BLOCK, 0, st>>>(
+        (h->hit_unroll == 8 ? k_gather_hits<int4, 8> : k_gather_hits<int4, 4>)<<<hit_grid, BLOCK, 0, st>>>(
             h->hit_list, h->list_cnt, h->line, reinterpret_cast<const int4*>(h->cache_rows),
             reinterpret_cast<int4*>(out), ci, sa);
         GIDS_LAUNCH_CHECK(h);

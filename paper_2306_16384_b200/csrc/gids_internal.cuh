@@ -273,7 +273,7 @@ struct gids_handle {
     uint64_t jump_inc_hi, jump_inc_lo;
     bool jump_valid;
     SampleCounters* sc;    // device
-    int64_t* contrib_dev;  // device scratch of gids_contribution_async
+    int64_t* contrib_dev;  // [2] scratch of gids_contribution_async (sum, blocks done; left 0)
     SampleCounters* sc_host;  // pinned mirror
     int64_t scan_parts_cap;
     int64_t* scan_parts;   // [scan_parts_cap * 2]
@@ -323,6 +323,8 @@ struct gids_handle {
     bool exact_smem;       // exact-policy tables fit in shared memory
     int gather_blocks;     // gather grid (resident blocks of 8 warps)
     int gather_unroll;     // 16-B loads in flight per lane in the host gather (1,2,4,8)
+    int hit_blocks;        // hit-gather grid (GIDS_HIT_BPS blocks of 8 warps per SM)
+    int hit_unroll;        // 16-B loads in flight per lane in the hit gather (4, 8)
 
     // HBM-sharded feature table: node v lives in
     // shard v % n_shards at row v / n_shards; shard pointers may be peer

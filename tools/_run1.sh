@@ -1,4 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
-timeout 1200 python -m pytest tests/test_gpu_sampler.py tests/test_gpu_loader.py tests/test_gpu_cache_api.py tests/test_gpu_fuzz.py -x -q 2>&1 | tail -4
-timeout 600 python tools/host_breakdown.py c1 400 2>&1 | tail -24
-timeout 600 python bench.py --workload c1 --steps 100 --warmup 40 --no-cpu-baseline > gpurun_out/bench_c1_shift.json 2>&1; tail -c 300 gpurun_out/bench_c1_shift.json
+for b in 1 2 3 4; do for u in 4 8; do
+GIDS_HIT_BPS=$b GIDS_HIT_UNROLL=$u timeout 600 python bench.py --workload c1 --steps 200 --warmup 40 --no-cpu-baseline > gpurun_out/c1_hit_${b}_${u}.json 2>&1
+python -c "
+import json;d=json.load(open('gpurun_out/c1_hit_${b}_${u}.json'));print('bps $b unroll $u', round(d['value'],1), round(d['e2e']['value'],1), {k: round(v,4) for k,v in d['phase_ms_per_step'].items()}, round(d['roofline']['achieved'],1))"
+done; done

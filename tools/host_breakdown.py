@@ -50,6 +50,29 @@ wrap(torch.cuda.Event, "record", "Event.record")
 wrap(torch.cuda.Stream, "wait_event", "Stream.wait_event")
 wrap(torch.cuda, "current_stream", "torch.cuda.current_stream")
 
+ready = collections.Counter()
+_so = L.Dataloader._sample_one
+
+
+def _sample_one_probe(self):
+    if self._spec:
+        ready["spec sampled ready at admission"] += bool(self._spec[0].event.query())
+        ready["spec admissions"] += 1
+    return _so(self)
+
+
+L.Dataloader._sample_one = _sample_one_probe
+_rs = L._Queued.resolve
+
+
+def _resolve_probe(self, *a):
+    if self.batch is None:
+        ready["contribution ready at resolve"] += bool(self.event.query())
+        ready["resolves"] += 1
+    return _rs(self, *a)
+
+
+L._Queued.resolve = _resolve_probe
 cfg = make_config({**bench.WORKLOADS[wl], "gids_policy": bench.DEFAULT_POLICY[wl]})
 dl = Dataloader(cfg)
 for n in ("push_iteration", "pop_iteration"):
@@ -59,6 +82,7 @@ for _ in range(40):
 torch.cuda.synchronize()
 acc.clear()
 samples.clear()
+ready.clear()
 ms0 = torch.cuda.memory_stats()
 t0 = time.perf_counter()
 for _ in range(steps):
@@ -75,4 +99,15 @@ for k, (c, ns) in sorted(acc.items(), key=lambda x: -x[1][1]):
     print(f"  {k:40s} calls/batch {c / steps:5.2f}  us/call {ns / c / 1e3:7.2f}  "
           f"us/batch {ns / steps / 1e3:7.2f}  median {sm[len(sm) // 2] / 1e3:7.2f}  "
           f"p90 {sm[int(len(sm) * 0.9)] / 1e3:7.2f}")
+print("event readiness:", dict(ready))
+torch.cuda.synchronize()
+for label, shape in (("out block", (dl._unique_cap, dl.features.dim)), ("4 MB", (1024, 1024))):
+    ts = []
+    for _ in range(50):
+        t = time.perf_counter_ns()
+        b = dl._empty_on(dl._gat, shape, torch.float32)
+        ts.append(time.perf_counter_ns() - t)
+        del b
+    ts.sort()
+    print(f"_empty_on({label}) idle: median {ts[25] / 1e3:.2f} us")
 dl.close()
