@@ -85,20 +85,45 @@ class RunSummary:
     total_time_us: float
 
 
+class _Slots:
+    """Equal blocks handed out K at a time from one allocation: each is a
+    view, and the allocation returns to torch's pool (after the streams
+    recorded on it) when the last of its views is gone."""
+
+    __slots__ = ("_alloc", "_k", "_big", "_next")
+
+    def __init__(self, alloc, k: int):
+        self._alloc, self._k, self._big, self._next = alloc, k, None, k
+
+    def take(self):
+        if self._next == self._k:
+            self._big, self._next = self._alloc(), 0
+        v = self._big[self._next]
+        self._next += 1
+        return v
+
+
 class _Queued:
     """A sampled batch whose outputs may still be in flight on the control
     stream; ``resolve()`` waits for them (normally long finished) and fixes
     the sizes, the run-ahead contribution and the host Generator's offset."""
 
-    __slots__ = ("seeds", "edges", "unique", "sizes", "event", "batch", "storage_accesses",
-                 "error")
+    __slots__ = ("seeds", "block", "ecap", "sizes", "sizes_ptr", "event", "batch",
+                 "storage_accesses", "error", "counted_at")
 
-    def __init__(self, seeds, edges, unique, sizes, event):
-        self.seeds, self.edges, self.unique, self.sizes, self.event = \
-            seeds, edges, unique, sizes, event
+    def __init__(self, seeds, block, ecap, sizes, sizes_ptr, event):
+        # block: int64 [2 ecap edges | unique nodes] (workspace bounds);
+        # sizes: its pinned sizes row (numpy view) at host address sizes_ptr
+        self.seeds, self.block, self.ecap, self.sizes, self.sizes_ptr, self.event = \
+            seeds, block, ecap, sizes, sizes_ptr, event
         self.batch = None
         self.storage_accesses = None
         self.error = None
+        self.counted_at = -1  # serves before its contribution was counted (-1: not yet)
+
+    @property
+    def unique_ptr(self) -> int:
+        return self.block.data_ptr() + 16 * self.ecap
 
     def resolve(self, n_layers: int, rng) -> None:
         if self.batch is not None:
@@ -110,14 +135,14 @@ class _Queued:
                                                     sz[n_layers + 3])
         if overflow:
             raise _native.GidsError("sampler workspace bound exceeded")
-        layers, off = [], 0
+        layers, off, b = [], 0, self.block
         for ln in lens:
-            layers.append(self.edges[off:off + ln])
+            layers.append(b[2 * off:2 * (off + ln)].view(ln, 2))
             off += ln
         if draws:
             rng.bit_generator.advance(draws)
         self.batch = MiniBatch(seeds=self.seeds, layers=layers,
-                               unique_nodes=self.unique[:n_unique])
+                               unique_nodes=b[2 * self.ecap:2 * self.ecap + n_unique])
         self.storage_accesses = contrib
 
 
@@ -258,18 +283,30 @@ class Dataloader:
         self._ringed = 0
         self._rng_on_device = False
         self._edge_cap, self._unique_cap = self._h.sample_capacity()
-        # pre-warm the gather stream's allocator pool with the blocks a
-        # pipelined caller keeps live (its batch, the one being gathered,
-        # the next one, and one freed but not yet retired)
-        warm = [self._out_block() for _ in range(4)]
+        # per-batch blocks come K at a time from one allocation (a torch
+        # allocation costs ~15 us of host time in the serving loop): output
+        # rows from the gather stream's pool, sampled edges + unique nodes
+        # from the sampling stream's
+        row_block = self._unique_cap * self.features.dim * 4
+        k_out = max(1, min(4, (2 << 30) // max(1, row_block)))
+        self._out_slots = _Slots(lambda: self._empty_on(
+            self._gat, (k_out, self._unique_cap, self.features.dim), torch.float32), k_out)
+        self._smp_slots = _Slots(lambda: self._empty_on(
+            self._smp, (8, 2 * self._edge_cap + self._unique_cap), torch.int64), 8)
+        # pre-warm the gather pool with the blocks a pipelined caller keeps
+        # live (its batch, the one being gathered, the next one, and one freed
+        # but not yet retired)
+        warm = [self._out_slots._alloc() for _ in range(2 if k_out > 1 else 4)]
         del warm
         ring = cfg.runahead_cap + cfg.gids_speculate + 4
         self._sizes = torch.zeros((ring, len(cfg.fanouts) + 5), dtype=torch.int64,
                                   pin_memory=True)
         self._sizes_np = self._sizes.numpy()
+        self._sizes_ptr = self._sizes.data_ptr()
         self._sizes_next = 0
 
         self._iteration = 0
+        self._serves = 0  # serves launched (contributions are counted between two)
         # host-time trace of next_batch (diagnostics): run-ahead, output
         # allocation, serve launch, wait for the decisions -- seconds per call
         self._trace = [] if os.environ.get("GIDS_TRACE_HOST") == "1" else None
@@ -423,10 +460,10 @@ class Dataloader:
     def _out_block(self):
         """Output rows of one batch: a block of the workspace bound (a view of
         the first U rows is returned), so torch's caching allocator keeps
-        cycling the same pre-warmed blocks (exact-size requests, U varies,
-        made it cudaMalloc fresh segments, stalling next_batch by 10-90 ms)."""
-        import torch
-        return self._empty_on(self._gat, (self._unique_cap, self.features.dim), torch.float32)
+        cycling the same pre-warmed allocations (exact-size requests, U
+        varies, made it cudaMalloc fresh segments, stalling next_batch by
+        10-90 ms)."""
+        return self._out_slots.take()
 
     def _upload_graph(self, g: GraphCsc):
         """Host GraphCsc -> (indptr int64, indices int32) CUDA tensors."""
@@ -545,23 +582,24 @@ class Dataloader:
         try:
             seeds = check_seeds(seeds, self.graph.num_nodes)
         except ValueError as e:
-            q = _Queued(seeds, None, None, None, None)
+            q = _Queued(seeds, None, 0, None, 0, None)
             q.error = e
             return q
         st = self._smp.cuda_stream
         words = None if self._rng_on_device else pcg_words(self._sampler_rng)
         self._h.sample(seeds, words, st)
         self._rng_on_device = True
-        # one allocation for the batch's edges and unique nodes (views of it)
-        block = self._empty_on(self._smp, 2 * self._edge_cap + self._unique_cap, torch.int64)
-        edges = block[:2 * self._edge_cap].view(self._edge_cap, 2)
-        unique = block[2 * self._edge_cap:]
-        sizes = self._sizes[self._sizes_next]
-        self._sizes_next = (self._sizes_next + 1) % len(self._sizes)
-        self._h.sample_export_async(edges, unique, sizes, st)
+        # one block for the batch's edges and unique nodes (views of it, made
+        # when the batch resolves), its sizes in a pinned row
+        block = self._smp_slots.take()
+        i = self._sizes_next
+        self._sizes_next = (i + 1) % self._sizes_np.shape[0]
+        ptr = self._sizes_ptr + i * self._sizes_np.strides[0]
+        b0 = block.data_ptr()
+        self._h.sample_export_async(b0, b0 + 16 * self._edge_cap, ptr, st)
         sampled = torch.cuda.Event()
         sampled.record(self._smp)
-        return _Queued(seeds, edges, unique, sizes, sampled)
+        return _Queued(seeds, block, self._edge_cap, self._sizes_np[i], ptr, sampled)
 
     def _sample_one(self) -> bool:
         """One batch joins the run-ahead queue (dataloader.py:194-205): the next
@@ -574,19 +612,37 @@ class Dataloader:
             return False
         if q.error is not None:
             raise q.error
+        if q.counted_at != self._serves:  # (else counted already, against this same cache)
+            self._count(q)
+        self._pending.append(q)
+        return True
+
+    def _count(self, q: _Queued) -> None:
+        """q's run-ahead contribution against the cache as the last serve left
+        it (the control stream's decisions), on the count stream."""
+        import torch
         L = len(self.cfg.fanouts)
-        row = q.sizes.data_ptr()
+        row = q.sizes_ptr
         cnt = self._cnt
         cnt.wait_event(q.event)  # the batch's sampling and size export
         if self._last_decided is not None:
             cnt.wait_event(self._last_decided)  # the cache as of the last serve
-        q.unique.record_stream(cnt)
-        self._h.contribution_async(q.unique, row + 8 * L, row + 8 * (L + 2), cnt.cuda_stream)
+        q.block.record_stream(cnt)
+        self._h.contribution_async(q.unique_ptr, row + 8 * L, row + 8 * (L + 2),
+                                   cnt.cuda_stream)
         q.event = torch.cuda.Event()
         q.event.record(cnt)
-        self._last_contrib = q.event
-        self._pending.append(q)
-        return True
+        q.counted_at = self._serves
+        self._last_contrib = q.event  # (the next serve waits for these reads)
+
+    def _precount(self) -> None:
+        """Count the batch the next call admits now: the cache stays as this
+        serve leaves it until the next serve, so the count is the one its
+        admission would make -- and the host does not wait for it there (a
+        serve in between, i.e. a call admitting nothing, makes it recount)."""
+        if self._spec and self._spec[0].error is None and \
+                self._spec[0].counted_at != self._serves:
+            self._count(self._spec[0])
 
     def _speculate(self) -> None:
         """Sample up to gids_speculate batches beyond the run-ahead queue, so
@@ -656,6 +712,7 @@ class Dataloader:
         pop, push = self.window.take_shift()
         self._h.serve_shift(unique, self._iteration, rows, self._ctl.cuda_stream,
                             self._gat.cuda_stream, pop, push)
+        self._serves += 1
         decided = torch.cuda.Event(enable_timing=tr is not None)
         decided.record(self._ctl)
         self._last_decided = decided
@@ -668,6 +725,7 @@ class Dataloader:
         # host accounts and returns (the sampled content is fixed by the seed
         # order and the sampler stream, not by when it is drawn)
         self._speculate()
+        self._precount()
         if tr is not None:
             t3 = time.perf_counter()
         c = self._h.serve_counts()  # waits for the decisions only, not the gather

@@ -35,8 +35,8 @@ def check_seeds(seeds, num_nodes: int) -> np.ndarray:
     s = np.asarray(seeds, dtype=np.int64)
     if len(s) == 0:
         raise ValueError("seeds must be non-empty")
-    out = (s < 0) | (s >= num_nodes)
-    if out.any():
+    if s.min() < 0 or s.max() >= num_nodes:
+        out = (s < 0) | (s >= num_nodes)
         raise ValueError(f"seed node {int(s[out][0])} out of range (num_nodes={num_nodes})")
     return s
 

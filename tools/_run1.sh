@@ -1,6 +1,8 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
-for b in 1 2 3 4; do for u in 4 8; do
-GIDS_HIT_BPS=$b GIDS_HIT_UNROLL=$u timeout 600 python bench.py --workload c1 --steps 200 --warmup 40 --no-cpu-baseline > gpurun_out/c1_hit_${b}_${u}.json 2>&1
+timeout 1200 python -m pytest tests/test_gpu_loader.py tests/test_gpu_sampler.py tests/test_gpu_multirank.py tests/test_gpu_shared_cache.py -x -q 2>&1 | tail -3
+timeout 600 python tools/host_breakdown.py c1 400 2>&1 | tail -28
+for i in 1 2; do
+timeout 600 python bench.py --workload c1 --steps 200 --warmup 40 --no-cpu-baseline > gpurun_out/bench_c1_slots$i.json 2>&1
 python -c "
-import json;d=json.load(open('gpurun_out/c1_hit_${b}_${u}.json'));print('bps $b unroll $u', round(d['value'],1), round(d['e2e']['value'],1), {k: round(v,4) for k,v in d['phase_ms_per_step'].items()}, round(d['roofline']['achieved'],1))"
-done; done
+import json;d=json.load(open('gpurun_out/bench_c1_slots$i.json'));print(round(d['value'],1), round(d['e2e']['value'],1), d['tier_roofline']['frac'], d['e2e_host_ms_per_call']['median'])"
+done
