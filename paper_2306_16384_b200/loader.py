@@ -19,6 +19,7 @@ the reference orders its numpy result.
 """
 from __future__ import annotations
 
+import functools
 import itertools
 import math
 import os
@@ -83,6 +84,26 @@ class RunSummary:
     total_fetch_us: float
     total_train_us: float
     total_time_us: float
+
+
+def _empty_on(device: int, torch_dev, stream, shape, dtype):
+    """torch.empty from `stream`'s allocator pool: the block is written on
+    that stream, so a freed block is reused there only after every stream
+    recorded on it passed its last use (allocating from the caller's pool
+    instead would let the sampler / gather overwrite a block the caller's
+    queued kernels still read).  Raw stream switches: torch.cuda.stream()
+    costs ~20 us of device-index lookups per use."""
+    import torch
+    dev0 = torch._C._cuda_getDevice()
+    prev = torch._C._cuda_getCurrentStream(device)
+    torch._C._cuda_setStream(stream_id=stream.stream_id, device_index=stream.device_index,
+                             device_type=stream.device_type)  # (makes `device` current)
+    try:
+        return torch.empty(shape, dtype=dtype, device=torch_dev)
+    finally:
+        torch._C._cuda_setStream(stream_id=prev[0], device_index=prev[1], device_type=prev[2])
+        if dev0 != device:
+            torch._C._cuda_setDevice(dev0)
 
 
 class _Slots:
@@ -289,10 +310,14 @@ class Dataloader:
         # from the sampling stream's
         row_block = self._unique_cap * self.features.dim * 4
         k_out = max(1, min(4, (2 << 30) // max(1, row_block)))
-        self._out_slots = _Slots(lambda: self._empty_on(
-            self._gat, (k_out, self._unique_cap, self.features.dim), torch.float32), k_out)
-        self._smp_slots = _Slots(lambda: self._empty_on(
-            self._smp, (8, 2 * self._edge_cap + self._unique_cap), torch.int64), 8)
+        # (functools.partial over plain values: no reference back to the
+        # loader, which must die -- and unmap its host tiers -- when dropped)
+        self._out_slots = _Slots(functools.partial(
+            _empty_on, self.device, self._torch_dev, self._gat,
+            (k_out, self._unique_cap, self.features.dim), torch.float32), k_out)
+        self._smp_slots = _Slots(functools.partial(
+            _empty_on, self.device, self._torch_dev, self._smp,
+            (8, 2 * self._edge_cap + self._unique_cap), torch.int64), 8)
         # pre-warm the gather pool with the blocks a pipelined caller keeps
         # live (its batch, the one being gathered, the next one, and one freed
         # but not yet retired)
@@ -438,24 +463,7 @@ class Dataloader:
         self._pinned_mask[self.buffer.node_ids] = True
 
     def _empty_on(self, stream, shape, dtype):
-        """torch.empty from `stream`'s allocator pool: the block is written on
-        that stream, so a freed block is reused there only after every stream
-        recorded on it passed its last use (allocating from the caller's pool
-        instead would let the sampler / gather overwrite a block the caller's
-        queued kernels still read).  Raw stream switches: torch.cuda.stream()
-        costs ~20 us of device-index lookups per use."""
-        import torch
-        dev0 = torch._C._cuda_getDevice()
-        prev = torch._C._cuda_getCurrentStream(self.device)
-        torch._C._cuda_setStream(stream_id=stream.stream_id, device_index=stream.device_index,
-                                 device_type=stream.device_type)  # (makes self.device current)
-        try:
-            return torch.empty(shape, dtype=dtype, device=self._torch_dev)
-        finally:
-            torch._C._cuda_setStream(stream_id=prev[0], device_index=prev[1],
-                                     device_type=prev[2])
-            if dev0 != self.device:
-                torch._C._cuda_setDevice(dev0)
+        return _empty_on(self.device, self._torch_dev, stream, shape, dtype)
 
     def _out_block(self):
         """Output rows of one batch: a block of the workspace bound (a view of
