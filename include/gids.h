@@ -314,6 +314,9 @@ GIDS_API int gids_phase_times(gids_handle* h, double out_ms[5]);
 
 /* Kernel launches issued by this handle since creation (evidence counter). */
 GIDS_API int64_t gids_launch_count(gids_handle* h);
+/* Serves replayed as CUDA graphs (decisions + rows) since creation (evidence
+ * counter; GIDS_NO_GRAPHS=1 launches every kernel directly instead). */
+GIDS_API int64_t gids_serve_graph_replays(gids_handle* h);
 
 /* Served batches whose exact-policy decisions were made by the CTA-parallel
  * kernel for a full cache (csrc/exact_par.cu) rather than the sequential warp,

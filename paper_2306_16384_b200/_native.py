@@ -98,6 +98,7 @@ def lib() -> C.CDLL:
         "gids_synthesize_rows": ([i32, u64, i64, i64, i32, vp, vp], C.c_int),
         "gids_verify_rows": ([i32, u64, vp, i64, i32, vp, vp, vp], C.c_int),
         "gids_launch_count": ([vp], i64),
+        "gids_serve_graph_replays": ([vp], i64),
         "gids_exact_par_batches": ([vp], i64),
         "gids_exact_par_stats": ([vp, vp], C.c_int),
         "gids_generate_uniform_graph": ([i32, i64, i64, u64, vp, vp, vp], C.c_int),
@@ -153,7 +154,7 @@ def exported_symbols() -> list[str]:
             "gids_exact_par_batches", "gids_exact_par_stats", "gids_owner_split",
             "gids_shared_marks", "gids_shared_final", "gids_shared_unsplit", "gids_shared_tiers",
             "gids_shared_gather", "gids_cache_rows_ptr", "gids_wait_served",
-            "gids_serve_shift"]
+            "gids_serve_shift", "gids_serve_graph_replays"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -426,6 +427,10 @@ class Handle:
 
     def launch_count(self) -> int:
         return int(lib().gids_launch_count(self.h))
+
+    def graphs_replayed(self) -> int:
+        """Serves replayed as CUDA graphs (evidence counter)."""
+        return int(lib().gids_serve_graph_replays(self.h))
 
     def exact_par_batches(self) -> int:
         return int(lib().gids_exact_par_batches(self.h))

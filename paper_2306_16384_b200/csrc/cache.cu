@@ -1265,6 +1265,7 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     if (graphs) {
         GIDS_CUDA_TRY(cudaGraphLaunch(h->dgraph[par], st));
         h->launches += h->dgraph_kernels[par];
+        h->serve_replays++;
     } else if (n > 0) {
         int rc = serve_decisions(h, uniq, n, epoch, st, nullptr, _ht);
         if (rc) return rc;

@@ -757,6 +757,8 @@ int gids_host_unregister(void* ptr) {
 }
 
 int64_t gids_cache_capacity(gids_handle* h) { return h ? h->L : -1; }
+int64_t gids_serve_graph_replays(gids_handle* h) { return h ? h->serve_replays : 0; }
+
 int64_t gids_launch_count(gids_handle* h) { return h ? h->launches : -1; }
 int64_t gids_exact_par_batches(gids_handle* h) { return h ? h->xp_batches : -1; }
 int gids_exact_par_stats(gids_handle* h, int64_t out[12]) {

@@ -340,6 +340,7 @@ struct gids_handle {
     cudaGraphExec_t dgraph[2], ggraph[2];
     int64_t dgraph_kernels[2], ggraph_kernels[2];
     int64_t serves;
+    int64_t serve_replays;
     bool graphs_failed;
     bool use_graphs;
     int n_sgraphs;

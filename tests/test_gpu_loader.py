@@ -260,3 +260,51 @@ def test_gpu_exact_policy_large_caches_match_oracle(lines, nodes, batch):
     assert np.array_equal(node, onode) and np.array_equal(state, ostate)
     assert dl.cache.eviction_rng_words().tolist() == ld.cache.rng_words().tolist()
     dl.close()
+
+
+@pytest.mark.parametrize("name", ["c2small", "locality_w8"])
+def test_gpu_loader_direct_launches_match_reference_run(name, monkeypatch):
+    """GIDS_NO_GRAPHS=1: the sampling sequence and the serve launched kernel by
+    kernel instead of replayed as CUDA graphs -- the same bits."""
+    monkeypatch.setenv("GIDS_NO_GRAPHS", "1")
+    fx = fixture(name)
+    dl = Dataloader(config_of(fx))
+    try:
+        for b in range(int(fx["n_batches"])):
+            mb, rows, st = dl.next_batch()
+            assert np.array_equal(mb.unique_nodes.cpu().numpy(), fx[f"b{b}_unique"]), b
+            assert sha(rows.cpu().numpy()) == str(fx[f"b{b}_rows_sha"]), b
+            assert st.csv_row() == str(fx["csv"][b]), b
+        assert not dl._h.graphs_replayed()
+    finally:
+        dl.close()
+
+
+def test_gpu_loader_serve_graphs_replayed():
+    """The default path replays the serve as graphs from the third batch on."""
+    fx = fixture("c2small")
+    dl = Dataloader(config_of(fx))
+    try:
+        for b in range(int(fx["n_batches"])):
+            mb, rows, st = dl.next_batch()
+            assert sha(rows.cpu().numpy()) == str(fx[f"b{b}_rows_sha"]), b
+        assert dl._h.graphs_replayed() == int(fx["n_batches"]) - 2  # (the first two direct)
+    finally:
+        dl.close()
+
+
+def test_gpu_loader_is_freed_without_the_cycle_collector():
+    """Dropping a loader frees it at once (its host tiers are unmapped then):
+    nothing it owns refers back to it."""
+    import gc
+    import weakref
+    gc.disable()
+    try:
+        dl = Dataloader(config_of(fixture("c09")))
+        dl.next_batch()
+        dl.close()
+        ref = weakref.ref(dl)
+        del dl
+        assert ref() is None
+    finally:
+        gc.enable()
