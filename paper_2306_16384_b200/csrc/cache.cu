@@ -1199,6 +1199,17 @@ static int serve_decisions(gids_handle* h, const int64_t* uniq, int64_t n, uint6
     return GIDS_OK;
 }
 
+void gids_drop_serve_graphs(gids_handle* h) {
+    if (!h->dgraph[0] && !h->dgraph[1] && !h->ggraph[0] && !h->ggraph[1]) return;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();  // (no launch of them still in flight)
+    for (int i = 0; i < 2; i++) {
+        if (h->dgraph[i]) cudaGraphExecDestroy(h->dgraph[i]);
+        if (h->ggraph[i]) cudaGraphExecDestroy(h->ggraph[i]);
+        h->dgraph[i] = h->ggraph[i] = nullptr;
+    }
+}
+
 // one capture of `st`'s work into *exec (kernel count into *kernels); false
 // (capture abandoned, the direct launches are used) on any failure
 template <typename F>

@@ -414,6 +414,7 @@ int gids_load_graph_device(gids_handle* h, const int64_t* indptr, const int32_t*
 
 int gids_set_backing(gids_handle* h, const float* table, int64_t n_rows) {
     CHECK_H(h);
+    gids_drop_serve_graphs(h);
     if (n_rows != h->N) {
         gids_set_error("feature table and graph disagree on node count");
         return GIDS_E_INVALID;
@@ -427,6 +428,7 @@ int gids_set_backing(gids_handle* h, const float* table, int64_t n_rows) {
 int gids_set_constant_buffer(gids_handle* h, const int64_t* node_ids, int64_t k,
                              const float* rows) {
     CHECK_H(h);
+    gids_drop_serve_graphs(h);
     if (h->buffer_registered) cudaHostUnregister(const_cast<float*>(h->buffer_rows));
     h->buffer_registered = false;
     std::vector<int32_t> off((size_t)h->N, -1);

@@ -444,6 +444,9 @@ int gids_launch_exact_par(gids_handle* h, int64_t n, cudaStream_t st,
 int gids_launch_xp_reset(gids_handle* h, cudaStream_t st);
 size_t gids_xp_smem_bytes(int64_t L);
 // cache.cu
+// the serve graphs bake the handle's table pointers in: dropped (and captured
+// again) whenever a setter changes one
+void gids_drop_serve_graphs(gids_handle* h);
 int gids_launch_serve(gids_handle* h, const int64_t* unique, int64_t n, uint64_t epoch,
                       float* out, cudaStream_t st, cudaStream_t gst);
 int gids_launch_window(gids_handle* h, const int64_t* nodes, int64_t n, int delta,

@@ -221,6 +221,7 @@ int gids_ipc_close(int device, void* dev_ptr) {
 
 int gids_set_sharded_table(gids_handle* h, const uint64_t* shard_ptrs, int32_t n_shards,
                            int32_t my_shard) {
+    if (h) gids_drop_serve_graphs(h);
     if (!h || !shard_ptrs || n_shards < 1 || my_shard < 0 || my_shard >= n_shards) {
         gids_set_error("set_sharded_table: need 1 <= n_shards and 0 <= my_shard < n_shards");
         return GIDS_E_INVALID;

@@ -279,6 +279,7 @@ extern "C" {
 
 int gids_set_storage_file(gids_handle* h, const char* path, int64_t offset, int32_t page_bytes,
                           int64_t max_pages, int32_t io_threads, int32_t direct) {
+    if (h) gids_drop_serve_graphs(h);
     if (!h || !path || offset < 0 || page_bytes < 16 || io_threads < 1) {
         gids_set_error("set_storage_file: need a path, offset >= 0, page_bytes >= 16, threads >= 1");
         return GIDS_E_INVALID;
