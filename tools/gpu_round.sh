@@ -18,7 +18,13 @@ export BENCH_PROFILE_STEADY=1
 timeout 1500 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
     --csv --log-file gpurun_out/c4_launches_steady.csv python bench.py --steps 6 --warmup 6 \
     --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none \
+    --csv --log-file gpurun_out/c1_launches_steady.csv python bench.py --workload c1 --steps 20 \
+    --warmup 40 --no-cpu-baseline > /dev/null 2>&1
 unset BENCH_PROFILE_STEADY
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gather_hits -s 60 -c 1 \
+    -o gpurun_out/prof_c1_gather_hits python bench.py --workload c1 --steps 5 --warmup 40 \
+    --no-cpu-baseline > /dev/null 2>&1
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_gather_host -s 12 -c 1 \
     -o gpurun_out/prof_c4_gather_host python bench.py --steps 5 --warmup 10 \
     --no-cpu-baseline > /dev/null 2>&1
