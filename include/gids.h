@@ -136,13 +136,21 @@ GIDS_API int gids_sample_export(gids_handle* h, int64_t* edges_dev, int64_t* uni
  * gids_contribution_async, ordered against the serving stream. */
 GIDS_API int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev,
                                       int64_t* sizes_host, void* stream);
+/* gids_sample + gids_sample_export_async in one call (the serving loop's
+ * per-batch sampling launch); seeds from pinned host memory copy without a
+ * host stall. */
+GIDS_API int gids_sample_async(gids_handle* h, const int64_t* seeds, int64_t n_seeds,
+                               const uint64_t* rng, void* stream, int64_t* edges_dev,
+                               int64_t* unique_dev, int64_t* sizes_host);
 GIDS_API int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* unique_cap);
 /* Run-ahead contribution (dataloader.py:188-192) of an exported batch --
  * its unpinned, non-resident nodes -- against the cache as `stream` reaches
  * the call: n is read through n_ptr (device-visible, e.g. the pinned sizes
  * row of gids_sample_export_async), the count lands in out_host (pinned).
  * Lets a caller sample ahead of the point where the reference samples.
- * Calls on one handle are serialised on one stream (they share a scratch). */
+ * Ordered on the device after the last gids_serve's decisions, and the next
+ * gids_serve waits for it.  Calls on one handle are serialised on one stream
+ * (they share a scratch). */
 GIDS_API int gids_contribution_async(gids_handle* h, const int64_t* unique_dev,
                                      const int64_t* n_ptr, int64_t* out_host, void* stream);
 /* Device-resident sampler stream state (synchronises; for tests). */

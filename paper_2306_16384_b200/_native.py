@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
         "gids_sample_export": ([vp, vp, vp, vp], C.c_int),
         "gids_sample_export_async": ([vp, vp, vp, vp, vp], C.c_int),
         "gids_sample_capacity": ([vp, vp, vp], C.c_int),
+        "gids_sample_async": ([vp, vp, i64, vp, vp, vp, vp, vp], C.c_int),
         "gids_sampler_rng": ([vp, vp], C.c_int),
         "gids_window_push": ([vp, vp, i64, vp], C.c_int),
         "gids_window_pop": ([vp, vp, i64, vp], C.c_int),
@@ -154,7 +155,7 @@ def exported_symbols() -> list[str]:
             "gids_exact_par_batches", "gids_exact_par_stats", "gids_owner_split",
             "gids_shared_marks", "gids_shared_final", "gids_shared_unsplit", "gids_shared_tiers",
             "gids_shared_gather", "gids_cache_rows_ptr", "gids_wait_served",
-            "gids_serve_shift", "gids_serve_graph_replays"]
+            "gids_serve_shift", "gids_serve_graph_replays", "gids_sample_async"]
 
 
 def check(rc: int, what: str = "") -> None:
@@ -277,6 +278,14 @@ class Handle:
         w = None if words is None else np.ascontiguousarray(words, dtype=np.uint64)
         check(lib().gids_sample(self.h, s.ctypes.data, len(s),
                                 None if w is None else w.ctypes.data, stream), "sample")
+
+    def sample_async(self, seeds: np.ndarray, words, stream: int, edges_ptr: int,
+                     unique_ptr: int, sizes_ptr: int) -> None:
+        """sample() then sample_export_async() in one call; seeds: contiguous
+        int64 (pinned: the copy does not stall the host)."""
+        check(lib().gids_sample_async(self.h, seeds.ctypes.data, len(seeds),
+                                      None if words is None else words.ctypes.data, stream,
+                                      edges_ptr, unique_ptr, sizes_ptr), "sample_async")
 
     def sample_frontier(self, frontier: np.ndarray, words, stream: int) -> None:
         """One layer over an explicit frontier, in order, repeats included."""

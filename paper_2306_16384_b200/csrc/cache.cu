@@ -1248,6 +1248,10 @@ int gids_launch_serve(gids_handle* h, const int64_t* uniq, int64_t n, uint64_t e
     h->host_list = h->host_list_buf[par];
     h->list_cnt = h->list_cnt_buf[par];
     if (h->gathered_valid[par]) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->gathered[par], 0));
+    if (h->contributed_valid) {  // admissions counted against the cache this serve changes
+        GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->contributed, 0));
+        h->contributed_valid = false;
+    }
     gids_harvest_gather(h, par);  // batch b-2's gather timing (profiling only)
     gids_mark(h, 2, st);
     if (h->n_shards > 0) {
@@ -1439,8 +1443,13 @@ extern "C" int gids_contribution_async(gids_handle* h, const int64_t* unique_dev
         GIDS_CUDA_TRY(cudaMemsetAsync(out_host, 0, sizeof(int64_t), st));
         return GIDS_OK;
     }
+    // against the cache as the last serve's decisions leave it; the next serve
+    // waits for these reads (both orderings on the device, no host events)
+    if (h->counted_valid) GIDS_CUDA_TRY(cudaStreamWaitEvent(st, h->counted, 0));
     k_contribution64<<<gids_grid(h->unique_cap, BLOCK, 4 * GIDS_SMS), BLOCK, 0, st>>>(
         unique_dev, n_ptr, h->pinned_off, h->slot_of, scratch, out_host);
     GIDS_LAUNCH_CHECK(h);
+    GIDS_CUDA_TRY(cudaEventRecord(h->contributed, st));
+    h->contributed_valid = true;
     return GIDS_OK;
 }

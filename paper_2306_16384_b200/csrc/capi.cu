@@ -147,6 +147,7 @@ static int init_handle(gids_handle* h, const uint64_t* eviction_rng) {
         for (int j = 0; j < 3; j++) GIDS_CUDA_TRY(cudaEventCreate(&h->gev[i][j]));
     }
     GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->decided, cudaEventDisableTiming));
+    GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->contributed, cudaEventDisableTiming));
     GIDS_CUDA_TRY(cudaEventCreateWithFlags(&h->counted, cudaEventDisableTiming));
     h->kind = h->kind_buf[0];
     h->line = h->line_buf[0];
@@ -341,6 +342,7 @@ int gids_destroy(gids_handle* h) {
     }
     if (h->decided) cudaEventDestroy(h->decided);
     if (h->counted) cudaEventDestroy(h->counted);
+    if (h->contributed) cudaEventDestroy(h->contributed);
     if (h->sc_host) cudaFreeHost(h->sc_host);
     if (h->jump_host) cudaFreeHost(h->jump_host);
     if (h->rng_host) cudaFreeHost(h->rng_host);
@@ -521,6 +523,12 @@ int gids_sample_export_async(gids_handle* h, int64_t* edges_dev, int64_t* unique
     if (edges_dev || unique_dev || sizes_host)
         TRY(gids_launch_export(h, edges_dev, unique_dev, st, sizes_host));
     return GIDS_OK;
+}
+
+int gids_sample_async(gids_handle* h, const int64_t* seeds, int64_t n_seeds, const uint64_t* rng,
+                      void* stream, int64_t* edges_dev, int64_t* unique_dev, int64_t* sizes_host) {
+    TRY(gids_sample(h, seeds, n_seeds, rng, stream));
+    return gids_sample_export_async(h, edges_dev, unique_dev, sizes_host, stream);
 }
 
 int gids_sample_capacity(gids_handle* h, int64_t* edge_cap, int64_t* unique_cap) {

@@ -208,6 +208,8 @@ struct gids_handle {
     cudaStream_t last_stream;
     cudaEvent_t counted = nullptr;  // the last serve's tier counts are in svc_host
     bool counted_valid = false;
+    cudaEvent_t contributed = nullptr;  // the last gids_contribution_async's reads done
+    bool contributed_valid = false;
 
     // graph (HBM)
     int64_t* indptr;       // [N+1]

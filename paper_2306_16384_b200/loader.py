@@ -270,8 +270,6 @@ class Dataloader:
         # decisions run on ctl (the decisions need a batch only after the
         # host resolved it, i.e. after its sampling finished)
         self._smp = torch.cuda.Stream(self.device, priority=0 if gather_first else -1)
-        self._last_decided = None
-        self._last_contrib = None
         self.cache = GpuCacheView(self._h, self.spec.page_bytes)
         self.window = WindowBuffer(cfg.window_depth, self._h, self._ctl.cuda_stream)
         self.window.defer = True  # (folded into the next serve: gids_serve_shift)
@@ -293,6 +291,7 @@ class Dataloader:
         else:
             self._sampler_rng = np.random.default_rng(sampler_ss)
         self._batches = _seed_stream(cfg, self.graph.num_nodes, work_ss, shuffle_ss)
+        self._seeds_trusted = True  # (int64 ids in [0, N) by construction)
         self._exhausted = False
         self._seeds_done = False
         self._pending: deque[_Queued] = deque()
@@ -328,6 +327,9 @@ class Dataloader:
                                   pin_memory=True)
         self._sizes_np = self._sizes.numpy()
         self._sizes_ptr = self._sizes.data_ptr()
+        self._seed_stage = torch.empty((ring, cfg.batch_size), dtype=torch.int64,
+                                       pin_memory=True).numpy()
+        self._cur_streams: dict = {}  # raw caller stream -> torch Stream (record_stream)
         self._sizes_next = 0
 
         self._iteration = 0
@@ -587,24 +589,26 @@ class Dataloader:
         except StopIteration:
             self._seeds_done = True
             return None
-        try:
-            seeds = check_seeds(seeds, self.graph.num_nodes)
+        try:  # (_seed_stream draws ids in [0, N): checked once, at construction)
+            seeds = seeds if self._seeds_trusted else check_seeds(seeds, self.graph.num_nodes)
         except ValueError as e:
             q = _Queued(seeds, None, 0, None, 0, None)
             q.error = e
             return q
         st = self._smp.cuda_stream
         words = None if self._rng_on_device else pcg_words(self._sampler_rng)
-        self._h.sample(seeds, words, st)
         self._rng_on_device = True
         # one block for the batch's edges and unique nodes (views of it, made
-        # when the batch resolves), its sizes in a pinned row
+        # when the batch resolves); its seeds and sizes in pinned ring rows (a
+        # row is reused only after its batch resolved, i.e. its stream work ran)
         block = self._smp_slots.take()
         i = self._sizes_next
         self._sizes_next = (i + 1) % self._sizes_np.shape[0]
         ptr = self._sizes_ptr + i * self._sizes_np.strides[0]
+        staged = self._seed_stage[i, :len(seeds)]
+        staged[:] = seeds
         b0 = block.data_ptr()
-        self._h.sample_export_async(b0, b0 + 16 * self._edge_cap, ptr, st)
+        self._h.sample_async(staged, words, st, b0, b0 + 16 * self._edge_cap, ptr)
         sampled = torch.cuda.Event()
         sampled.record(self._smp)
         return _Queued(seeds, block, self._edge_cap, self._sizes_np[i], ptr, sampled)
@@ -633,15 +637,14 @@ class Dataloader:
         row = q.sizes_ptr
         cnt = self._cnt
         cnt.wait_event(q.event)  # the batch's sampling and size export
-        if self._last_decided is not None:
-            cnt.wait_event(self._last_decided)  # the cache as of the last serve
+        # (the handle orders the count after the last serve's decisions and the
+        # next serve after the count, on the device)
         q.block.record_stream(cnt)
         self._h.contribution_async(q.unique_ptr, row + 8 * L, row + 8 * (L + 2),
                                    cnt.cuda_stream)
         q.event = torch.cuda.Event()
         q.event.record(cnt)
         q.counted_at = self._serves
-        self._last_contrib = q.event  # (the next serve waits for these reads)
 
     def _precount(self) -> None:
         """Count the batch the next call admits now: the cache stays as this
@@ -714,17 +717,13 @@ class Dataloader:
         unique.record_stream(self._ctl)
         if tr is not None:
             t2 = time.perf_counter()
-        if self._last_contrib is not None:  # admissions read the cache this serve changes
-            self._ctl.wait_event(self._last_contrib)
-            self._last_contrib = None
         pop, push = self.window.take_shift()
         self._h.serve_shift(unique, self._iteration, rows, self._ctl.cuda_stream,
                             self._gat.cuda_stream, pop, push)
         self._serves += 1
-        decided = torch.cuda.Event(enable_timing=tr is not None)
-        decided.record(self._ctl)
-        self._last_decided = decided
         if tr is not None:  # device timeline per batch: decisions done, rows done
+            decided = torch.cuda.Event(enable_timing=True)
+            decided.record(self._ctl)
             gathered = torch.cuda.Event(enable_timing=True)
             gathered.record(self._gat)
             self._timeline.append((decided, gathered))
@@ -741,7 +740,11 @@ class Dataloader:
             tr.append((t1 - t0, t2 - t1, t3 - t2, time.perf_counter() - t3))
         self.last_counts = c
         # hand the batch to the caller's stream without blocking the host
-        cur = torch.cuda.current_stream(self.device)
+        sid = torch._C._cuda_getCurrentStream(self.device)
+        cur = self._cur_streams.get(sid)
+        if cur is None:
+            cur = self._cur_streams.setdefault(sid, torch.cuda.Stream(
+                stream_id=sid[0], device_index=sid[1], device_type=sid[2]))
         self._h.wait_served(cur.cuda_stream)
         rows.record_stream(cur)
         unique.record_stream(cur)  # (the layers share unique's allocation)

@@ -42,13 +42,19 @@ def wrap(owner, name, label=None):
 for n in ("next_batch", "run_ahead", "_sample_one", "_launch_sample", "_speculate", "_resolve",
           "_out_block", "_account", "_storage_at_least"):
     wrap(L.Dataloader, n)
-for n in ("sample", "sample_export_async", "contribution_async", "window_push", "window_pop",
-          "serve", "serve_counts"):
+for n in ("sample", "sample_export_async", "sample_async", "contribution_async", "window_push",
+          "window_pop", "serve", "serve_shift", "serve_counts", "wait_served"):
     wrap(_native.Handle, n)
+wrap(L._Slots, "take")
+wrap(L, "check_seeds", "check_seeds")
+wrap(L, "pcg_words", "pcg_words")
+wrap(L, "MiniBatch", "MiniBatch()")
 wrap(L._Queued, "resolve")
 wrap(torch.cuda.Event, "record", "Event.record")
 wrap(torch.cuda.Stream, "wait_event", "Stream.wait_event")
 wrap(torch.cuda, "current_stream", "torch.cuda.current_stream")
+wrap(torch.cuda.Event, "synchronize", "Event.synchronize")
+wrap(torch.cuda, "Event", "Event()")
 
 ready = collections.Counter()
 _so = L.Dataloader._sample_one
