@@ -759,6 +759,7 @@ class Dataloader:
         """One global step of the owner-sharded cache (shared_cache.py): this
         rank's batch, decided by the owners of its nodes, gathered from the
         owners' lines and this rank's host tiers.  Collective over the ranks."""
+        import torch
         sh = self.shared
         G, r = sh.G, self.cfg.gids_dp_rank
         st = _native.stream_ptr(self.device)
@@ -780,6 +781,8 @@ class Dataloader:
         batch = entry.batch
         unique = batch.unique_nodes
         n = unique.numel()
+        # the owner decisions change residency the admissions' counts read
+        torch.cuda.current_stream(self.device).wait_stream(self._cnt)
         dec, tiers = sh.serve_step(self._iteration, unique, st)
         rows = self._out_block()[:n]
         sh.gather(unique, dec, rows, st)
