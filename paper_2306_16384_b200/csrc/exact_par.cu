@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[7] = 0;   // unconverted candidates of the round
             x.MISC[8] = XT;  // end by a Lemire rejection
             x.MISC[9] = XT;  // end by a full change list
+            x.MISC[14] = XT;  // first candidate whose line the previous round took (min)
         }
         int32_t ni, pdr, psel, pchg;
         bool sel, dr, chg;
@@ -870,42 +871,38 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 }
                 if (moved) x.MISC[10] = 1;
             }
+            // ---------------- F (with the check, one barrier): a candidate whose
+            // line an earlier eviction took -- each access checks its own answer
+            // of this pass (MISC[1], redone by a further pass) and of the previous
+            // round (MISC[14], once) against the round's few candidates
+            if (sel && in) {
+                const int32_t cl = cand_lane(x, cur);
+                if (cl > t) atomicMin(&x.MISC[1], cl);
+            }
+            if (pass == 0) {
+                const int32_t mine_prev = x.PANS[t];
+                if (mine_prev >= 0) {
+                    const int32_t cl = cand_lane(x, mine_prev);
+                    if (cl >= 0) atomicMin(&x.MISC[14], cl);
+                }
+            }
             __syncthreads();
             for (int32_t b = mlo; b <= mhi; b++) x.MOVM[b] = 0ull;  // (read above, all done)
             mhi = -1;
             if (!x.MISC[10]) break;
+            if (t == 0) x.MISC[1] = XT;  // (read only after the last pass's barrier)
             if (chg && in && cls == C_MU) x.CSLOT[pchg] = cur;  // next pass
         }
+        const int32_t pans = (sel && in) ? cur : -1;  // this thread's answer, for the next round's F
+        const int lost = x.MISC[1] < x.MISC[14] ? x.MISC[1] : x.MISC[14];
+        const int E = Epre < lost ? Epre : lost;
         if (t == 0) {
             tn = clock64();
-            prof[8] += tn - tc;
-            tc = tn;
-        }
-        // ---------------- F: a candidate whose line an earlier eviction took
-        // (each access checks its own answer of this and the previous round
-        // against the round's few candidates)
-        int32_t pans = -1;  // this thread's answer, for the next round's F
-        {
-            const int32_t my = (sel && in) ? cur : -1, mine_prev = x.PANS[t];
-            pans = my;
-            if (my >= 0) {
-                const int32_t cl = cand_lane(x, my);
-                if (cl > t) atomicMin(&x.MISC[1], cl);
-            }
-            if (mine_prev >= 0) {
-                const int32_t cl = cand_lane(x, mine_prev);
-                if (cl >= 0) atomicMin(&x.MISC[1], cl);
-            }
-        }
-        __syncthreads();
-        const int E = Epre < x.MISC[1] ? Epre : x.MISC[1];
-        if (t == 0) {
-            tn = clock64();
-            prof[6] += tn - tc;  // F
+            prof[8] += tn - tc;  // check + F
             tc = tn;
             st_rounds++;
             if (E < n - pos && E < XT) {
-                if (E == x.MISC[1]) st_conv++;
+                if (E == lost) st_conv++;
                 else if (E == x.MISC[8]) st_rej++;
                 else if (E == x.MISC[9]) st_chg++;
             }

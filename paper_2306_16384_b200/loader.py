@@ -314,9 +314,11 @@ class Dataloader:
         self._out_slots = _Slots(functools.partial(
             _empty_on, self.device, self._torch_dev, self._gat,
             (k_out, self._unique_cap, self.features.dim), torch.float32), k_out)
+        smp_block = (2 * self._edge_cap + self._unique_cap) * 8
+        k_smp = max(1, min(8, (256 << 20) // max(1, smp_block)))
         self._smp_slots = _Slots(functools.partial(
             _empty_on, self.device, self._torch_dev, self._smp,
-            (8, 2 * self._edge_cap + self._unique_cap), torch.int64), 8)
+            (k_smp, 2 * self._edge_cap + self._unique_cap), torch.int64), k_smp)
         # pre-warm the gather pool with the blocks a pipelined caller keeps
         # live (its batch, the one being gathered, the next one, and one freed
         # but not yet retired)

@@ -1,7 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
-GIDS_NO_GRAPHS=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gather_hits -s 60 -c 1 \
-    -o gpurun_out/prof_c1_gather_hits python bench.py --workload c1 --steps 5 --warmup 40 \
-    --no-cpu-baseline > gpurun_out/ncu_c1.log 2>&1
-tail -3 gpurun_out/ncu_c1.log
-ls -la gpurun_out/*.ncu-rep
-timeout 1500 python tools/run_reference_tests.py > gpurun_out/reftests.txt 2>&1; tail -5 gpurun_out/reftests.txt
+timeout 1500 python -m pytest tests/test_gpu_exact_par.py tests/test_gpu_fuzz.py tests/test_gpu_loader.py -q -x 2>&1 | tail -3
+timeout 1200 python bench.py --steps 10 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c4_vf.json 2>&1
+python -c "
+import json;d=json.load(open('gpurun_out/bench_c4_vf.json'));print(round(d['value'],2), round(d['e2e']['value'],2), d['decision_kernel']['ms_per_batch'])"
+timeout 1500 python -m pytest tests/test_gpu_fullsize.py -q -x 2>&1 | tail -3
