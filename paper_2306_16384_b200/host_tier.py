@@ -68,6 +68,7 @@ class SharedRegion:
         _barrier()  # everyone attached
         if creator:
             self.region.unlink()
+        _barrier()  # the name is gone for every rank when this returns
         self.array = self.region.array(shape, dtype) if nbytes else np.empty(shape, dtype)
 
     def close(self) -> None:
