@@ -537,10 +537,10 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     long long tc = clock64();
 
     while (pos < n) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(RING_LAG));
-        __syncthreads();
+        // (the ring entries this round reads were waited for before the last
+        // round's closing barrier, which also ordered its commit)
         long long tn = clock64();
-        prof[10] += tn - tc;  // (ring wait + refill: with G)
+        prof[10] += tn - tc;  // (refill issue)
         tc = tn;
         // ---------------- A: classify, saturating safe-count prefix, draw prefix
         const int32_t p = pos + t;
@@ -952,10 +952,14 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[5] = pdr + (dr ? 1 + extra : 0);  // halves consumed through it
             x.MISC[6] = psel + (sel ? 1 : 0);        // log entries through it
         }
+        // the next round's staged entries have landed (the groups issued before
+        // this round's refill, RING_LAG - 1 of them still in flight: as with a
+        // wait of RING_LAG after it), for every thread after the barrier
+        asm volatile("cp.async.wait_group %0;" ::"n"(RING_LAG - 1));
         __syncthreads();
         if (t == 0) {
             tn = clock64();
-            prof[9] += tn - tc;  // G commit
+            prof[9] += tn - tc;  // G commit (+ ring wait)
             tc = tn;
         }
         if (E > 0) {
