@@ -280,6 +280,27 @@ def cpu_baseline_sample(cfg, dl, seconds: float = 12.0) -> dict:
                       f"policy={cfg.gids_policy}, same graph and rows as the GPU run"}
 
 
+def _gc_probe(stop=None):
+    """Durations (ms) of the Python cyclic collector's passes: a list filled
+    by a gc callback until _gc_probe(stop=that list) removes it."""
+    import gc
+    if stop is not None:
+        for cb in list(gc.callbacks):
+            if getattr(cb, "_gids_probe", None) is stop:
+                gc.callbacks.remove(cb)
+        return stop
+    out, t = [], [0.0]
+
+    def cb(phase, info):
+        if phase == "start":
+            t[0] = time.perf_counter()
+        else:
+            out.append((time.perf_counter() - t[0]) * 1e3)
+    cb._gids_probe = out
+    gc.callbacks.append(cb)
+    return out
+
+
 def _timeline(dl):
     """GIDS_TRACE_HOST=1: (decisions done, rows done) per batch of the last
     timed steps, ms after the first batch's decisions (device clock)."""
@@ -470,6 +491,7 @@ def main() -> None:
     t0 = time.perf_counter()
     start.record()
     call_ms = []  # host time per next_batch call (diagnostic: outliers in the e2e pass)
+    gc_ms = _gc_probe()  # Python collector pauses inside the timed steps (diagnostic)
     tr0 = len(dl._trace) if dl._trace is not None else 0
     for _ in range(args.steps):
         th = time.perf_counter()
@@ -482,6 +504,7 @@ def main() -> None:
     end.record()
     torch.cuda.synchronize(local)
     wall = time.perf_counter() - t0
+    _gc_probe(stop=gc_ms)
     trace1 = dl._trace[tr0:] if dl._trace is not None else None
     timeline1 = _timeline(dl)  # (pass 1's last batches)
     if steady_profile:
@@ -648,6 +671,8 @@ def main() -> None:
         "numa": numa,
         "e2e_host_trace_slowest_s": (sorted(trace1, key=sum)[-3:] if trace1 else None),
         "e2e_timeline_ms": timeline1,
+        "gc_pauses_ms": {"count": len(gc_ms), "max": max(gc_ms) if gc_ms else 0.0,
+                         "total": sum(gc_ms)},
         "e2e_host_ms_per_call": {"min": float(np.min(call_ms)), "median": float(np.median(call_ms)),
                                  "p90": float(np.percentile(call_ms, 90)),
                                  "max": float(np.max(call_ms)),

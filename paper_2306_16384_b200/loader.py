@@ -323,6 +323,10 @@ class Dataloader:
         # live (its batch, the one being gathered, the next one, and one freed
         # but not yet retired)
         warm = [self._out_slots._alloc() for _ in range(2 if k_out > 1 else 4)]
+        # ... and the sampling pool with the groups a steady run-ahead window
+        # keeps live (a cudaMalloc inside the loop stalled a C4 step by 40-90 ms)
+        warm += [self._smp_slots._alloc() for _ in
+                 range(-(-(cfg.window_depth + cfg.gids_speculate + 8) // k_smp))]
         del warm
         ring = cfg.runahead_cap + cfg.gids_speculate + 4
         self._sizes = torch.zeros((ring, len(cfg.fanouts) + 5), dtype=torch.int64,
@@ -724,6 +728,7 @@ class Dataloader:
                             self._gat.cuda_stream, pop, push)
         self._serves += 1
         if tr is not None:  # device timeline per batch: decisions done, rows done
+            t2s = time.perf_counter()
             decided = torch.cuda.Event(enable_timing=True)
             decided.record(self._ctl)
             gathered = torch.cuda.Event(enable_timing=True)
@@ -734,12 +739,17 @@ class Dataloader:
         # host accounts and returns (the sampled content is fixed by the seed
         # order and the sampler stream, not by when it is drawn)
         self._speculate()
+        if tr is not None:
+            t2p = time.perf_counter()
         self._precount()
         if tr is not None:
             t3 = time.perf_counter()
         c = self._h.serve_counts()  # waits for the decisions only, not the gather
         if tr is not None:
-            tr.append((t1 - t0, t2 - t1, t3 - t2, time.perf_counter() - t3))
+            # run-ahead, output block, serve + speculate + precount, counts wait;
+            # then the serve / speculate parts of the third
+            tr.append((t1 - t0, t2 - t1, t3 - t2, time.perf_counter() - t3, t2s - t2,
+                       t2p - t2s))
         self.last_counts = c
         # hand the batch to the caller's stream without blocking the host
         sid = torch._C._cuda_getCurrentStream(self.device)
