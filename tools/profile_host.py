@@ -44,7 +44,8 @@ for _ in range(steps):
 torch.cuda.synchronize()
 print(f"{wl}: {(time.perf_counter() - t0) / steps * 1e3:.3f} ms per next_batch (no profiler), "
       f"{calls['sample']} sample launches, {len(dl._pending)} pending, {len(dl._spec)} speculated")
-if dl._trace is not None:  # GIDS_TRACE_HOST=1: run_ahead / out block / serve / counts wait
+if dl._trace is not None:  # GIDS_TRACE_HOST=1: run_ahead / out block / serve+speculate+precount /
+    # counts wait / serve alone / speculate alone
     import numpy as np
     tr = np.array(dl._trace[tr0:]) * 1e3
     print("trace ms median:", np.round(np.median(tr, axis=0), 4), "p90:",
