@@ -418,6 +418,24 @@ __device__ __forceinline__ uint32_t get_half(const Xs& x, const XpArgs& a, int32
     return half_direct(a.meta, k);
 }
 
+// numpy's Generator.integers(n) (Lemire, buffered 32-bit halves) from stream
+// position k: r in [0, n), `extra` halves consumed beyond the first
+__device__ __forceinline__ void lemire(const Xs& x, const XpArgs& a, int32_t k, int32_t kfill,
+                                       uint32_t n, uint32_t& r, int& extra) {
+    extra = 0;
+    uint64_t m = (uint64_t)get_half(x, a, k, kfill) * n;
+    uint32_t left = (uint32_t)m;
+    if (left < n) {
+        const uint32_t thr = (0u - n) % n;
+        while (left < thr) {
+            extra++;
+            m = (uint64_t)get_half(x, a, k + extra, kfill) * n;
+            left = (uint32_t)m;
+        }
+    }
+    r = (uint32_t)(m >> 32);
+}
+
 // (d, c): x -> max(x + d, c); (d2, c2) becomes "(d1, c1) first, then (d2, c2)"
 __device__ __forceinline__ void sat_compose(int32_t d1, int32_t c1, int32_t& d2, int32_t& c2) {
     const int32_t c = max(c1 + d2, c2);
@@ -563,7 +581,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[1] = XT;  // first candidate that lost its line (min)
             x.MISC[3] = 0;   // set changes in the round
             x.MISC[7] = 0;   // unconverted candidates of the round
-            x.MISC[8] = XT;  // end by a Lemire rejection
+            x.MISC[8] = XT;  // first Lemire rejection (+1)
+            x.MISC[15] = 0;  // Lemire rejections in the round
             x.MISC[9] = XT;  // end by a full change list
             x.MISC[14] = XT;  // first candidate whose line the previous round took (min)
         }
@@ -680,21 +699,11 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         uint32_t r = 0;
         int extra = 0;
         if (dr) {
-            const int32_t k = kpos + pdr;
-            uint64_t m = (uint64_t)get_half(x, a, k, kfill) * (uint32_t)ni;
-            uint32_t left = (uint32_t)m;
-            if (left < (uint32_t)ni) {
-                const uint32_t thr = (0u - (uint32_t)ni) % (uint32_t)ni;
-                while (left < thr) {  // Lemire rejection: the round ends after this access
-                    extra++;
-                    m = (uint64_t)get_half(x, a, k + extra, kfill) * (uint32_t)ni;
-                    left = (uint32_t)m;
-                }
-            }
-            r = (uint32_t)(m >> 32);
-            if (extra) {
-                atomicMin(&x.MISC[0], t + 1);
+            lemire(x, a, kpos + pdr, kfill, (uint32_t)ni, r, extra);
+            if (extra) {  // a Lemire rejection: later draws sit `extra` halves later
                 atomicMin(&x.MISC[8], t + 1);
+                atomicAdd(&x.MISC[15], 1);
+                x.MISC[2] = extra;  // (read only when it is the round's one rejection)
             }
         }
         if (chg && pchg == XP_MAX_CHG) {  // change list full
@@ -702,6 +711,23 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             atomicMin(&x.MISC[9], t);
         }
         __syncthreads();
+        if (x.MISC[15] == 1) {
+            // the round's one rejection: the accesses after it redraw from
+            // their shifted stream positions instead of ending the round; a
+            // rejection among those redraws ends the round after it
+            const int j = x.MISC[8] - 1, ex = x.MISC[2];
+            if (t > j) {
+                pdr += ex;
+                if (dr) {
+                    lemire(x, a, kpos + pdr, kfill, (uint32_t)ni, r, extra);
+                    if (extra) atomicMin(&x.MISC[0], t + 1);
+                }
+            }
+            __syncthreads();
+        } else if (x.MISC[15] > 1) {  // several: the round ends after the first
+            if (t == 0) x.MISC[0] = min(x.MISC[0], x.MISC[8]);
+            __syncthreads();
+        }
         if (t == 0) {
             tn = clock64();
             prof[0] += tn - tc;  // A + B
@@ -903,8 +929,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             st_rounds++;
             if (E < n - pos && E < XT) {
                 if (E == lost) st_conv++;
-                else if (E == x.MISC[8]) st_rej++;
                 else if (E == x.MISC[9]) st_chg++;
+                else st_rej++;
             }
         }
         if (t == E && E < Epre)  // (atomic: other lanes OR their pend_cidx bits into the same words)
