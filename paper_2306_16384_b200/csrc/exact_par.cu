@@ -25,7 +25,9 @@
 // The kernel walks the batch in rounds of XT accesses, one per thread:
 //   A  classify, saturating prefix of the safe count, prefix of the draws
 //   B  Lemire-bounded draw per miss (numpy integers(n), buffered 32-bit
-//      halves); a rejection ends the round after that access
+//      halves); a rejection moves every later draw of the round by the
+//      halves it consumed: the first is absorbed (the later accesses redraw),
+//      a second ends the round after it
 //   C  the round's ADD lines join the bitmap and the prefix counts at once:
 //      T = start set + ADDs.  An access then sees T minus its "holes" -- the
 //      ADD lines of later accesses and the lines earlier MU accesses removed
