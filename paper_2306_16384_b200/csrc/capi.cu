@@ -272,8 +272,6 @@ int gids_create(const gids_config* cfg, const uint64_t eviction_rng[6], gids_han
         A(h->list_cnt_buf[b], 2);
     }
     A(h->sargs, 2);
-    A(h->flag_hit, h->serve_cap);
-    A(h->flag_host, h->serve_cap);
     A(h->log_line, h->serve_cap);
     A(h->log_pos, h->serve_cap);
     A(h->set_cnt, h->sets);
@@ -324,8 +322,8 @@ int gids_destroy(gids_handle* h) {
                     h->kind_buf[1], h->line_buf[1], h->ins_buf[1],            h->log_line,
                     h->log_pos,   h->set_cnt,  h->set_off,    h->set_cur,    h->bucket,
                     h->svc,       h->hit_list_buf[0], h->hit_list_buf[1], h->host_list_buf[0],
-                    h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1], h->flag_hit,
-                    h->flag_host, h->sel_tmp,      (void*)h->shard_ptrs, h->contrib_dev,
+                    h->host_list_buf[1], h->list_cnt_buf[0], h->list_cnt_buf[1],
+                    (void*)h->shard_ptrs, h->contrib_dev,
                     h->serve_parts, h->serve_word_parts, h->cand_of_slot, h->cand_slot,
                     h->xcls,      h->xp_halves, h->line_mark, h->shared_rows, h->sargs};
     for (void* p : ptrs)

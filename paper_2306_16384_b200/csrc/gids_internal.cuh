@@ -299,10 +299,6 @@ struct gids_handle {
     int32_t* hit_list_buf[2];   // [serve_cap]
     int2* host_list_buf[2];     // [serve_cap]
     int64_t* list_cnt_buf[2];   // [2] hits, host rows
-    uint8_t* flag_hit;          // [serve_cap] compaction flags (decide phase only)
-    uint8_t* flag_host;
-    void* sel_tmp;              // CUB select scratch (lazily sized for serve_cap)
-    size_t sel_tmp_bytes;
     int8_t* kind;          // current set (alias)
     int32_t* line;
     int32_t* ins;
@@ -434,7 +430,6 @@ int gids_scan_i32_to_i64(gids_handle* h, const int32_t* in, int64_t n, int64_t* 
 int gids_launch_sample(gids_handle* h, int64_t n_seeds, const uint64_t* rng_words, bool raw,
                        cudaStream_t st);
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st);
-int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st);
 int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, cudaStream_t st,
                        int64_t* sizes_host = nullptr);
 // exact_par.cu

@@ -547,10 +547,6 @@ int gids_launch_export(gids_handle* h, int64_t* edges_dev, int64_t* unique_dev, 
     return GIDS_OK;
 }
 
-int gids_launch_export_edges(gids_handle* h, int64_t* edges_dev, cudaStream_t st) {
-    return gids_launch_export(h, edges_dev, nullptr, st);
-}
-
 int gids_launch_export_unique(gids_handle* h, int64_t* unique_dev, cudaStream_t st) {
     return gids_launch_export(h, nullptr, unique_dev, st);
 }
