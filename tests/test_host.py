@@ -87,3 +87,57 @@ def test_data_parallel_split_partitions_the_batch_sequence():
     for r, part in enumerate(parts):
         assert all(np.array_equal(a, b) for a, b in zip(part, full[r::3]))
     assert sum(len(p) for p in parts) == len(full)
+
+
+def test_window_deferred_shift_folds_one_pop_then_one_push():
+    """WindowBuffer in the loader's deferred mode: one pop then one push are
+    handed to the serve (gids_serve_shift); any other sequence is launched in
+    order (a recording stand-in for the handle)."""
+    from paper_2306_16384_b200.feature_cache import WindowBuffer
+
+    class _H:
+        def __init__(self):
+            self.ops = []
+
+        def window_push(self, nodes, st):
+            self.ops.append(("push", nodes))
+
+        def window_pop(self, nodes, st):
+            self.ops.append(("pop", nodes))
+
+    class _T(list):  # a tensor stand-in: numel() and identity
+        def numel(self):
+            return len(self)
+
+    h = _H()
+    w = WindowBuffer(4, h, stream=0)
+    w.defer = True
+    a, b, c = _T([1, 2]), _T([3]), _T([4, 5])
+    w.push_iteration(a, trusted=True)
+    w.push_iteration(b, trusted=True)
+    assert w.take_shift() == (None, None) and h.ops == [("push", a), ("push", b)]
+    h.ops.clear()
+    assert w.pop_iteration() is a
+    w.push_iteration(c, trusted=True)
+    pop, push = w.take_shift()
+    assert pop is a and push is c and h.ops == []
+    assert w.pop_iteration() is b
+    assert w.take_shift() == (b, None) and h.ops == []
+    assert list(w.lists) == [c]
+
+
+def test_slots_hand_out_views_k_at_a_time():
+    """Per-batch blocks come K at a time from one allocation."""
+    import numpy as np
+
+    from paper_2306_16384_b200.loader import _Slots
+    allocs = []
+
+    def alloc():
+        allocs.append(np.zeros((3, 4)))
+        return allocs[-1]
+
+    s = _Slots(alloc, 3)
+    views = [s.take() for _ in range(7)]
+    assert len(allocs) == 3
+    assert all(v.base is allocs[i // 3] for i, v in enumerate(views))
