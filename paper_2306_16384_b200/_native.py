@@ -447,11 +447,14 @@ class Handle:
     def exact_par_stats(self) -> dict:
         out = np.zeros(16, np.int64)
         check(lib().gids_exact_par_stats(self.h, out.ctypes.data), "exact_par_stats")
-        return dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line",
-                         "cyc_draws", "cyc_tables", "cyc_first_select", "cyc_sort",
-                         "cyc_masks", "cyc_resolve", "cyc_lost_lines", "fixpoint_passes",
-                         "cyc_verify", "cyc_commit", "cyc_ring", "cyc_spare"),
-                        out.tolist()), batches=self.exact_par_batches())
+        d = dict(zip(("rounds", "ended_rejection", "ended_change_list", "ended_lost_line",
+                      "cyc_draws", "cyc_tables", "cyc_first_select", "cyc_sort",
+                      "cyc_masks", "cyc_resolve", "cyc_lost_lines", "fixpoint_passes",
+                      "cyc_verify", "cyc_commit", "cyc_ring", "cyc_spare"),
+                     out.tolist()), batches=self.exact_par_batches())
+        # (the per-phase cycle counters are compiled in only with -DGIDS_XP_PROF=1)
+        d["cycle_counters"] = any(v for k, v in d.items() if k.startswith("cyc_"))
+        return d
 
 
 def synthesize_rows(device: int, seed: int, row0: int, n: int, dim: int, dst, stream: int) -> None:

@@ -49,6 +49,20 @@
 // sequential warp (k_exact_seq) decides the batch instead.
 #include "gids_internal.cuh"
 
+// per-phase cycle counters of thread 0 (exact_par_stats): compiled in with
+// -DGIDS_XP_PROF=1 -- the clock reads sit on warp 0's path through every phase
+#ifndef GIDS_XP_PROF
+#define GIDS_XP_PROF 0
+#endif
+#define XP_MARK(i)                                \
+    do {                                          \
+        if (GIDS_XP_PROF && t == 0) {             \
+            const long long _n = clock64();       \
+            prof[i] += _n - tc;                   \
+            tc = _n;                              \
+        }                                         \
+    } while (0)
+
 namespace {
 
 constexpr int XT = 512;           // threads = accesses per round
@@ -554,14 +568,12 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
     int64_t hits = 0, misses = 0, byp = 0;
     int64_t st_rounds = 0, st_rej = 0, st_chg = 0, st_conv = 0;  // round ends (thread 0)
     long long prof[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // cycles per phase, passes (thread 0)
-    long long tc = clock64();
+    long long tc = GIDS_XP_PROF ? clock64() : 0;
 
     while (pos < n) {
         // (the ring entries this round reads were waited for before the last
         // round's closing barrier, which also ordered its commit)
-        long long tn = clock64();
-        prof[10] += tn - tc;  // (refill issue)
-        tc = tn;
+        XP_MARK(10);  // (refill issue)
         // ---------------- A: classify, saturating safe-count prefix, draw prefix
         const int32_t p = pos + t;
         const bool valid = p < n;
@@ -585,6 +597,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             x.MISC[7] = 0;   // unconverted candidates of the round
             x.MISC[8] = XT;  // first Lemire rejection (+1)
             x.MISC[15] = 0;  // Lemire rejections in the round
+            x.MISC[11] = 0;  // ADD changes (bits by change index, 11: 0-31, 12: 32-63)
+            x.MISC[12] = 0;
             x.MISC[9] = XT;  // end by a full change list
             x.MISC[14] = XT;  // first candidate whose line the previous round took (min)
         }
@@ -730,11 +744,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             if (t == 0) x.MISC[0] = min(x.MISC[0], x.MISC[8]);
             __syncthreads();
         }
-        if (t == 0) {
-            tn = clock64();
-            prof[0] += tn - tc;  // A + B
-            tc = tn;
-        }
+        XP_MARK(0);  // A + B
         const int Epre0 = x.MISC[0];
         const int Epre = (int)((n - pos) < Epre0 ? (n - pos) : Epre0);
         const bool in = t < Epre;
@@ -746,6 +756,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
             if (cls == C_ADD) {
                 x.CSLOT[pchg] = s;
                 atomicOr(&a.safe_bits[s >> 5], 1u << (s & 31));
+                atomicOr(reinterpret_cast<unsigned*>(&x.MISC[11 + (pchg >> 5)]), 1u << (pchg & 31));
             }
         }
         if (valid && in && cls == C_CAND && !conv) {
@@ -761,11 +772,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 if (x.CTYPE[e] > 0) t_update_warp(x, x.CSLOT[e], +1, lane);
         }
         __syncthreads();
-        if (t == 0) {
-            tn = clock64();
-            prof[1] += tn - tc;  // C: T tables
-            tc = tn;
-        }
+        XP_MARK(1);  // C: T tables
         const int nchg = x.MISC[3];
         const uint32_t total = x.SUPP[ns];
         Grp B;
@@ -783,11 +790,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                                                                   (float)(B.cnt ? B.cnt : 1u));
         }
         __syncthreads();
-        if (t == 0) {
-            tn = clock64();
-            prof[2] += tn - tc;  // C selects
-            tc = tn;
-        }
+        XP_MARK(2);  // C selects
         // ---------------- D/E: every eviction resolves against the change list.
         // The MU lines are themselves answers, so a pass uses the previous
         // pass's MU lines (the first pass: their no-hole lines); the result is
@@ -822,17 +825,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 x.MISC[10] = 0;
                 x.MISC[13] = 0;  // an MU moved across more than MOVSPAN buckets
             }
-            if (pass == 0 && wid == XW - 1) {  // ADD mask (CTYPE is fixed for the round)
-                const unsigned a0 = __ballot_sync(0xffffffffu, lane < nchg && x.CTYPE[lane] > 0);
-                const unsigned a1 =
-                    __ballot_sync(0xffffffffu, lane + 32 < nchg && x.CTYPE[lane + 32] > 0);
-                if (lane == 0) {
-                    x.MISC[11] = (int32_t)a0;
-                    x.MISC[12] = (int32_t)a1;
-                }
-            }
             __syncthreads();
-            if (t == 0) { tn = clock64(); prof[3] += tn - tc; tc = tn; }  // sort
+            XP_MARK(3);  // sort
             // PM[k] = change indices of the k lowest lines: thread (k, half)
             // builds one 32-bit half from the ranks (no serial scan)
             if (t < 2 * (nchg + 1)) {
@@ -850,7 +844,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 for (int b = lo; b <= hi; b++) x.CUMB[b] = j;
             }
             __syncthreads();
-            if (t == 0) { tn = clock64(); prof[4] += tn - tc; tc = tn; }  // resolve
+            XP_MARK(4);  // resolve
             const unsigned long long addm =
                 (unsigned long long)(uint32_t)x.MISC[11] |
                 ((unsigned long long)(uint32_t)x.MISC[12] << 32);
@@ -873,7 +867,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
                 }
             }
             __syncthreads();
-            if (t == 0) { tn = clock64(); prof[5] += tn - tc; tc = tn; }  // verify
+            XP_MARK(5);  // verify
             if (t == 0) prof[7]++;
             // the earlier MU lines this access counted, used vs found: only
             // those whose move crossed a bucket of the lines it looked at
@@ -924,10 +918,8 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         const int32_t pans = (sel && in) ? cur : -1;  // this thread's answer, for the next round's F
         const int lost = x.MISC[1] < x.MISC[14] ? x.MISC[1] : x.MISC[14];
         const int E = Epre < lost ? Epre : lost;
+        XP_MARK(8);  // check + F
         if (t == 0) {
-            tn = clock64();
-            prof[8] += tn - tc;  // check + F
-            tc = tn;
             st_rounds++;
             if (E < n - pos && E < XT) {
                 if (E == lost) st_conv++;
@@ -985,11 +977,7 @@ __global__ void __launch_bounds__(XT, 1) k_exact_par(XpArgs a) {
         // wait of RING_LAG after it), for every thread after the barrier
         asm volatile("cp.async.wait_group %0;" ::"n"(RING_LAG - 1));
         __syncthreads();
-        if (t == 0) {
-            tn = clock64();
-            prof[9] += tn - tc;  // G commit (+ ring wait)
-            tc = tn;
-        }
+        XP_MARK(9);  // G commit (+ ring wait)
         if (E > 0) {
             nsafe = x.MISC[4];
             kpos += x.MISC[5];
